@@ -1,0 +1,260 @@
+/*
+ * lbp_oracle.c -- CPU ORACLE for the fused-depth LBP descriptor + linear SVM
+ * hot path of arXiv 1504.01883 (Naik & Rathna).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py (cpu_baseline leg and --impl reference) may load this library.
+ * The product path (paper_1504_01883_b200/) never links, imports or calls it,
+ * and this file shares no code, header, table or constant generator with it.
+ *
+ * Plain, slow, obviously-correct, single-threaded C99.  No SIMD intrinsics,
+ * no blocking, no reordering beyond what the definitions below state.
+ * Citations: "P:L" = line L of PAPER.md (the paper text), "S:L" = line L of
+ * SPEC.md, "§8c" = SURVEY.md section 8(c) (the readings of the paper that this
+ * build takes; each reading is also listed in DESIGN.md §3).
+ *
+ * Every function here is pinned by tests/test_oracle.py against values the
+ * paper prints (Fig. 7), closed forms, invariants and brute force; see the
+ * header comment of each function for the pins that cover it.
+ */
+#include <stdint.h>
+#include <stddef.h>
+#include <string.h>
+#include <math.h>
+
+/* Status codes: the contract of SURVEY §8(b), restated (not shared) here. */
+#define ORC_OK 0
+#define ORC_E_ARG (-1)
+#define ORC_E_ROI (-2)
+#define ORC_E_GRID (-3)
+#define ORC_E_OVERFLOW (-4)
+
+/* ------------------------------------------------------------------------ */
+/* Eq. 2 with the Fig. 7 weights.                   */
+/*                                                                          */
+/*   LBP(x_c, y_c) = sum_{p=0}^{7} S(g_p - g_c) * 2^p                       */
+/*                                                                          */
+/* S(x) = 1 iff x >= 0 (Fig. 7: neighbour 6 vs centre 6 thresholds to 1).   */
+/* The sampling points p = 0..7 carry the Fig. 7 weights matrix             */
+/*       [[  1,  2,  4],                                                    */
+/*        [128,  .,  8],                                                    */
+/*        [ 64, 32, 16]]                                                    */
+/* i.e. p=0 top-left, 1 top, 2 top-right, 3 right, 4 bottom-right,          */
+/* 5 bottom, 6 bottom-left, 7 left.                                         */
+/* ------------------------------------------------------------------------ */
+
+/* (row offset, column offset) of sampling point p, read off Fig. 7. */
+static const int ORC_DY[8] = {-1, -1, -1, 0, 1, 1, 1, 0};
+static const int ORC_DX[8] = {-1, 0, 1, 1, 1, 0, -1, -1};
+
+static int orc_S(int64_t x) { return x >= 0 ? 1 : 0; }
+
+/* window: 3x3 samples, row-major (window[r*3+c]); any unsigned width. */
+int32_t oracle_lbp_code_window(const uint32_t window[9])
+{
+    int64_t gc = window[4];
+    int32_t code = 0;
+    for (int p = 0; p < 8; ++p) {
+        int64_t gp = window[(1 + ORC_DY[p]) * 3 + (1 + ORC_DX[p])];
+        code += orc_S(gp - gc) * (1 << p);
+    }
+    return code;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Uniform-pattern bin map (J.north_star "uniform-pattern histograms",      */
+/* SURVEY §8c step 6).  A code is uniform iff its circular bit string       */
+/* (p = 0..7, p=7 adjacent to p=0 -- the Fig. 7 positions go round the      */
+/* centre) has at most 2 transitions 0<->1.  Uniform codes, in ascending    */
+/* code order, get bins 0..57; every other code gets bin 58.                */
+/* Returns the number of uniform codes (58).                                */
+/* ------------------------------------------------------------------------ */
+int32_t oracle_uniform_table(uint8_t table[256])
+{
+    int next = 0;
+    for (int code = 0; code < 256; ++code) {
+        int transitions = 0;
+        for (int p = 0; p < 8; ++p) {
+            int bit_p = (code >> p) & 1;
+            int bit_next = (code >> ((p + 1) % 8)) & 1;
+            if (bit_p != bit_next) transitions += 1;
+        }
+        table[code] = (transitions <= 2) ? (uint8_t)next++ : 0xFF;
+    }
+    for (int code = 0; code < 256; ++code)
+        if (table[code] == 0xFF) table[code] = (uint8_t)next;
+    return next; /* = number of uniform codes; bins = next + 1 */
+}
+
+/* Code map of an 8-bit image: out[i*(w-2)+j] = LBP at image pixel (i+1,j+1).
+ * The 1-px border has no code.  Returns ORC_E_ROI if w<3 or h<3. */
+int32_t oracle_lbp_map_u8(const uint8_t* img, int32_t h, int32_t w, int64_t pitch, uint8_t* out)
+{
+    if (!img || !out) return ORC_E_ARG;
+    if (w < 3 || h < 3) return ORC_E_ROI;
+    for (int32_t i = 0; i < h - 2; ++i)
+        for (int32_t j = 0; j < w - 2; ++j) {
+            uint32_t win[9];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c)
+                    win[r * 3 + c] = img[(int64_t)(i + r) * pitch + (j + c)];
+            out[(int64_t)i * (w - 2) + j] = (uint8_t)oracle_lbp_code_window(win);
+        }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Fused-depth descriptor, per ROI n:                 */
+/*  1. r = clamp(roi, image); empty / r.w<3 / r.h<3 -> ORC_E_ROI     */
+/*     (S:86), zero row.                                             */
+/*  2. interior W' = r.w-2, H' = r.h-2; code-map pixel (i,j) is image pixel */
+/*     (r.y+1+i, r.x+1+j).  cells_x > W' or cells_y > H' ->         */
+/*     ORC_E_GRID.  Largest cell area > 65535 -> ORC_E_OVERFLOW.    */
+/*  3. cell b spans [floor(b*W'/K), floor((b+1)*W'/K)), row-major   */
+/*     concatenation of the cells (Eq. 3: K sub-histograms).     */
+/*  4. valid = (depth == NULL) or (d != 0 and dmin <= d <= dmax), d = depth */
+/*     at the CENTRE pixel (P:49-63 mask; S:37 0 = no reading).             */
+/*  5. code = Eq. 2 above on the grey 3x3 neighbourhood.            */
+/*  6. bin = code (bins = 256, "ranging from 0 to 255") or           */
+/*     U[code] (bins = 59, uniform patterns, J.north_star).                 */
+/*  7. hist[(cy*Kx+cx)*bins + bin] += 1 (Eq. 3, f = indicator).             */
+/* ------------------------------------------------------------------------ */
+int32_t oracle_lbp_extract(const uint8_t* grey, const uint16_t* depth,
+                           int32_t n_images, int32_t height, int32_t width,
+                           int64_t grey_pitch, int64_t depth_pitch,
+                           int64_t grey_img_stride, int64_t depth_img_stride,
+                           const int32_t* rois /* [n_rois][5] = img,x,y,w,h */, int32_t n_rois,
+                           uint16_t dmin, uint16_t dmax,
+                           int32_t cells_x, int32_t cells_y, int32_t bins,
+                           uint16_t* desc /* [n_rois][cells_y*cells_x*bins] */,
+                           int32_t* roi_status /* nullable [n_rois] */)
+{
+    if (n_rois < 0) return ORC_E_ARG;
+    if (n_rois == 0) return ORC_OK;
+    if (!grey || !rois || !desc) return ORC_E_ARG;
+    if (bins != 59 && bins != 256) return ORC_E_ARG;
+    if (cells_x < 1 || cells_y < 1) return ORC_E_ARG;
+    if (dmin > dmax) return ORC_E_ARG;
+    if (n_images < 1 || height < 1 || width < 1) return ORC_E_ARG;
+    if (grey_pitch < width || grey_img_stride < grey_pitch * (height - 1) + width) return ORC_E_ARG;
+    if (depth && (depth_pitch < width || depth_img_stride < depth_pitch * (height - 1) + width))
+        return ORC_E_ARG;
+    int64_t dim = (int64_t)cells_x * cells_y * bins;
+    if (dim > 0x7FFFFFFF) return ORC_E_ARG;
+
+    uint8_t U[256];
+    oracle_uniform_table(U);
+
+    for (int32_t n = 0; n < n_rois; ++n) {
+        uint16_t* h = desc + (int64_t)n * dim;
+        for (int64_t d = 0; d < dim; ++d) h[d] = 0;
+        int32_t status = ORC_OK;
+
+        const int32_t* roi = rois + (int64_t)n * 5;
+        int64_t img = roi[0];
+        /* step 1: clamp to [0,W) x [0,H) */
+        int64_t x0 = roi[1], y0 = roi[2];
+        int64_t x1 = x0 + roi[3], y1 = y0 + roi[4];
+        if (x0 < 0) x0 = 0;
+        if (y0 < 0) y0 = 0;
+        if (x1 > width) x1 = width;
+        if (y1 > height) y1 = height;
+        int64_t rw = x1 - x0, rh = y1 - y0;
+        if (img < 0 || img >= n_images || rw < 3 || rh < 3) status = ORC_E_ROI;
+
+        /* step 2 */
+        int64_t Wi = rw - 2, Hi = rh - 2;
+        if (status == ORC_OK && (cells_x > Wi || cells_y > Hi)) status = ORC_E_GRID;
+        if (status == ORC_OK) {
+            int64_t maxw = 0, maxh = 0;
+            for (int32_t b = 0; b < cells_x; ++b) {
+                int64_t cw = ((int64_t)(b + 1) * Wi) / cells_x - ((int64_t)b * Wi) / cells_x;
+                if (cw > maxw) maxw = cw;
+            }
+            for (int32_t b = 0; b < cells_y; ++b) {
+                int64_t ch = ((int64_t)(b + 1) * Hi) / cells_y - ((int64_t)b * Hi) / cells_y;
+                if (ch > maxh) maxh = ch;
+            }
+            if (maxw * maxh > 65535) status = ORC_E_OVERFLOW;
+        }
+        if (roi_status) roi_status[n] = status;
+        if (status != ORC_OK) continue;
+
+        const uint8_t* G = grey + img * grey_img_stride;
+        const uint16_t* D = depth ? depth + img * depth_img_stride : NULL;
+
+        /* step 3: loop over blocks with their floor ranges */
+        for (int32_t cy = 0; cy < cells_y; ++cy) {
+            int64_t i_begin = ((int64_t)cy * Hi) / cells_y;
+            int64_t i_end = ((int64_t)(cy + 1) * Hi) / cells_y;
+            for (int32_t cx = 0; cx < cells_x; ++cx) {
+                int64_t j_begin = ((int64_t)cx * Wi) / cells_x;
+                int64_t j_end = ((int64_t)(cx + 1) * Wi) / cells_x;
+                uint32_t count[256];
+                for (int b = 0; b < 256; ++b) count[b] = 0;
+                for (int64_t i = i_begin; i < i_end; ++i)
+                    for (int64_t j = j_begin; j < j_end; ++j) {
+                        int64_t yy = y0 + 1 + i, xx = x0 + 1 + j; /* image pixel */
+                        /* step 4: depth window at the centre pixel */
+                        int valid = 1;
+                        if (D) {
+                            uint16_t d = D[yy * depth_pitch + xx];
+                            valid = (d != 0) && (d >= dmin) && (d <= dmax);
+                        }
+                        if (!valid) continue;
+                        /* step 5: Eq. 2 */
+                        uint32_t win[9];
+                        for (int r = 0; r < 3; ++r)
+                            for (int c = 0; c < 3; ++c)
+                                win[r * 3 + c] = G[(yy - 1 + r) * grey_pitch + (xx - 1 + c)];
+                        int32_t code = oracle_lbp_code_window(win);
+                        /* step 6 */
+                        int32_t bin = (bins == 256) ? code : U[code];
+                        /* step 7 */
+                        count[bin] += 1;
+                    }
+                for (int32_t b = 0; b < bins; ++b)
+                    h[((int64_t)cy * cells_x + cx) * bins + b] = (uint16_t)count[b];
+            }
+        }
+    }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Linear one-vs-rest SVM decision ("a classifier defined by a    */
+/* hyperplane"; S:467-475 predict):                      */
+/*   s[n][c] = (float)( (double)b[c] + sum_{d ascending} (double)W[c][d] *  */
+/*                                                      (double)h[n][d] )   */
+/* rounded once to nearest-even fp32; label = argmax_c s over the fp32      */
+/* values, ties -> smallest c; top < reject_threshold -> -1. */
+/* ------------------------------------------------------------------------ */
+int32_t oracle_svm_score(const uint16_t* desc, int32_t n, int32_t dim,
+                         const float* W /* [C][dim] */, const float* bias /* [C] */,
+                         int32_t n_classes,
+                         float* scores /* nullable [n][C] */, int32_t* labels /* nullable [n] */,
+                         float* top_score /* nullable [n] */, float reject_threshold)
+{
+    if (n < 0 || dim < 1 || n_classes < 1) return ORC_E_ARG;
+    if (n == 0) return ORC_OK;
+    if (!desc || !W || !bias) return ORC_E_ARG;
+    for (int32_t i = 0; i < n; ++i) {
+        const uint16_t* h = desc + (int64_t)i * dim;
+        float best = 0.0f;
+        int32_t best_c = 0;
+        for (int32_t c = 0; c < n_classes; ++c) {
+            const float* w = W + (int64_t)c * dim;
+            double acc = (double)bias[c];
+            for (int32_t d = 0; d < dim; ++d) acc += (double)w[d] * (double)h[d];
+            float s = (float)acc;
+            if (scores) scores[(int64_t)i * n_classes + c] = s;
+            if (c == 0 || s > best) {
+                best = s;
+                best_c = c;
+            }
+        }
+        if (top_score) top_score[i] = best;
+        if (labels) labels[i] = (best < reject_threshold) ? -1 : best_c;
+    }
+    return ORC_OK;
+}

@@ -1,0 +1,148 @@
+"""Seeded synthetic Kinect-shaped inputs (grey u8 + depth u16 face crops, SVM weights).
+
+This module is the ONLY code shared by the oracle side (tests / bench cpu leg)
+and the CUDA side.  It holds none of the method's arithmetic (no LBP codes, no
+histograms, no SVM scores): it only draws inputs.  The recipe is DESIGN.md §4.
+
+Every sample is a pure function of (seed, global crop index, y, x) through a
+counter-based integer hash, so crop i is bit-identical whichever rank or batch
+produces it.  ``synthgen/synth_gen.cu`` implements the same integer recipe on
+the GPU for large batches; tests/test_synth_gpu.py checks the two bit-exactly.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+DIST_FACE, DIST_CONSTANT, DIST_NOISE = 0, 1, 2
+DISTS = {"face": DIST_FACE, "constant": DIST_CONSTANT, "noise": DIST_NOISE}
+
+# default depth window (mm) of the synthetic workload: face at ~1 m
+DMIN, DMAX = 600, 1400
+
+_M1 = np.uint32(0x7FEB352D)
+_M2 = np.uint32(0x846CA68B)
+_GOLD = np.uint32(0x9E3779B9)
+
+
+def _lowbias32(x):
+    x = x.astype(np.uint32, copy=True)
+    x ^= x >> np.uint32(16)
+    x *= _M1
+    x ^= x >> np.uint32(15)
+    x *= _M2
+    x ^= x >> np.uint32(16)
+    return x
+
+
+def hash5(seed, n, a, b, salt):
+    """32-bit counter hash of (seed, crop index n, a, b, salt); numpy broadcasting."""
+    with np.errstate(over="ignore"):
+        h = _lowbias32(np.asarray(np.uint32(seed) + _GOLD * np.uint32(salt), dtype=np.uint32))
+        h = _lowbias32(h ^ np.asarray(n, dtype=np.uint64).astype(np.uint32))
+        h = _lowbias32(h ^ np.asarray(a, dtype=np.int64).astype(np.uint32))
+        h = _lowbias32(h ^ np.asarray(b, dtype=np.int64).astype(np.uint32))
+    return h
+
+
+def _value_noise(seed, n, y, x, shift, mask, salt):
+    """Integer bilinear value noise on a 2^shift lattice; returns int64 in [0, mask]."""
+    cell = 1 << shift
+    Y, X = y >> shift, x >> shift
+    fy, fx = y & (cell - 1), x & (cell - 1)
+    v00 = (hash5(seed, n, Y, X, salt) & mask).astype(np.int64)
+    v01 = (hash5(seed, n, Y, X + 1, salt) & mask).astype(np.int64)
+    v10 = (hash5(seed, n, Y + 1, X, salt) & mask).astype(np.int64)
+    v11 = (hash5(seed, n, Y + 1, X + 1, salt) & mask).astype(np.int64)
+    acc = (v00 * (cell - fx) * (cell - fy) + v01 * fx * (cell - fy)
+           + v10 * (cell - fx) * fy + v11 * fx * fy)
+    return acc >> (2 * shift)
+
+
+def _crop_chunk(seed, idx, H, W, dist):
+    n = idx[:, None, None].astype(np.int64)
+    y = np.arange(H, dtype=np.int64)[None, :, None]
+    x = np.arange(W, dtype=np.int64)[None, None, :]
+    shape = (idx.shape[0], H, W)
+    if dist == DIST_CONSTANT:
+        return np.full(shape, 128, np.uint8), np.full(shape, 1000, np.uint16)
+    if dist == DIST_NOISE:
+        g = (hash5(seed, n, y, x, 8) & 255).astype(np.uint8)
+        return np.broadcast_to(g, shape).copy(), np.full(shape, 1000, np.uint16)
+    # --- face-like grey: 2-octave value noise, quantised to steps of 4 ---
+    v16 = _value_noise(seed, n, y, x, 4, 255, 1)
+    v4 = _value_noise(seed, n, y, x, 2, 63, 2)
+    base = 60 + (hash5(seed, n, 0, 0, 3) % 141).astype(np.int64)
+    g = base + (((v16 - 128) * 3) >> 2) + (v4 - 32)
+    g = (np.clip(g, 0, 255) & ~3).astype(np.uint8)
+    g = np.broadcast_to(g, shape)
+    # --- depth: background plane + face ellipse with nose relief + shadow holes ---
+    bg = 2000 + (hash5(seed, n, 0, 0, 4) % 1001).astype(np.int64)
+    cx = W // 2 + (hash5(seed, n, 0, 0, 5) % (W // 8 + 1)).astype(np.int64) - W // 16
+    cy = H // 2 + (hash5(seed, n, 0, 0, 9) % (H // 8 + 1)).astype(np.int64) - H // 16
+    a = (W * 36) // 100
+    b = (H * 43) // 100
+    a2, b2 = a * a, b * b
+    R = a2 * b2
+    fd = 900 + (hash5(seed, n, 0, 0, 6) % 201).astype(np.int64)
+    dx, dy = x - cx, y - cy
+    e = dx * dx * b2 + dy * dy * a2
+    rn = max(W // 8, 1)
+    r2 = dx * dx + dy * dy
+    relief = np.where(r2 < rn * rn, 40 - (40 * r2) // (rn * rn), 0)
+    d = np.where(e <= R, fd - relief, bg)
+    by, bx = y // 3, x // 3
+    ecx, ecy = 3 * bx + 1 - cx, 3 * by + 1 - cy
+    ec = ecx * ecx * b2 + ecy * ecy * a2
+    near = np.abs(ec - R) * 100 < 15 * R
+    p = np.where(near, 200, 10)
+    hole = (hash5(seed, n, by, bx, 7) % 1000).astype(np.int64) < p
+    d = np.where(hole, 0, d)
+    return g.copy(), np.broadcast_to(d, shape).astype(np.uint16)
+
+
+def face_crops(n: int, H: int, W: int, seed: int = 42, first_index: int = 0,
+               dist: str | int = "face", chunk: int = 256):
+    """Crops [n][H][W] grey u8 and depth u16 for global crop indices first_index..+n."""
+    dist = DISTS[dist] if isinstance(dist, str) else int(dist)
+    grey = np.empty((n, H, W), np.uint8)
+    depth = np.empty((n, H, W), np.uint16)
+    for s in range(0, n, chunk):
+        idx = np.arange(first_index + s, first_index + min(n, s + chunk), dtype=np.int64)
+        g, d = _crop_chunk(seed, idx, H, W, dist)
+        grey[s:s + len(idx)] = g
+        depth[s:s + len(idx)] = d
+    return grey, depth
+
+
+def full_rois(n: int, H: int, W: int) -> np.ndarray:
+    """One ROI per image covering the whole crop: (img, 0, 0, W, H)."""
+    r = np.zeros((n, 5), np.int32)
+    r[:, 0] = np.arange(n)
+    r[:, 3] = W
+    r[:, 4] = H
+    return r
+
+
+def svm_weights(n_classes: int, dim: int, seed: int = 42, sigma: float = 2.0 ** -4):
+    """W ~ N(0, sigma^2) fp32 [C][dim], b ~ N(0, 1) fp32 [C]; seeded, rank-independent."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0x5F3]))
+    W = (rng.standard_normal((n_classes, dim)) * sigma).astype(np.float32)
+    b = rng.standard_normal(n_classes).astype(np.float32)
+    return W, b
+
+
+def random_rois(n: int, n_images: int, H: int, W: int, seed: int, min_size: int = 3,
+                max_size: int | None = None, allow_outside: bool = True) -> np.ndarray:
+    """Random ROI rects; with allow_outside they may stick out of the image (clamp tests)."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0x201]))
+    max_size = max_size or max(H, W)
+    w = rng.integers(min_size, max_size + 1, n)
+    h = rng.integers(min_size, max_size + 1, n)
+    if allow_outside:
+        x = rng.integers(-4, W, n)
+        y = rng.integers(-4, H, n)
+    else:
+        w, h = np.minimum(w, W), np.minimum(h, H)
+        x = (rng.random(n) * (W - w + 1)).astype(np.int64)
+        y = (rng.random(n) * (H - h + 1)).astype(np.int64)
+    return np.stack([rng.integers(0, n_images, n), x, y, w, h], axis=1).astype(np.int32)
