@@ -1,0 +1,460 @@
+#!/usr/bin/env python
+"""Benchmark of the fused-depth LBP descriptor + linear-SVM hot path (arXiv 1504.01883).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lbpfused|reference]
+
+One step = the whole hot path (depth mask, LBP codes,
+uniform bins, cell histograms, u16 descriptor, linear OvR SVM scores + labels)
+over one batch of synthetic crops already resident in HBM.  The default
+workload is BASELINE.json configs[2] ("config3"): 16,384 face crops of 128x128
+grey u8 + depth u16 per GPU, 8x8 cells x 59 uniform bins, 100-identity SVM.
+Multi-GPU (torchrun): every rank owns its own 16,384 crops (weak scaling, no
+data-path collective); time = max over ranks.  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, plain single-threaded C, run on
+T host threads over disjoint shards) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import platform
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "face crops/sec (LBP+hist+SVM) at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+UNIT = "crops/s"
+
+WORKLOADS = {
+    # name: (crops per GPU, H, W, cells_x, cells_y, bins, classes, description)
+    "config3": (16384, 128, 128, 8, 8, 59, 100,
+                "BASELINE configs[2]: 16384 x 128x128 grey+depth crops with depth masks, "
+                "8x8 cells x 59 uniform bins, 100-identity one-vs-all linear SVM"),
+    "config4": (131072, 128, 128, 8, 8, 59, 1000,
+                "BASELINE configs[3] shard: 131072 x 128x128 crops per GPU (2^20 over 8 GPUs), "
+                "1000-identity SVM"),
+    "config1": (1, 64, 64, 8, 8, 59, 2,
+                "BASELINE configs[0]: single 64x64 grey+depth crop, 8x8x59, 2-class SVM"),
+}
+DMIN, DMAX = 600, 1400
+
+
+def bytes_per_crop(H, W, cx, cy, bins):
+    """Algorithmic HBM bytes of the extraction kernel per crop:
+    grey u8 + depth u16 read once, u16 descriptor written once."""
+    return H * W * (1 + 2) + cx * cy * bins * 2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="lbpfused", choices=["lbpfused", "reference"])
+    p.add_argument("--workload", default="config3", choices=sorted(WORKLOADS))
+    p.add_argument("--crops", type=int, default=0, help="override crops per GPU")
+    p.add_argument("--dist", default="face", choices=["face", "constant", "noise"])
+    p.add_argument("--no-depth", action="store_true")
+    p.add_argument("--bins", type=int, default=0)
+    p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 10)")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    p.add_argument("--skip-cpu", action="store_true")
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks (NVML)
+
+class ClockSampler:
+    """Polls SM clock and throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML on this host
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        busy = [s for s in self.samples]
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(busy)}
+
+
+# --------------------------------------------------------------------------- CPU oracle
+
+def oracle_rate(grey, depth, rois, W, b, cx, cy, bins, budget_s, threads):
+    """Times the UNMODIFIED oracle (extraction + SVM) on T threads over disjoint shards.
+
+    Returns (crops/s, crops processed, seconds, descriptors, labels) for the sample."""
+    import oracle
+    n = grey.shape[0]
+    # calibrate on a few crops single-threaded
+    k = min(n, 8)
+    t0 = time.perf_counter()
+    d = oracle.lbp_extract(grey[:k], depth[:k] if depth is not None else None,
+                           _local_rois(rois[:k]), DMIN, DMAX, cx, cy, bins)
+    oracle.svm_score(d, W, b)
+    per_crop = (time.perf_counter() - t0) / k
+    m = int(max(threads, min(n, budget_s * threads / max(per_crop, 1e-9))))
+    m = min(m, n)
+    shards = np.array_split(np.arange(m), threads)
+    out_desc = [None] * threads
+    out_lab = [None] * threads
+
+    def work(i):
+        idx = shards[i]
+        if idx.size == 0:
+            return
+        dd = oracle.lbp_extract(grey[idx], depth[idx] if depth is not None else None,
+                                _local_rois(rois[idx]), DMIN, DMAX, cx, cy, bins)
+        _, lab, _ = oracle.svm_score(dd, W, b)
+        out_desc[i], out_lab[i] = dd, lab
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    dt = time.perf_counter() - t0
+    desc = np.concatenate([x for x in out_desc if x is not None])
+    lab = np.concatenate([x for x in out_lab if x is not None])
+    return m / dt, m, dt, desc, lab
+
+
+def _local_rois(rois):
+    r = np.array(rois, np.int32, copy=True)
+    r[:, 0] = np.arange(r.shape[0])
+    return r
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor()
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import synthgen
+    n_gpu_crops, H, Wd, cx, cy, bins, C, desc_txt = WORKLOADS[args.workload]
+    bins = args.bins or bins
+    threads = len(os.sched_getaffinity(0))
+    per_step = max(threads, 4 * threads)
+    total = per_step * (args.steps + args.warmup)
+    grey, depth = synthgen.face_crops(per_step, H, Wd, seed=args.seed, dist=args.dist)
+    if args.no_depth:
+        depth = None
+    rois = synthgen.full_rois(per_step, H, Wd)
+    W, b = synthgen.svm_weights(C, cx * cy * bins, seed=args.seed)
+    import oracle
+    shards = np.array_split(np.arange(per_step), threads)
+
+    def step():
+        def work(idx):
+            d = oracle.lbp_extract(grey[idx], None if depth is None else depth[idx],
+                                   _local_rois(rois[idx]), DMIN, DMAX, cx, cy, bins)
+            oracle.svm_score(d, W, b)
+        ts = [threading.Thread(target=work, args=(s,)) for s in shards if s.size]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    sample = (f"{per_step} crops per step ({desc_txt.split(':')[0]} crop shape), "
+              f"{threads} threads x unmodified single-threaded oracle on disjoint shards")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": workload_config(args, n_gpu_crops, H, Wd, cx, cy, bins, C, desc_txt),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, n, H, W, cx, cy, bins, C, desc_txt):
+    return {"workload": f"{args.workload}: {desc_txt}", "crops_per_gpu": n, "crop": f"{H}x{W}",
+            "cells": f"{cx}x{cy}", "bins": bins, "classes": C, "dist": args.dist,
+            "depth_mask": not args.no_depth, "depth_window_mm": [DMIN, DMAX],
+            "parallelism": f"crop-sharded dp{args.gpus}",
+            "l2": "inputs larger than L2 (no flush needed)" if n * H * W * 3 > 126e6 else
+                  "inputs L2-resident (latency config)"}
+
+
+# --------------------------------------------------------------------------- own arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1504_01883_b200 as lb
+    import synthgen
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, H, Wd, cx, cy, bins, C, desc_txt = WORKLOADS[args.workload]
+    n = args.crops or n
+    bins = args.bins or bins
+    dim = cx * cy * bins
+    first = rank * n  # global crop indices of this rank: [rank*n, (rank+1)*n)
+
+    grey, depth = synthgen.gpu_face_crops(n, H, Wd, seed=args.seed, first_index=first,
+                                          dist=args.dist, device=dev)
+    if args.no_depth:
+        depth = None
+    rois = torch.from_numpy(synthgen.full_rois(n, H, Wd)).to(dev)
+    W_np, b_np = synthgen.svm_weights(C, dim, seed=args.seed)
+    W = torch.from_numpy(W_np).to(dev)
+    b = torch.from_numpy(b_np).to(dev)
+    prepared = lb.svm_prepare(W)
+    desc = torch.empty((n, dim), dtype=torch.uint16, device=dev)
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    top = torch.empty(n, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        lb.lbp_fused_extract(grey, depth, rois, DMIN, DMAX, cx, cy, bins, out=desc, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        lb.svm_score(desc, W, b, prepared=prepared, want_scores=False, labels=labels,
+                     top_score=top, stream=stream)
+
+    launches_per_step = 2
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, barrier + sync on both sides, events on the launching stream
+    ev_ext = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(ev_ext[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    ext_ms = sum(a.elapsed_time(b_) for a, b_ in ev_ext) / args.steps
+    t = torch.tensor([ms, ext_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, ext_ms = float(t[0]), float(t[1])
+    ms_per_step = ms / args.steps
+    value = n * world / (ms_per_step * 1e-3)
+
+    # ---- end to end through the public C ABI from pinned HOST buffers
+    e2e = run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins, W, b,
+                  prepared, n)
+
+    # ---- roofline of the dominant kernel (lbp_hist): algorithmic bytes / avg launch time
+    peaks = load_peaks()
+    bpc = bytes_per_crop(H, Wd, cx, cy, bins) if depth is not None else H * Wd + dim * 2
+    achieved = bpc * n / (ext_ms * 1e-3) / 1e9
+    peak, peak_src = peaks
+    roofline = {"bound": "hbm", "kernel": "lbp_hist (extraction)", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
+                "peak_source": peak_src, "bytes_per_crop": bpc,
+                "kernel_ms": ext_ms, "kernel_share_of_step": ext_ms / ms_per_step,
+                "traffic": load_traffic(args.workload)}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only) + equivalence gate on its sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        cpu, gate_ok = run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np,
+                                   cx, cy, bins)
+        if not gate_ok:
+            print(json.dumps({"error": "equivalence gate failed: GPU != oracle on the sample"}),
+                  flush=True)
+            return 3
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": workload_config(args, n, H, Wd, cx, cy, bins, C, desc_txt),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins, W, b, prepared, n):
+    """Same metric through lbp_recognize_host: H2D of the step's inputs from pinned host memory,
+    extraction + SVM, D2H of labels and top scores, every step."""
+    import synthgen
+    steps = args.e2e_steps or min(args.steps, 10)
+    g_h = grey.cpu().pin_memory()
+    d_h = depth.cpu().pin_memory() if depth is not None else None
+    r_h = torch.from_numpy(synthgen.full_rois(n, H, Wd)).pin_memory()
+    lab_h = torch.empty(n, dtype=torch.int32).pin_memory()
+    top_h = torch.empty(n, dtype=torch.float32).pin_memory()
+    geom = lb.images_geometry(g_h, d_h)
+    ws = torch.empty(lb.lbp_recognize_workspace_bytes(geom, d_h is not None, n, cx, cy, bins),
+                     dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        lb.lbp_recognize_host(g_h, d_h, r_h, DMIN, DMAX, cx, cy, bins, W, b, prepared, ws, lab_h,
+                              top_h, stream=stream)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    z.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(z) / steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    h2d = g_h.numel() + (d_h.numel() * 2 if d_h is not None else 0) + r_h.numel() * 4
+    return {"value": n * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(n * 8),
+            "api": "lbp_recognize_host (C ABI, pinned host buffers)"}
+
+
+def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins):
+    """Oracle timed on this host's cores on a bounded sample; the sample's oracle output is
+    also the equivalence gate (descriptors bit-exact, labels equal away from ties)."""
+    threads = len(os.sched_getaffinity(0))
+    n = grey.shape[0]
+    m = min(n, 4096)
+    g = grey[:m].cpu().numpy()
+    d = depth[:m].cpu().view(torch.int16).numpy().view(np.uint16) if depth is not None else None
+    r = rois[:m].cpu().numpy()
+    rate, done, secs, odesc, olab = oracle_rate(g, d, r, W_np, b_np, cx, cy, bins,
+                                                args.cpu_seconds, threads)
+    gdesc = desc[:done].cpu().view(torch.int16).numpy().view(np.uint16)
+    glab = labels[:done].cpu().numpy()
+    ok = bool(np.array_equal(gdesc, odesc))
+    if ok:
+        import oracle
+        s_ref, _, _ = oracle.svm_score(odesc, W_np, b_np)
+        srt = np.sort(s_ref, axis=1)
+        clear = (srt[:, -1] - srt[:, -2]) > 1e-4 * np.maximum(np.abs(srt[:, -1]), 1e-3)
+        ok = bool(np.array_equal(glab[clear], olab[clear]))
+    cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+           "sample": f"first {done} crops of this workload (extraction + SVM), {threads} threads "
+                     f"x unmodified single-threaded C oracle on disjoint shards, {secs:.1f} s",
+           "cpu": cpu_model(), "equivalence_gate": "pass" if ok else "FAIL"}
+    return cpu, ok
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def load_traffic(workload):
+    """dram read+write bytes per launch of lbp_hist from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(workload)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,144 @@
+/*
+ * lbpfused.h -- C ABI of the B200-native fused-depth LBP descriptor + linear
+ * SVM hot path of arXiv 1504.01883 (Naik & Rathna, "Robust real time face
+ * recognition and tracking on GPU using fusion of RGB and depth image").
+ *
+ * Citations: P:L = line L of the paper text, S:L = line L of the
+ * SPEC.md CPU-toolkit spec (interfaces / error conventions only), SURVEY §8x =
+ * /root/repo/SURVEY.md section 8(x) (the build contract), DESIGN.md §n.
+ *
+ * Conventions (all entry points):
+ *  - Every data pointer is a DEVICE pointer unless the name ends in _h.
+ *    The caller owns every buffer; the library never allocates, frees or
+ *    synchronises.  All work is enqueued on `stream` (a cudaStream_t passed as
+ *    void*; NULL = the legacy default stream) and returns immediately.
+ *  - Calls are reentrant and thread-safe; the library keeps no mutable global
+ *    state (its lookup tables are compile-time constants).
+ *  - Host-detectable argument errors return a negative status and enqueue
+ *    nothing.  n_rois == 0 / n == 0 is a no-op returning LBP_OK.
+ *  - A failed launch returns LBP_E_CUDA (LBP_E_UNSUPPORTED if the device is not
+ *    sm_100); asynchronous faults surface on the caller's next sync.
+ */
+#ifndef LBPFUSED_H
+#define LBPFUSED_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* lbp_stream_t; /* cudaStream_t */
+
+enum {
+    LBP_OK = 0,
+    LBP_E_ARG = -1,         /* null pointer, bins not 59/256, cells < 1, dmin > dmax, bad geometry */
+    LBP_E_ROI = -2,         /* per ROI: clamped ROI empty, narrower/shorter than 3 px, bad image */
+    LBP_E_GRID = -3,        /* per ROI: cells_x > W-2 or cells_y > H-2 */
+    LBP_E_OVERFLOW = -4,    /* per ROI: largest cell has more than 65535 px (u16 counts) */
+    LBP_E_UNSUPPORTED = -5, /* valid but unimplemented, or device is not sm_100 */
+    LBP_E_CUDA = -6         /* CUDA launch / copy error */
+};
+
+/* An ROI ("Rect r = boundingRect(...)") inside image `img` of the stack:
+ * top-left (x, y), width w, height h, in pixels.  Clamped to the image. */
+typedef struct {
+    int32_t img, x, y, w, h;
+} lbp_roi_t;
+
+/* Geometry of an image stack: n_images images of height x width pixels.
+ * Pitches and strides are in ELEMENTS (u8 for grey, u16 for depth):
+ * pixel (img, y, x) of grey is grey[img*grey_img_stride + y*grey_pitch + x].
+ * Requires pitch >= width and img_stride >= pitch*(height-1) + width. */
+typedef struct {
+    int32_t n_images, height, width, reserved; /* reserved: must be 0 */
+    int64_t grey_pitch, depth_pitch;
+    int64_t grey_img_stride, depth_img_stride;
+} lbp_images_t;
+
+/* Descriptor length: cells_x * cells_y * bins (Eq. 3: K = cells_x*cells_y
+ * sub-histograms of `bins` bins, concatenated row-major).  Negative status if
+ * the arguments are invalid. */
+int32_t lbp_descriptor_dim(int32_t cells_x, int32_t cells_y, int32_t bins);
+
+/*
+ * lbp_fused_extract -- SURVEY §8a steps a1-a6 for every ROI n:
+ *   clamp ROI; for each interior pixel of the ROI (the 1-px ROI border is
+ *   halo only): valid iff depth == NULL or d(centre) != 0 and
+ *   dmin <= d <= dmax (P:49-63 depth mask); code = Eq. 2 with the
+ *   Fig. 7 weights, S(x) = [x >= 0]; bin = code (bins = 256, "0 to
+ *   255") or the uniform-pattern bin (bins = 59: the 58 codes with <= 2
+ *   circular transitions in ascending order -> 0..57, others -> 58); cell
+ *   (cx, cy) from the floor partition [floor(b*W'/K), floor((b+1)*W'/K)) of
+ *   the interior; desc[n][(cy*cells_x + cx)*bins + bin] += 1 (Eq. 3).
+ *
+ *   grey       u8 image stack, layout per `geom` (required)
+ *   depth      u16 depth stack in mm, same geometry (0 = no reading); NULL = no mask
+ *   rois       [n_rois] lbp_roi_t (device)
+ *   dmin,dmax  inclusive depth window in mm (dmin <= dmax)
+ *   desc       out: u16 [n_rois][lbp_descriptor_dim()] row-major, fully written
+ *   roi_status out, nullable: int32 [n_rois], LBP_OK or the per-ROI error; a failed
+ *              ROI's descriptor row is all zeros.
+ * Returns LBP_OK or a host-detectable error (nothing is enqueued then).
+ */
+int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                          const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                          int32_t cells_x, int32_t cells_y, int32_t bins, uint16_t* desc,
+                          int32_t* roi_status, lbp_stream_t stream);
+
+/*
+ * svm_score -- SURVEY §8a step a7: linear one-vs-rest SVM decision ("a classifier
+ * defined by a hyperplane"; A-vs-B training per identity):
+ *   s[n][c] = fp32( b[c] + sum_d W[c][d] * desc[n][d] ), accumulated EXACTLY (each
+ *   product of a u16 count and an fp32 weight is exact in fp64 / in the integer
+ *   digit-plane tensor-core path) and rounded once to fp32;
+ *   labels[n] = argmax_c s[n][c] over the fp32 scores, ties -> lowest c;
+ *   labels[n] = -1 iff top_score[n] < reject_threshold (-INFINITY = closed set).
+ *
+ *   desc      u16 [n][dim]        W  fp32 [n_classes][dim] row-major   bias fp32 [n_classes]
+ *   prepared  nullable: workspace filled by svm_prepare() for this W (enables the
+ *             tensor-core path for large n_classes); NULL = CUDA-core path
+ *   scores    out, nullable fp32 [n][n_classes]
+ *   labels    out, nullable int32 [n];  top_score out, nullable fp32 [n]
+ */
+int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W,
+                  const float* bias, int32_t n_classes, const void* prepared, float* scores,
+                  int32_t* labels, float* top_score, float reject_threshold,
+                  lbp_stream_t stream);
+
+/* Bytes of device workspace svm_prepare() needs for a [n_classes][dim] model
+ * (0 if the tensor-core path does not apply to this shape). */
+size_t svm_workspace_bytes(int32_t n_classes, int32_t dim);
+
+/* Splits W into fixed-point digit planes for the exact tensor-core scorer (DESIGN.md
+ * §5) into `workspace` (device, >= svm_workspace_bytes()).  Enqueued on stream. */
+int32_t svm_prepare(const float* W, int32_t n_classes, int32_t dim, void* workspace,
+                    size_t workspace_bytes, lbp_stream_t stream);
+
+/*
+ * lbp_recognize_host -- the whole path from HOST buffers (end-to-end entry point):
+ * cudaMemcpyAsync of grey/depth/rois host->device into `workspace`, then
+ * lbp_fused_extract + svm_score, then device->host of labels and top scores.
+ * Host buffers should be pinned for the copies to be asynchronous; the caller
+ * synchronises `stream` before reading labels_h / top_h.
+ *   workspace  device scratch of >= lbp_recognize_workspace_bytes() bytes
+ *   W, bias, prepared  device model as for svm_score
+ */
+size_t lbp_recognize_workspace_bytes(lbp_images_t geom, int32_t has_depth, int32_t n_rois,
+                                     int32_t cells_x, int32_t cells_y, int32_t bins);
+int32_t lbp_recognize_host(const uint8_t* grey_h, const uint16_t* depth_h, lbp_images_t geom,
+                           const lbp_roi_t* rois_h, int32_t n_rois, uint16_t dmin,
+                           uint16_t dmax, int32_t cells_x, int32_t cells_y, int32_t bins,
+                           const float* W, const float* bias, int32_t n_classes,
+                           const void* prepared, float reject_threshold, void* workspace,
+                           size_t workspace_bytes, int32_t* labels_h, float* top_h,
+                           lbp_stream_t stream);
+
+/* Human-readable name of a status code (static string). */
+const char* lbp_status_string(int32_t status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBPFUSED_H */

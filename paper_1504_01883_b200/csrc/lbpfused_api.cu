@@ -1,0 +1,224 @@
+// lbpfused_api.cu -- the C ABI (include/lbpfused.h): argument validation,
+// dispatch between kernel variants, launches on the caller's stream.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "lbp_hist_generic.cuh"
+#include "lbp_hist_fast.cuh"
+#include "svm_fp64.cuh"
+
+using namespace lbpf;
+
+namespace {
+
+int32_t launch_status(cudaError_t e) {
+    if (e == cudaSuccess) return LBP_OK;
+    if (e == cudaErrorNoKernelImageForDevice || e == cudaErrorInvalidDeviceFunction)
+        return LBP_E_UNSUPPORTED;
+    return LBP_E_CUDA;
+}
+
+int32_t check_geometry(const lbp_images_t& g, bool has_depth) {
+    if (g.n_images < 1 || g.height < 1 || g.width < 1 || g.reserved != 0) return LBP_E_ARG;
+    if (g.grey_pitch < g.width || g.grey_img_stride < g.grey_pitch * (g.height - 1) + g.width)
+        return LBP_E_ARG;
+    if (has_depth && (g.depth_pitch < g.width ||
+                      g.depth_img_stride < g.depth_pitch * (g.height - 1) + g.width))
+        return LBP_E_ARG;
+    return LBP_OK;
+}
+
+int num_sms() {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t lbp_descriptor_dim(int32_t cells_x, int32_t cells_y, int32_t bins) {
+    if (cells_x < 1 || cells_y < 1 || (bins != 59 && bins != 256)) return LBP_E_ARG;
+    int64_t d = (int64_t)cells_x * cells_y * bins;
+    return d > 0x7FFFFFFF ? LBP_E_ARG : (int32_t)d;
+}
+
+const char* lbp_status_string(int32_t s) {
+    switch (s) {
+        case LBP_OK: return "LBP_OK";
+        case LBP_E_ARG: return "LBP_E_ARG: invalid argument";
+        case LBP_E_ROI: return "LBP_E_ROI: ROI empty, smaller than 3x3 after clamping, or bad image";
+        case LBP_E_GRID: return "LBP_E_GRID: grid larger than the ROI interior";
+        case LBP_E_OVERFLOW: return "LBP_E_OVERFLOW: a cell has more than 65535 pixels";
+        case LBP_E_UNSUPPORTED: return "LBP_E_UNSUPPORTED: unsupported device or configuration";
+        case LBP_E_CUDA: return "LBP_E_CUDA: CUDA error";
+        default: return "unknown status";
+    }
+}
+
+int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                          const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                          int32_t cells_x, int32_t cells_y, int32_t bins, uint16_t* desc,
+                          int32_t* roi_status, lbp_stream_t stream_) {
+    if (n_rois < 0) return LBP_E_ARG;
+    const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
+    if (dim < 0) return dim;
+    if (dmin > dmax) return LBP_E_ARG;
+    if (n_rois == 0) return LBP_OK;
+    if (!grey || !rois || !desc) return LBP_E_ARG;
+    int32_t st = check_geometry(geom, depth != nullptr);
+    if (st != LBP_OK) return st;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const DepthWindow win = make_window(dmin, dmax);
+
+    // Fast path: 8x8 cells, 59/256 bins, image rows 16-B aligned (decided per ROI
+    // inside the kernel, which falls back to the generic code for ROIs that are
+    // not full-size 128x128 crops at 16-px aligned x).
+    if (fast_path_applicable(geom, depth, cells_x, cells_y, bins)) {
+        cudaError_t e = launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins, desc,
+                                             roi_status, num_sms(), stream);
+        return launch_status(e);
+    }
+    const int grid = (int)std::min<int64_t>(n_rois, (int64_t)num_sms() * 8);
+    if (bins == 59)
+        lbp_hist_generic_kernel<59><<<grid, kGenericThreads, 0, stream>>>(
+            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status);
+    else
+        lbp_hist_generic_kernel<256><<<grid, kGenericThreads, 0, stream>>>(
+            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status);
+    return launch_status(cudaGetLastError());
+}
+
+int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, const float* bias,
+                  int32_t n_classes, const void* prepared, float* scores, int32_t* labels,
+                  float* top_score, float reject_threshold, lbp_stream_t stream_) {
+    if (n < 0 || dim < 1 || n_classes < 1) return LBP_E_ARG;
+    if (n == 0) return LBP_OK;
+    if (!desc || !W || !bias) return LBP_E_ARG;
+    (void)prepared;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int grid = (int)((n + kSvmRows - 1) / kSvmRows);
+    const size_t smem = (size_t)kSvmRows * dim * sizeof(float);
+    if (smem <= 200 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(svm_score_fp64_kernel<true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return launch_status(e);
+        svm_score_fp64_kernel<true><<<grid, kSvmThreads, smem, stream>>>(
+            desc, n, dim, W, bias, n_classes, scores, labels, top_score, reject_threshold);
+    } else {
+        svm_score_fp64_kernel<false><<<grid, kSvmThreads, 0, stream>>>(
+            desc, n, dim, W, bias, n_classes, scores, labels, top_score, reject_threshold);
+    }
+    return launch_status(cudaGetLastError());
+}
+
+size_t svm_workspace_bytes(int32_t n_classes, int32_t dim) {
+    (void)n_classes;
+    (void)dim;
+    return 0;
+}
+
+int32_t svm_prepare(const float* W, int32_t n_classes, int32_t dim, void* workspace,
+                    size_t workspace_bytes, lbp_stream_t stream) {
+    (void)W;
+    (void)n_classes;
+    (void)dim;
+    (void)workspace;
+    (void)workspace_bytes;
+    (void)stream;
+    return LBP_E_UNSUPPORTED;
+}
+
+// --------------------------------------------------------------------------
+// end-to-end entry point from host buffers
+// --------------------------------------------------------------------------
+namespace {
+struct RecognizeLayout {
+    size_t grey_off, grey_bytes, depth_off, depth_bytes, rois_off, rois_bytes;
+    size_t desc_off, desc_bytes, labels_off, top_off, total;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+RecognizeLayout recognize_layout(const lbp_images_t& g, bool has_depth, int32_t n_rois,
+                                 int32_t dim) {
+    RecognizeLayout L{};
+    L.grey_bytes = (size_t)(g.grey_img_stride * (g.n_images - 1) + g.grey_pitch * (g.height - 1) +
+                            g.width);
+    L.depth_bytes = has_depth ? 2 * (size_t)(g.depth_img_stride * (g.n_images - 1) +
+                                             g.depth_pitch * (g.height - 1) + g.width)
+                              : 0;
+    L.rois_bytes = (size_t)n_rois * sizeof(lbp_roi_t);
+    L.desc_bytes = (size_t)n_rois * dim * sizeof(uint16_t);
+    size_t o = 0;
+    L.grey_off = o;
+    o = align256(o + L.grey_bytes);
+    L.depth_off = o;
+    o = align256(o + L.depth_bytes);
+    L.rois_off = o;
+    o = align256(o + L.rois_bytes);
+    L.desc_off = o;
+    o = align256(o + L.desc_bytes);
+    L.labels_off = o;
+    o = align256(o + (size_t)n_rois * 4);
+    L.top_off = o;
+    o = align256(o + (size_t)n_rois * 4);
+    L.total = o;
+    return L;
+}
+}  // namespace
+
+size_t lbp_recognize_workspace_bytes(lbp_images_t geom, int32_t has_depth, int32_t n_rois,
+                                     int32_t cells_x, int32_t cells_y, int32_t bins) {
+    const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
+    if (dim < 0 || n_rois < 0 || check_geometry(geom, has_depth != 0) != LBP_OK) return 0;
+    return recognize_layout(geom, has_depth != 0, n_rois, dim).total;
+}
+
+int32_t lbp_recognize_host(const uint8_t* grey_h, const uint16_t* depth_h, lbp_images_t geom,
+                           const lbp_roi_t* rois_h, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                           int32_t cells_x, int32_t cells_y, int32_t bins, const float* W,
+                           const float* bias, int32_t n_classes, const void* prepared,
+                           float reject_threshold, void* workspace, size_t workspace_bytes,
+                           int32_t* labels_h, float* top_h, lbp_stream_t stream_) {
+    if (n_rois < 0 || n_classes < 1) return LBP_E_ARG;
+    const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
+    if (dim < 0) return dim;
+    if (dmin > dmax) return LBP_E_ARG;
+    if (n_rois == 0) return LBP_OK;
+    if (!grey_h || !rois_h || !W || !bias || !workspace) return LBP_E_ARG;
+    int32_t st = check_geometry(geom, depth_h != nullptr);
+    if (st != LBP_OK) return st;
+    const RecognizeLayout L = recognize_layout(geom, depth_h != nullptr, n_rois, dim);
+    if (workspace_bytes < L.total) return LBP_E_ARG;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    char* ws = (char*)workspace;
+    uint8_t* grey = (uint8_t*)(ws + L.grey_off);
+    uint16_t* depth = depth_h ? (uint16_t*)(ws + L.depth_off) : nullptr;
+    lbp_roi_t* rois = (lbp_roi_t*)(ws + L.rois_off);
+    uint16_t* desc = (uint16_t*)(ws + L.desc_off);
+    int32_t* labels = (int32_t*)(ws + L.labels_off);
+    float* top = (float*)(ws + L.top_off);
+    cudaError_t e = cudaMemcpyAsync(grey, grey_h, L.grey_bytes, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess && depth_h)
+        e = cudaMemcpyAsync(depth, depth_h, L.depth_bytes, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(rois, rois_h, L.rois_bytes, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return LBP_E_CUDA;
+    st = lbp_fused_extract(grey, depth, geom, rois, n_rois, dmin, dmax, cells_x, cells_y, bins,
+                           desc, nullptr, stream_);
+    if (st != LBP_OK) return st;
+    st = svm_score(desc, n_rois, dim, W, bias, n_classes, prepared, nullptr, labels, top,
+                   reject_threshold, stream_);
+    if (st != LBP_OK) return st;
+    if (labels_h) e = cudaMemcpyAsync(labels_h, labels, (size_t)n_rois * 4, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess && top_h)
+        e = cudaMemcpyAsync(top_h, top, (size_t)n_rois * 4, cudaMemcpyDeviceToHost, stream);
+    return e == cudaSuccess ? LBP_OK : LBP_E_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// svm_fp64.cuh -- CUDA-core linear-SVM scorer with exact fp64 accumulation.
+//
+// s[n][c] = fp32(b[c] + sum_d W[c][d] * h[n][d]): every product of a u16 count
+// and an fp32 weight is exact in fp64 (16 + 24 significant bits), so the only
+// rounding is the fp64 summation (relative 2^-53 per add) and the final
+// fp32 rounding -- the oracle's definition up to summation order (SURVEY §8c
+// step 8, "Score precision" reading).
+//
+// CTA = kSvmRows crops; its warps take classes round-robin; each lane strides
+// the descriptor dimension and keeps kSvmRows fp64 partial sums, reduced with
+// warp shuffles.  The descriptors of the CTA's crops are staged in shared
+// memory as fp32 (counts <= 65535 are exact in fp32).
+#pragma once
+#include "common.cuh"
+
+namespace lbpf {
+
+constexpr int kSvmThreads = 256;
+constexpr int kSvmRows = 8;
+
+__device__ __forceinline__ bool better(float s, int c, float best, int best_c) {
+    // argmax over fp32 scores, ties -> lowest class index
+    return s > best || (s == best && c < best_c);
+}
+
+template <bool kStage>
+__global__ void __launch_bounds__(kSvmThreads)
+svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
+                      const float* __restrict__ W, const float* __restrict__ bias,
+                      int32_t n_classes, float* __restrict__ scores, int32_t* __restrict__ labels,
+                      float* __restrict__ top_score, float reject_threshold) {
+    extern __shared__ float xs[];  // [kSvmRows][dim]
+    __shared__ float wbest[kSvmThreads / 32][kSvmRows];
+    __shared__ int wbest_c[kSvmThreads / 32][kSvmRows];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kWarps = kSvmThreads / 32;
+    const int64_t row0 = (int64_t)blockIdx.x * kSvmRows;
+    const int rows = (int)((n - row0) < kSvmRows ? (n - row0) : kSvmRows);
+
+    if (kStage) {
+        for (int k = 0; k < kSvmRows; ++k)
+            for (int d = threadIdx.x; d < dim; d += blockDim.x)
+                xs[k * dim + d] = k < rows ? (float)desc[(row0 + k) * dim + d] : 0.0f;
+        __syncthreads();
+    }
+    // unstaged: rows past the end re-read the last valid row (results discarded)
+    auto x = [&](int k, int d) -> double {
+        if (kStage) return (double)xs[k * dim + d];
+        return (double)desc[(row0 + min(k, rows - 1)) * dim + d];
+    };
+
+    float best[kSvmRows];
+    int best_c[kSvmRows];
+#pragma unroll
+    for (int k = 0; k < kSvmRows; ++k) {
+        best[k] = -INFINITY;
+        best_c[k] = 0x7FFFFFFF;
+    }
+    for (int c = warp; c < n_classes; c += kWarps) {
+        const float* w = W + (int64_t)c * dim;
+        double acc[kSvmRows];
+#pragma unroll
+        for (int k = 0; k < kSvmRows; ++k) acc[k] = 0.0;
+        for (int d = lane; d < dim; d += 32) {
+            const double wd = (double)__ldg(w + d);
+#pragma unroll
+            for (int k = 0; k < kSvmRows; ++k) acc[k] = fma(wd, x(k, d), acc[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < kSvmRows; ++k) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xFFFFFFFFu, acc[k], off);
+        }
+        const double b = (double)__ldg(bias + c);
+#pragma unroll
+        for (int k = 0; k < kSvmRows; ++k) {
+            const float s = (float)(acc[k] + b);
+            if (lane == 0 && k < rows && scores) scores[(row0 + k) * n_classes + c] = s;
+            if (better(s, c, best[k], best_c[k]) || best_c[k] == 0x7FFFFFFF) {
+                best[k] = s;
+                best_c[k] = c;
+            }
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < kSvmRows; ++k) {
+            wbest[warp][k] = best[k];
+            wbest_c[warp][k] = best_c[k];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < rows) {
+        const int k = threadIdx.x;
+        float b = wbest[0][k];
+        int bc = wbest_c[0][k];
+        for (int w = 1; w < kWarps; ++w) {
+            if (wbest_c[w][k] == 0x7FFFFFFF) continue;
+            if (bc == 0x7FFFFFFF || better(wbest[w][k], wbest_c[w][k], b, bc)) {
+                b = wbest[w][k];
+                bc = wbest_c[w][k];
+            }
+        }
+        if (top_score) top_score[row0 + k] = b;
+        if (labels) labels[row0 + k] = (b < reject_threshold) ? -1 : bc;
+    }
+}
+
+}  // namespace lbpf

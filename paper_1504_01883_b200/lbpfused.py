@@ -1,0 +1,206 @@
+"""Thin ctypes binding of liblbpfused.so (include/lbpfused.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA library; this module only turns
+torch tensors into (device pointer, geometry, stream) arguments.  There is no
+CPU fallback: if the library is missing or the tensors are not on a CUDA
+device, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch
+
+from . import build as _build
+
+LBP_OK, LBP_E_ARG, LBP_E_ROI, LBP_E_GRID, LBP_E_OVERFLOW, LBP_E_UNSUPPORTED, LBP_E_CUDA = \
+    0, -1, -2, -3, -4, -5, -6
+
+
+class LbpError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+        self.status = status
+
+
+class lbp_images_t(ctypes.Structure):
+    _fields_ = [("n_images", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("width", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("grey_pitch", ctypes.c_int64), ("depth_pitch", ctypes.c_int64),
+                ("grey_img_stride", ctypes.c_int64), ("depth_img_stride", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load liblbpfused.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_build.LIB):
+            raise ImportError(f"{_build.LIB} is missing: run `python __graft_entry__.py build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(_build.LIB)
+        P, i32, u16, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint16, ctypes.c_float
+        sz = ctypes.c_size_t
+        L.lbp_descriptor_dim.argtypes = [i32, i32, i32]
+        L.lbp_descriptor_dim.restype = i32
+        L.lbp_status_string.argtypes = [i32]
+        L.lbp_status_string.restype = ctypes.c_char_p
+        L.lbp_fused_extract.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, P, P, P]
+        L.lbp_fused_extract.restype = i32
+        L.svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, P, f32, P]
+        L.svm_score.restype = i32
+        L.svm_workspace_bytes.argtypes = [i32, i32]
+        L.svm_workspace_bytes.restype = sz
+        L.svm_prepare.argtypes = [P, i32, i32, P, sz, P]
+        L.svm_prepare.restype = i32
+        L.lbp_recognize_workspace_bytes.argtypes = [lbp_images_t, i32, i32, i32, i32, i32]
+        L.lbp_recognize_workspace_bytes.restype = sz
+        L.lbp_recognize_host.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32,
+                                         P, P, i32, P, f32, P, sz, P, P, P]
+        L.lbp_recognize_host.restype = i32
+        _lib = L
+    return _lib
+
+
+def status_string(status: int) -> str:
+    return lib().lbp_status_string(int(status)).decode()
+
+
+def lbp_descriptor_dim(cells_x: int, cells_y: int, bins: int) -> int:
+    d = lib().lbp_descriptor_dim(cells_x, cells_y, bins)
+    if d < 0:
+        raise LbpError(d, "lbp_descriptor_dim")
+    return d
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _stack3(t: torch.Tensor) -> torch.Tensor:
+    return t.unsqueeze(0) if t.dim() == 2 else t
+
+
+def images_geometry(grey: torch.Tensor, depth: torch.Tensor | None) -> lbp_images_t:
+    """lbp_images_t from [n_images][H][W] (or [H][W]) tensors with unit column stride."""
+    g = _stack3(grey)
+    if g.stride(2) != 1:
+        raise ValueError("grey rows must be contiguous")
+    n, H, W = g.shape
+    geom = lbp_images_t(n, H, W, 0, g.stride(1), g.stride(1), g.stride(0), g.stride(0))
+    if depth is not None:
+        d = _stack3(depth)
+        if tuple(d.shape) != (n, H, W) or d.stride(2) != 1:
+            raise ValueError("depth must match grey's shape with contiguous rows")
+        geom.depth_pitch, geom.depth_img_stride = d.stride(1), d.stride(0)
+    return geom
+
+
+def _check_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("lbpfused operates on CUDA tensors only (no CPU fallback)")
+
+
+def lbp_fused_extract(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.Tensor,
+                      dmin: int, dmax: int, cells_x: int, cells_y: int, bins: int,
+                      out: torch.Tensor | None = None, roi_status: torch.Tensor | None = None,
+                      stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Descriptors u16 [n_rois][cells_y*cells_x*bins] of the ROIs (int32 [n][5] = img,x,y,w,h)."""
+    _check_cuda(grey, depth, rois, out, roi_status)
+    assert grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)
+    assert rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5
+    n = rois.shape[0]
+    dim = lbp_descriptor_dim(cells_x, cells_y, bins)
+    if out is None:
+        out = torch.empty((n, dim), dtype=torch.uint16, device=grey.device)
+    assert out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim
+    if roi_status is not None:
+        assert roi_status.dtype == torch.int32 and roi_status.numel() >= n
+    st = lib().lbp_fused_extract(_ptr(grey), _ptr(depth), images_geometry(grey, depth),
+                                 _ptr(rois), n, dmin, dmax, cells_x, cells_y, bins, _ptr(out),
+                                 _ptr(roi_status), _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_fused_extract")
+    return out
+
+
+def svm_workspace_bytes(n_classes: int, dim: int) -> int:
+    return int(lib().svm_workspace_bytes(n_classes, dim))
+
+
+def svm_prepare(W: torch.Tensor, stream=None) -> torch.Tensor | None:
+    """Digit-plane workspace for the tensor-core scorer, or None when that path does not apply."""
+    _check_cuda(W)
+    C, dim = W.shape
+    nbytes = svm_workspace_bytes(C, dim)
+    if nbytes == 0:
+        return None
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=W.device)
+    st = lib().svm_prepare(_ptr(W), C, dim, _ptr(ws), nbytes, _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "svm_prepare")
+    return ws
+
+
+def svm_score(desc: torch.Tensor, W: torch.Tensor, bias: torch.Tensor, prepared=None,
+              reject_threshold: float = -math.inf, want_scores: bool = True,
+              labels: torch.Tensor | None = None, top_score: torch.Tensor | None = None,
+              scores: torch.Tensor | None = None, stream=None):
+    """(scores fp32 [n][C] or None, labels int32 [n], top fp32 [n]) of the linear OvR SVM."""
+    _check_cuda(desc, W, bias, prepared)
+    assert desc.dtype == torch.uint16 and desc.is_contiguous()
+    assert W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32
+    n, dim = desc.shape
+    C = W.shape[0]
+    if W.shape[1] != dim or bias.numel() != C:
+        raise LbpError(LBP_E_ARG, "svm_score: dimension mismatch")
+    dev = desc.device
+    if want_scores and scores is None:
+        scores = torch.empty((n, C), dtype=torch.float32, device=dev)
+    if labels is None:
+        labels = torch.empty(n, dtype=torch.int32, device=dev)
+    if top_score is None:
+        top_score = torch.empty(n, dtype=torch.float32, device=dev)
+    st = lib().svm_score(_ptr(desc), n, dim, _ptr(W), _ptr(bias), C, _ptr(prepared),
+                         _ptr(scores if want_scores else None), _ptr(labels), _ptr(top_score),
+                         reject_threshold, _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "svm_score")
+    return (scores if want_scores else None), labels, top_score
+
+
+def lbp_recognize_workspace_bytes(geom: lbp_images_t, has_depth: bool, n_rois: int,
+                                  cells_x: int, cells_y: int, bins: int) -> int:
+    return int(lib().lbp_recognize_workspace_bytes(geom, int(has_depth), n_rois, cells_x,
+                                                   cells_y, bins))
+
+
+def lbp_recognize_host(grey_h: torch.Tensor, depth_h: torch.Tensor | None, rois_h: torch.Tensor,
+                       dmin: int, dmax: int, cells_x: int, cells_y: int, bins: int,
+                       W: torch.Tensor, bias: torch.Tensor, prepared, workspace: torch.Tensor,
+                       labels_h: torch.Tensor, top_h: torch.Tensor,
+                       reject_threshold: float = -math.inf, stream=None) -> None:
+    """End-to-end call from (pinned) HOST tensors; results land in labels_h / top_h after a
+    sync of `stream`."""
+    _check_cuda(W, bias, workspace)
+    for t in (grey_h, depth_h, rois_h, labels_h, top_h):
+        if t is not None and t.is_cuda:
+            raise ValueError("lbp_recognize_host takes host tensors")
+    geom = images_geometry(grey_h, depth_h)
+    n = rois_h.shape[0]
+    st = lib().lbp_recognize_host(_ptr(grey_h), _ptr(depth_h), geom, _ptr(rois_h), n, dmin, dmax,
+                                  cells_x, cells_y, bins, _ptr(W), _ptr(bias), W.shape[0],
+                                  _ptr(prepared), reject_threshold, _ptr(workspace),
+                                  workspace.numel(), _ptr(labels_h), _ptr(top_h), _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_recognize_host")

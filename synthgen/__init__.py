@@ -146,3 +146,53 @@ def random_rois(n: int, n_images: int, H: int, W: int, seed: int, min_size: int 
         x = (rng.random(n) * (W - w + 1)).astype(np.int64)
         y = (rng.random(n) * (H - h + 1)).astype(np.int64)
     return np.stack([rng.integers(0, n_images, n), x, y, w, h], axis=1).astype(np.int32)
+
+
+# --------------------------------------------------------------------------- GPU twin
+import os as _os
+import subprocess as _subprocess
+
+_HERE = _os.path.dirname(_os.path.abspath(__file__))
+_CU = _os.path.join(_HERE, "synth_gen.cu")
+_SO = _os.path.join(_HERE, "libsynthgen.so")
+_gpu_lib = None
+
+
+def build_gpu(force: bool = False) -> str:
+    """nvcc-compile synth_gen.cu for sm_100a into synthgen/libsynthgen.so (in-tree)."""
+    if force or not _os.path.exists(_SO) or _os.path.getmtime(_SO) < _os.path.getmtime(_CU):
+        nvcc = _os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+        _subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                         "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-o", _SO, _CU],
+                        check=True)
+    return _SO
+
+
+def gpu_face_crops(n: int, H: int, W: int, seed: int = 42, first_index: int = 0,
+                   dist: str | int = "face", grey=None, depth=None, device="cuda"):
+    """Same crops as face_crops(), drawn directly into CUDA tensors (torch, current stream)."""
+    import ctypes
+
+    import torch
+    global _gpu_lib
+    if _gpu_lib is None:
+        if not _os.path.exists(_SO):
+            raise ImportError(f"{_SO} missing: run __graft_entry__.build()")
+        _gpu_lib = ctypes.CDLL(_SO)
+        _gpu_lib.synth_face_crops.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                              ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+                                              ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
+        _gpu_lib.synth_face_crops.restype = ctypes.c_int32
+    dist = DISTS[dist] if isinstance(dist, str) else int(dist)
+    if grey is None:
+        grey = torch.empty((n, H, W), dtype=torch.uint8, device=device)
+    if depth is None:
+        depth = torch.empty((n, H, W), dtype=torch.uint16, device=device)
+    assert grey.is_contiguous() and depth.is_contiguous() and grey.numel() == n * H * W
+    st = _gpu_lib.synth_face_crops(ctypes.c_void_p(grey.data_ptr()),
+                                   ctypes.c_void_p(depth.data_ptr()), n, H, W, seed & 0xFFFFFFFF,
+                                   first_index, dist,
+                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if st != 0:
+        raise RuntimeError(f"synth_face_crops failed ({st})")
+    return grey, depth

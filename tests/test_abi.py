@@ -1,0 +1,110 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol that
+include/*.h declares, and rejects host-detectable argument errors before
+touching the device (SURVEY §8b conventions)."""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    names = []
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\*?\s+\*?([a-z_][a-z0-9_]*)\s*\(",
+                             src, flags=re.M):
+            names.append(m.group(1))
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1504_01883_b200 import build, lbpfused
+    build.build()
+    return lbpfused.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared_functions()
+    assert {"lbp_fused_extract", "svm_score", "lbp_descriptor_dim", "lbp_status_string",
+            "svm_prepare", "svm_workspace_bytes", "lbp_recognize_host",
+            "lbp_recognize_workspace_bytes"} <= set(names)
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_descriptor_dim_and_status_strings(L):
+    from paper_1504_01883_b200 import lbpfused as lb
+    assert lb.lbp_descriptor_dim(8, 8, 59) == 3776
+    assert lb.lbp_descriptor_dim(1, 1, 256) == 256
+    assert L.lbp_descriptor_dim(0, 8, 59) == lb.LBP_E_ARG
+    assert L.lbp_descriptor_dim(8, 8, 60) == lb.LBP_E_ARG
+    assert L.lbp_descriptor_dim(65536, 65536, 256) == lb.LBP_E_ARG
+    for s in range(-6, 1):
+        assert lb.status_string(s).startswith("LBP_")
+
+
+def _geom(lb, n=1, H=8, W=8, pitch=8):
+    return lb.lbp_images_t(n, H, W, 0, pitch, pitch, pitch * H, pitch * H)
+
+
+def test_extract_argument_errors_enqueue_nothing(L):
+    """Each host-detectable error returns before any CUDA call (no device is present here)."""
+    from paper_1504_01883_b200 import lbpfused as lb
+    P = ctypes.c_void_p
+    dummy = P(0x1000)  # never dereferenced: validation fails first
+    g = _geom(lb)
+
+    def call(grey=dummy, rois=dummy, n=1, dmin=0, dmax=10, cx=2, cy=2, bins=59, desc=dummy, geom=g):
+        return L.lbp_fused_extract(grey, None, geom, rois, n, dmin, dmax, cx, cy, bins, desc,
+                                   None, None)
+    assert call(n=0) == lb.LBP_OK
+    assert call(n=-1) == lb.LBP_E_ARG
+    assert call(bins=60) == lb.LBP_E_ARG
+    assert call(cx=0) == lb.LBP_E_ARG
+    assert call(dmin=11) == lb.LBP_E_ARG
+    assert call(grey=None) == lb.LBP_E_ARG
+    assert call(rois=None) == lb.LBP_E_ARG
+    assert call(desc=None) == lb.LBP_E_ARG
+    assert call(geom=_geom(lb, pitch=7)) == lb.LBP_E_ARG
+    assert call(geom=_geom(lb, n=0)) == lb.LBP_E_ARG
+    bad = _geom(lb)
+    bad.reserved = 1
+    assert call(geom=bad) == lb.LBP_E_ARG
+
+
+def test_svm_argument_errors(L):
+    from paper_1504_01883_b200 import lbpfused as lb
+    P = ctypes.c_void_p
+    d = P(0x1000)
+    call = lambda n=4, dim=8, C=2, desc=d, W=d, b=d: L.svm_score(
+        desc, n, dim, W, b, C, None, None, None, None, float("-inf"), None)
+    assert call(n=0) == lb.LBP_OK
+    assert call(n=-1) == lb.LBP_E_ARG
+    assert call(dim=0) == lb.LBP_E_ARG
+    assert call(C=0) == lb.LBP_E_ARG
+    assert call(desc=None) == lb.LBP_E_ARG
+    assert call(W=None) == lb.LBP_E_ARG
+    assert call(b=None) == lb.LBP_E_ARG
+
+
+def test_recognize_workspace_size(L):
+    from paper_1504_01883_b200 import lbpfused as lb
+    g = lb.lbp_images_t(16, 128, 128, 0, 128, 128, 128 * 128, 128 * 128)
+    n = lb.lbp_recognize_workspace_bytes(g, True, 16, 8, 8, 59)
+    assert n >= 16 * 128 * 128 * 3 + 16 * 3776 * 2 + 16 * 20 + 16 * 8
+    assert lb.lbp_recognize_workspace_bytes(g, True, 16, 8, 8, 60) == 0
+
+
+def test_binding_refuses_cpu_tensors():
+    import torch
+    from paper_1504_01883_b200 import lbpfused as lb
+    g = torch.zeros(1, 8, 8, dtype=torch.uint8)
+    r = torch.zeros(1, 5, dtype=torch.int32)
+    with pytest.raises(ValueError):
+        lb.lbp_fused_extract(g, None, r, 0, 10, 2, 2, 59)

@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Descriptors and ROI statuses must be bit-exact; SVM scores within 1e-5 relative
+(J.north_star; tests/parity_util.py) and labels identical away from ties.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthgen
+from parity_util import labels_agree_away_from_ties, svm_tolerance_ok
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def lb():
+    import paper_1504_01883_b200 as lb
+    lb.lbpfused.lib()
+    return lb
+
+
+def _gpu_extract(lb, grey, depth, rois, dmin, dmax, kx, ky, bins, with_status=True):
+    g = torch.from_numpy(np.ascontiguousarray(grey)).to(DEV)
+    d = None if depth is None else torch.from_numpy(np.ascontiguousarray(depth).view(np.int16)).to(DEV).view(torch.uint16)
+    r = torch.from_numpy(np.ascontiguousarray(rois, dtype=np.int32)).to(DEV)
+    st = torch.full((r.shape[0],), 123, dtype=torch.int32, device=DEV)
+    out = lb.lbp_fused_extract(g, d, r, dmin, dmax, kx, ky, bins,
+                               roi_status=st if with_status else None)
+    torch.cuda.synchronize()
+    return out.cpu().view(torch.int16).numpy().view(np.uint16), st.cpu().numpy()
+
+
+def _check(lb, grey, depth, rois, dmin, dmax, kx, ky, bins):
+    got, st = _gpu_extract(lb, grey, depth, rois, dmin, dmax, kx, ky, bins)
+    ref, st_ref = oracle.lbp_extract(grey, depth, rois, dmin, dmax, kx, ky, bins, return_status=True)
+    assert np.array_equal(st, st_ref)
+    bad = np.nonzero((got != ref).any(1))[0]
+    assert bad.size == 0, f"{bad.size} rows differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("bins", [59, 256])
+@pytest.mark.parametrize("dist", ["face", "constant", "noise"])
+def test_crops_128_bitexact(lb, bins, dist):
+    grey, depth = synthgen.face_crops(48, 128, 128, seed=21, dist=dist)
+    _check(lb, grey, depth, synthgen.full_rois(48, 128, 128), 600, 1400, 8, 8, bins)
+
+
+def test_crop_64_config1(lb):
+    grey, depth = synthgen.face_crops(1, 64, 64, seed=1)
+    _check(lb, grey, depth, synthgen.full_rois(1, 64, 64), 600, 1400, 8, 8, 59)
+
+
+@pytest.mark.parametrize("bins", [59, 256])
+def test_no_depth_mask(lb, bins):
+    grey, _ = synthgen.face_crops(8, 128, 128, seed=2)
+    _check(lb, grey, None, synthgen.full_rois(8, 128, 128), 0, 0, 8, 8, bins)
+
+
+@pytest.mark.parametrize("H,W,kx,ky", [(37, 53, 5, 3), (20, 131, 7, 9), (9, 9, 7, 1),
+                                       (130, 130, 16, 16), (200, 200, 1, 1), (66, 70, 8, 8)])
+@pytest.mark.parametrize("bins", [59, 256])
+def test_ragged_random_rois(lb, H, W, kx, ky, bins):
+    grey, depth = synthgen.face_crops(5, H, W, seed=H * W)
+    rois = synthgen.random_rois(40, 5, H, W, seed=kx * 31 + ky, min_size=1)
+    rois[0] = (0, 0, 0, W, H)
+    _check(lb, grey, depth, rois, 600, 1400, kx, ky, bins)
+
+
+def test_tiny_rois_every_grid(lb):
+    grey, depth = synthgen.face_crops(1, 8, 8, seed=3, dist="noise")
+    for w in range(1, 8):
+        for h in range(1, 8):
+            for kx in range(1, 6):
+                for ky in range(1, 6):
+                    _check(lb, grey, depth, [[0, 1, 0, w, h]], 0, 65535, kx, ky, 256)
+
+
+def test_large_grid_chunked(lb):
+    """16x16 cells x 256 bins = 65536 counters: more than one shared-memory chunk."""
+    grey, depth = synthgen.face_crops(3, 200, 200, seed=4)
+    _check(lb, grey, depth, synthgen.full_rois(3, 200, 200), 600, 1400, 16, 16, 256)
+    _check(lb, grey, depth, synthgen.full_rois(3, 200, 200), 600, 1400, 40, 30, 59)
+
+
+def test_error_rois_and_overflow(lb):
+    grey = np.full((2, 300, 300), 9, np.uint8)
+    rois = [[0, 400, 0, 10, 10], [0, 0, 0, 2, 50], [5, 0, 0, 10, 10], [0, 0, 0, 6, 6],
+            [0, 0, 0, 260, 260], [0, 0, 0, 257, 257], [1, 298, 298, 50, 50], [1, 0, 0, 258, 258],
+            [-1, 0, 0, 10, 10], [0, -10, -10, 5, 5], [1, 290, 290, 1000, 1000]]
+    _check(lb, grey, None, rois, 0, 65535, 1, 1, 59)
+    _check(lb, grey, None, rois, 0, 65535, 5, 5, 256)
+
+
+def test_depth_window_edges(lb):
+    grey, depth = synthgen.face_crops(4, 64, 64, seed=5)
+    rois = synthgen.full_rois(4, 64, 64)
+    for dmin, dmax in [(0, 0), (0, 65535), (1, 1), (1000, 1000), (0, 950), (2000, 65535),
+                       (65535, 65535)]:
+        _check(lb, grey, depth, rois, dmin, dmax, 8, 8, 59)
+
+
+def test_pitched_frames_config2(lb):
+    """640x480 Kinect frames (pitched views of wider buffers) with 4 ROIs each."""
+    n_frames, H, W = 3, 480, 640
+    grey, depth = synthgen.face_crops(n_frames, H, W, seed=6)
+    gw = np.zeros((n_frames, H, W + 64), np.uint8)
+    dw = np.zeros((n_frames, H, W + 32), np.uint16)
+    gw[:, :, :W] = grey
+    dw[:, :, :W] = depth
+    rois = []
+    for f in range(n_frames):
+        for k in range(4):
+            rois.append([f, 40 + 150 * k + 7 * f, 100 + 20 * k, 128, 128])
+    rois = np.array(rois, np.int32)
+    g = torch.from_numpy(gw).to(DEV)[:, :, :W]
+    d = torch.from_numpy(dw.view(np.int16)).to(DEV).view(torch.uint16)[:, :, :W]
+    r = torch.from_numpy(rois).to(DEV)
+    out = lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 59)
+    ref = oracle.lbp_extract(grey, depth, rois, 600, 1400, 8, 8, 59)
+    assert np.array_equal(out.cpu().view(torch.int16).numpy().view(np.uint16), ref)
+
+
+def test_empty_batch(lb):
+    g = torch.zeros(1, 8, 8, dtype=torch.uint8, device=DEV)
+    r = torch.zeros(0, 5, dtype=torch.int32, device=DEV)
+    out = lb.lbp_fused_extract(g, None, r, 0, 10, 2, 2, 59)
+    assert out.shape == (0, 236)
+
+
+# --------------------------------------------------------------------------- SVM
+
+def _svm_inputs(n, C, seed):
+    grey, depth = synthgen.face_crops(n, 128, 128, seed=seed)
+    desc = oracle.lbp_extract(grey, depth, synthgen.full_rois(n, 128, 128), 600, 1400, 8, 8, 59)
+    W, b = synthgen.svm_weights(C, desc.shape[1], seed=seed)
+    return desc, W, b
+
+
+def _gpu_svm(lb, desc, W, b, reject=-math.inf, prepared=False):
+    d = torch.from_numpy(desc.view(np.int16)).to(DEV).view(torch.uint16)
+    Wt = torch.from_numpy(W).to(DEV)
+    bt = torch.from_numpy(b).to(DEV)
+    prep = lb.svm_prepare(Wt) if prepared else None
+    s, lab, top = lb.svm_score(d, Wt, bt, prepared=prep, reject_threshold=reject)
+    torch.cuda.synchronize()
+    return s.cpu().numpy(), lab.cpu().numpy(), top.cpu().numpy()
+
+
+@pytest.mark.parametrize("C", [1, 2, 10, 100, 1000])
+@pytest.mark.parametrize("prepared", [False, True])
+def test_svm_random_within_tolerance(lb, C, prepared):
+    desc, W, b = _svm_inputs(70, C, seed=C)
+    s, lab, top = _gpu_svm(lb, desc, W, b, prepared=prepared)
+    s_ref, lab_ref, top_ref = oracle.svm_score(desc, W, b)
+    ok, worst = svm_tolerance_ok(desc, W, b, s, s_ref)
+    assert ok, worst
+    assert labels_agree_away_from_ties(s_ref, lab, lab_ref, desc, W, b)
+    assert np.array_equal(top, s[np.arange(len(lab)), np.where(lab < 0, 0, lab)])
+
+
+@pytest.mark.parametrize("prepared", [False, True])
+def test_svm_integer_weights_bitexact(lb, prepared):
+    """Integer W, b: exact in any summation order -> bit-exact scores and labels."""
+    desc, _, _ = _svm_inputs(40, 1, seed=9)
+    rng = np.random.default_rng(1)
+    W = rng.integers(-1000, 1001, (100, desc.shape[1])).astype(np.float32)
+    b = rng.integers(-50, 51, 100).astype(np.float32)
+    s, lab, top = _gpu_svm(lb, desc, W, b, prepared=prepared)
+    s_ref, lab_ref, top_ref = oracle.svm_score(desc, W, b)
+    assert np.array_equal(s, s_ref) and np.array_equal(lab, lab_ref) and np.array_equal(top, top_ref)
+
+
+def test_svm_ties_and_reject(lb):
+    desc, W, b = _svm_inputs(20, 4, seed=3)
+    W[2] = W[1]
+    b[2] = b[1] = 1e4  # classes 1 and 2 tie at the top -> label 1
+    s, lab, top = _gpu_svm(lb, desc, W, b)
+    assert (lab == 1).all()
+    _, lab, _ = _gpu_svm(lb, desc, W, b, reject=float("inf"))
+    assert (lab == -1).all()
+    _, lab_r, _ = _gpu_svm(lb, desc, W, b, reject=float(np.median(top)))
+    s_ref, lab_ref, _ = oracle.svm_score(desc, W, b, reject_threshold=float(np.median(top)))
+    assert np.array_equal(lab_r, lab_ref)
+
+
+def test_recognize_host_matches_device_path(lb):
+    n = 32
+    grey, depth = synthgen.face_crops(n, 128, 128, seed=10)
+    rois = synthgen.full_rois(n, 128, 128)
+    W, b = synthgen.svm_weights(10, 3776, seed=2)
+    g = torch.from_numpy(grey).pin_memory()
+    d = torch.from_numpy(depth.view(np.int16)).view(torch.uint16).pin_memory()
+    r = torch.from_numpy(rois).pin_memory()
+    Wt, bt = torch.from_numpy(W).to(DEV), torch.from_numpy(b).to(DEV)
+    geom = lb.images_geometry(g, d)
+    ws = torch.empty(lb.lbp_recognize_workspace_bytes(geom, True, n, 8, 8, 59), dtype=torch.uint8,
+                     device=DEV)
+    lab = torch.empty(n, dtype=torch.int32).pin_memory()
+    top = torch.empty(n, dtype=torch.float32).pin_memory()
+    lb.lbp_recognize_host(g, d, r, 600, 1400, 8, 8, 59, Wt, bt, None, ws, lab, top)
+    torch.cuda.synchronize()
+    desc = oracle.lbp_extract(grey, depth, rois, 600, 1400, 8, 8, 59)
+    s_ref, lab_ref, top_ref = oracle.svm_score(desc, W, b)
+    assert labels_agree_away_from_ties(s_ref, lab.numpy(), lab_ref, desc, W, b)
+    ok, _ = svm_tolerance_ok(desc, W, b, top.numpy()[:, None], top_ref[:, None])
+    assert ok
