@@ -95,4 +95,11 @@ __device__ __forceinline__ RoiGeom clamp_roi(const lbp_roi_t r, const lbp_images
     return o;
 }
 
+// ROIs handled by the TMA fast kernel: fully inside the image, exactly kFastTile square.
+constexpr int kFastTile = 128;
+__device__ __forceinline__ bool roi_is_fast(const lbp_roi_t& r, const lbp_images_t& g) {
+    return r.w == kFastTile && r.h == kFastTile && r.img >= 0 && r.img < g.n_images && r.x >= 0 &&
+           r.y >= 0 && (int64_t)r.x + kFastTile <= g.width && (int64_t)r.y + kFastTile <= g.height;
+}
+
 }  // namespace lbpf

@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(kGenericThreads)
 lbp_hist_generic_kernel(const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
                         lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
                         DepthWindow win, int32_t cells_x, int32_t cells_y,
-                        uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status) {
+                        uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status,
+                        int skip_fast) {
     __shared__ uint32_t hist[kGenericHistCap];
     __shared__ uint8_t lut[256];
     constexpr int kCellsPerChunk = kGenericHistCap / BINS;
@@ -48,7 +49,9 @@ lbp_hist_generic_kernel(const uint8_t* __restrict__ grey, const uint16_t* __rest
         lut[i] = (BINS == 59) ? kUniformLutDev.v[i] : (uint8_t)i;
 
     for (int32_t n = blockIdx.x; n < n_rois; n += gridDim.x) {
-        const RoiGeom r = clamp_roi(rois[n], geom, cells_x, cells_y);
+        const lbp_roi_t roi = rois[n];
+        if (skip_fast && roi_is_fast(roi, geom)) continue;  // done by lbp_hist_fast_kernel
+        const RoiGeom r = clamp_roi(roi, geom, cells_x, cells_y);
         uint16_t* out = desc + (int64_t)n * dim;
         if (threadIdx.x == 0 && roi_status) roi_status[n] = r.status;
         if (r.status != LBP_OK) {

@@ -74,21 +74,22 @@ int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images
     cudaStream_t stream = (cudaStream_t)stream_;
     const DepthWindow win = make_window(dmin, dmax);
 
-    // Fast path: 8x8 cells, 59/256 bins, image rows 16-B aligned (decided per ROI
-    // inside the kernel, which falls back to the generic code for ROIs that are
-    // not full-size 128x128 crops at 16-px aligned x).
-    if (fast_path_applicable(geom, depth, cells_x, cells_y, bins)) {
+    // Fast path (8x8 cells, 16-B aligned rows): the TMA kernel takes every ROI that is a
+    // fully-inside 128x128 box; the generic kernel then takes the remaining ROIs.
+    int skip_fast = 0;
+    if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc)) {
         cudaError_t e = launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins, desc,
                                              roi_status, num_sms(), stream);
-        return launch_status(e);
+        if (e != cudaSuccess) return launch_status(e);
+        skip_fast = 1;
     }
     const int grid = (int)std::min<int64_t>(n_rois, (int64_t)num_sms() * 8);
     if (bins == 59)
         lbp_hist_generic_kernel<59><<<grid, kGenericThreads, 0, stream>>>(
-            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status);
+            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status, skip_fast);
     else
         lbp_hist_generic_kernel<256><<<grid, kGenericThreads, 0, stream>>>(
-            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status);
+            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status, skip_fast);
     return launch_status(cudaGetLastError());
 }
 
