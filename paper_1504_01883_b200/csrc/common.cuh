@@ -2,6 +2,7 @@
 // includes or links anything under oracle/).
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "lbpfused.h"

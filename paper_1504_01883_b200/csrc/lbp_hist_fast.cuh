@@ -19,12 +19,13 @@
 //    shared-memory increment (ATOMS), integer and order-independent -> bit-exact.
 //  * Epilogue: u32 counters -> u16, 16-B vector stores of the 7,552-B descriptor, counters
 //    re-zeroed in the same pass.
-// ROIs that are not fully-inside 128x128 boxes are skipped here and handled by the
-// generic kernel (same launch sequence, second kernel).
+// ROIs that are not fully-inside 128x128 boxes are processed by the same group with the
+// generic code path (extract_roi_generic), so one launch covers every ROI.
 #pragma once
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "lbp_hist_generic.cuh"
 #include "ptx.cuh"
 
 namespace lbpf {
@@ -85,7 +86,9 @@ __device__ __forceinline__ uint32_t code2(uint32_t c, uint32_t tl, uint32_t t, u
 template <int BINS, bool HAS_DEPTH>
 __global__ void __launch_bounds__(kFastThreads, 1)
 lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
-                     const __grid_constant__ CUtensorMap depth_map, lbp_images_t geom,
+                     const __grid_constant__ CUtensorMap depth_map,
+                     const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
+                     lbp_images_t geom,
                      const lbp_roi_t* __restrict__ rois, int32_t n_rois, DepthWindow win,
                      uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status) {
     using Cfg = FastCfg<BINS>;
@@ -157,9 +160,19 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
     uint32_t phase_bits = 0;
     int stage = 0;
 
+    struct GroupSync {
+        uint32_t id;
+        __device__ __forceinline__ void operator()() const { named_barrier_sync(id, kFastGroupThreads); }
+    };
     for (int32_t n = gid; n < n_rois; n += n_groups) {
         const lbp_roi_t r = rois[n];
-        if (!roi_is_fast(r, geom)) continue;  // generic kernel handles it (uniform per group)
+        if (!roi_is_fast(r, geom)) {  // clamped / odd-sized ROI: generic path, same group
+            extract_roi_generic<BINS, kFastGroupThreads>(
+                grey, HAS_DEPTH ? depth : nullptr, geom, r, n, win, kFastCells, kFastCells, desc,
+                roi_status, hist, Cfg::kHistWords, lut, BINS == 59 ? 2 : 0, gtid, GroupSync{bar_id});
+            named_barrier_sync(bar_id, kFastGroupThreads);
+            continue;
+        }
         mbar_wait(&bars[stage], (phase_bits >> stage) & 1u);
         phase_bits ^= 1u << stage;
         const uint8_t* st = gbase + stage * Cfg::kStageBytes;
@@ -278,7 +291,8 @@ inline bool encode_stack_map(CUtensorMap* map, const void* base, CUtensorMapData
 }
 
 template <int BINS, bool HAS_DEPTH>
-inline cudaError_t launch_fast_t(const CUtensorMap& gm, const CUtensorMap& dm,
+inline cudaError_t launch_fast_t(const CUtensorMap& gm, const CUtensorMap& dm, const uint8_t* grey,
+                                 const uint16_t* depth,
                                  const lbp_images_t& geom, const lbp_roi_t* rois, int32_t n_rois,
                                  const DepthWindow& win, uint16_t* desc, int32_t* roi_status,
                                  int sms, cudaStream_t stream) {
@@ -287,7 +301,8 @@ inline cudaError_t launch_fast_t(const CUtensorMap& gm, const CUtensorMap& dm,
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(sms, (n_rois + kFastGroups - 1) / kFastGroups));
-    kern<<<grid, kFastThreads, smem, stream>>>(gm, dm, geom, rois, n_rois, win, desc, roi_status);
+    kern<<<grid, kFastThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win, desc,
+                                               roi_status);
     return cudaGetLastError();
 }
 
@@ -308,10 +323,10 @@ inline cudaError_t launch_lbp_hist_fast(const uint8_t* grey, const uint16_t* dep
         dm = gm;
     }
     if (bins == 59)
-        return depth ? launch_fast_t<59, true>(gm, dm, geom, rois, n_rois, win, desc, roi_status, sms, stream)
-                     : launch_fast_t<59, false>(gm, dm, geom, rois, n_rois, win, desc, roi_status, sms, stream);
-    return depth ? launch_fast_t<256, true>(gm, dm, geom, rois, n_rois, win, desc, roi_status, sms, stream)
-                 : launch_fast_t<256, false>(gm, dm, geom, rois, n_rois, win, desc, roi_status, sms, stream);
+        return depth ? launch_fast_t<59, true>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, roi_status, sms, stream)
+                     : launch_fast_t<59, false>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, roi_status, sms, stream);
+    return depth ? launch_fast_t<256, true>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, roi_status, sms, stream)
+                 : launch_fast_t<256, false>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, roi_status, sms, stream);
 }
 
 }  // namespace lbpf

@@ -1,13 +1,13 @@
-// lbp_hist_generic.cuh -- generic fused-depth LBP histogram kernel.
+// lbp_hist_generic.cuh -- generic fused-depth LBP histogram code path.
 //
 // Handles every geometry the ABI accepts (any ROI size / position / clamping,
-// any grid, bins 59 or 256).  One CTA per ROI (grid-stride over ROIs); the
-// cell histograms of a chunk of cells live in shared memory as u32 counters
-// and are updated with shared-memory atomics (integer adds: order-independent,
-// so the result is bit-exact whatever the thread schedule).  Grids whose
-// histograms exceed the shared-memory budget are processed in chunks of whole
-// cells, re-scanning only the rows of the chunk.  The fast path for uniform
-// 128x128-class crops lives in lbp_hist_fast.cuh.
+// any grid, bins 59 or 256).  `extract_roi_generic` processes ONE ROI with a
+// group of NT threads; the cell histograms of a chunk of cells live in shared
+// memory as u32 counters updated with shared-memory atomics (integer adds:
+// order-independent, so the result is bit-exact whatever the schedule).  Grids
+// whose histograms exceed the chunk capacity are processed in chunks of whole
+// cells, re-scanning only the rows of the chunk.  It is used by the generic
+// kernel (one CTA per ROI) and, for the odd ROI, inside the TMA fast kernel.
 #pragma once
 #include "common.cuh"
 
@@ -31,68 +31,84 @@ __device__ __forceinline__ uint32_t lbp_code_scalar(const uint8_t* __restrict__ 
     return code;
 }
 
+// One ROI (index n) by a group of NT threads (t = 0..NT-1), hist = `cap` u32 of smem
+// that is all-zero on entry and is all-zero again on return.  lut[code] >> lut_shift is
+// the bin.  `sync()` synchronises the group.
+template <int BINS, int NT, typename Sync>
+__device__ __forceinline__ void extract_roi_generic(
+    const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth, const lbp_images_t& geom,
+    const lbp_roi_t roi, int32_t n, const DepthWindow& win, int32_t cells_x, int32_t cells_y,
+    uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status, uint32_t* hist, int cap,
+    const uint8_t* lut, int lut_shift, int t, Sync sync) {
+    const int64_t dim = (int64_t)cells_x * cells_y * BINS;
+    const int warp = t >> 5, lane = t & 31;
+    constexpr int kWarps = NT / 32;
+    const RoiGeom r = clamp_roi(roi, geom, cells_x, cells_y);
+    uint16_t* out = desc + (int64_t)n * dim;
+    if (t == 0 && roi_status) roi_status[n] = r.status;
+    if (r.status != LBP_OK) {
+        for (int64_t i = t; i < dim; i += NT) out[i] = 0;
+        return;
+    }
+    const uint8_t* G = grey + (int64_t)r.img * geom.grey_img_stride;
+    const uint16_t* D = depth ? depth + (int64_t)r.img * geom.depth_img_stride : nullptr;
+    const int32_t n_cells = cells_x * cells_y;
+    const int32_t cells_per_chunk = cap / BINS;
+
+    for (int32_t c0 = 0; c0 < n_cells; c0 += cells_per_chunk) {
+        const int32_t c1 = min(n_cells, c0 + cells_per_chunk);
+        // interior rows covered by cell rows [c0/Kx, (c1-1)/Kx]
+        const int32_t cy_a = c0 / cells_x, cy_b = (c1 - 1) / cells_x;
+        const int32_t i_begin = (int32_t)(((int64_t)cy_a * r.hi) / cells_y);
+        const int32_t i_end = (int32_t)(((int64_t)(cy_b + 1) * r.hi) / cells_y);
+        for (int32_t i = i_begin + warp; i < i_end; i += kWarps) {
+            const int32_t cy = (int32_t)(((int64_t)(i + 1) * cells_y - 1) / r.hi);
+            const int64_t yy = (int64_t)r.y0 + 1 + i;
+            const uint8_t* grow = G + yy * geom.grey_pitch + r.x0 + 1;
+            const uint16_t* drow = D ? D + yy * geom.depth_pitch + r.x0 + 1 : nullptr;
+            for (int32_t j = lane; j < r.wi; j += 32) {
+                const int32_t cx = (int32_t)(((int64_t)(j + 1) * cells_x - 1) / r.wi);
+                const int32_t cell = cy * cells_x + cx;
+                if (cell < c0 || cell >= c1) continue;
+                if (drow) {
+                    const uint32_t d = drow[j];
+                    if (win.none_valid || (d - win.lo) > win.span) continue;
+                }
+                const uint32_t code = lbp_code_scalar(grow + j, geom.grey_pitch);
+                atomicAdd(&hist[(cell - c0) * BINS + (lut[code] >> lut_shift)], 1u);
+            }
+        }
+        sync();
+        uint16_t* o = out + (int64_t)c0 * BINS;
+        for (int i = t; i < (c1 - c0) * BINS; i += NT) {
+            o[i] = (uint16_t)hist[i];
+            hist[i] = 0;
+        }
+        sync();
+    }
+}
+
+struct CtaSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
 template <int BINS>
 __global__ void __launch_bounds__(kGenericThreads)
 lbp_hist_generic_kernel(const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
                         lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
                         DepthWindow win, int32_t cells_x, int32_t cells_y,
-                        uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status,
-                        int skip_fast) {
+                        uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status) {
     __shared__ uint32_t hist[kGenericHistCap];
     __shared__ uint8_t lut[256];
-    constexpr int kCellsPerChunk = kGenericHistCap / BINS;
-    const int64_t dim = (int64_t)cells_x * cells_y * BINS;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int kWarps = kGenericThreads / 32;
-
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
         lut[i] = (BINS == 59) ? kUniformLutDev.v[i] : (uint8_t)i;
-
+    for (int i = threadIdx.x; i < kGenericHistCap; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
     for (int32_t n = blockIdx.x; n < n_rois; n += gridDim.x) {
-        const lbp_roi_t roi = rois[n];
-        if (skip_fast && roi_is_fast(roi, geom)) continue;  // done by lbp_hist_fast_kernel
-        const RoiGeom r = clamp_roi(roi, geom, cells_x, cells_y);
-        uint16_t* out = desc + (int64_t)n * dim;
-        if (threadIdx.x == 0 && roi_status) roi_status[n] = r.status;
-        if (r.status != LBP_OK) {
-            for (int64_t i = threadIdx.x; i < dim; i += blockDim.x) out[i] = 0;
-            continue;
-        }
-        const uint8_t* G = grey + (int64_t)r.img * geom.grey_img_stride;
-        const uint16_t* D = depth ? depth + (int64_t)r.img * geom.depth_img_stride : nullptr;
-        const int32_t n_cells = cells_x * cells_y;
-
-        for (int32_t c0 = 0; c0 < n_cells; c0 += kCellsPerChunk) {
-            const int32_t c1 = min(n_cells, c0 + kCellsPerChunk);
-            __syncthreads();  // previous chunk's read-out done; lut visible
-            for (int i = threadIdx.x; i < (c1 - c0) * BINS; i += blockDim.x) hist[i] = 0;
-            __syncthreads();
-            // interior rows covered by cell rows [c0/Kx, (c1-1)/Kx]
-            const int32_t cy_a = c0 / cells_x, cy_b = (c1 - 1) / cells_x;
-            const int32_t i_begin = (int32_t)(((int64_t)cy_a * r.hi) / cells_y);
-            const int32_t i_end = (int32_t)(((int64_t)(cy_b + 1) * r.hi) / cells_y);
-            for (int32_t i = i_begin + warp; i < i_end; i += kWarps) {
-                const int32_t cy = (int32_t)(((int64_t)(i + 1) * cells_y - 1) / r.hi);
-                const int64_t yy = (int64_t)r.y0 + 1 + i;
-                const uint8_t* grow = G + yy * geom.grey_pitch + r.x0 + 1;
-                const uint16_t* drow = D ? D + yy * geom.depth_pitch + r.x0 + 1 : nullptr;
-                for (int32_t j = lane; j < r.wi; j += 32) {
-                    const int32_t cx = (int32_t)(((int64_t)(j + 1) * cells_x - 1) / r.wi);
-                    const int32_t cell = cy * cells_x + cx;
-                    if (cell < c0 || cell >= c1) continue;
-                    if (drow) {
-                        const uint32_t d = drow[j];
-                        if (win.none_valid || (d - win.lo) > win.span) continue;
-                    }
-                    const uint32_t code = lbp_code_scalar(grow + j, geom.grey_pitch);
-                    atomicAdd(&hist[(cell - c0) * BINS + lut[code]], 1u);
-                }
-            }
-            __syncthreads();
-            uint16_t* o = out + (int64_t)c0 * BINS;
-            for (int i = threadIdx.x; i < (c1 - c0) * BINS; i += blockDim.x) o[i] = (uint16_t)hist[i];
-        }
-        __syncthreads();
+        extract_roi_generic<BINS, kGenericThreads>(grey, depth, geom, rois[n], n, win, cells_x,
+                                                   cells_y, desc, roi_status, hist,
+                                                   kGenericHistCap, lut, 0, (int)threadIdx.x,
+                                                   CtaSync{});
     }
 }
 

@@ -7,6 +7,7 @@
 #include "lbp_hist_generic.cuh"
 #include "lbp_hist_fast.cuh"
 #include "svm_fp64.cuh"
+#include "svm_gemm.cuh"
 
 using namespace lbpf;
 
@@ -74,22 +75,18 @@ int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images
     cudaStream_t stream = (cudaStream_t)stream_;
     const DepthWindow win = make_window(dmin, dmax);
 
-    // Fast path (8x8 cells, 16-B aligned rows): the TMA kernel takes every ROI that is a
-    // fully-inside 128x128 box; the generic kernel then takes the remaining ROIs.
-    int skip_fast = 0;
-    if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc)) {
-        cudaError_t e = launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins, desc,
-                                             roi_status, num_sms(), stream);
-        if (e != cudaSuccess) return launch_status(e);
-        skip_fast = 1;
-    }
+    // Fast path (8x8 cells, 16-B aligned rows): one TMA-staged persistent kernel; ROIs that
+    // are not fully-inside 128x128 boxes take the generic code path inside it.
+    if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc))
+        return launch_status(launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins,
+                                                  desc, roi_status, num_sms(), stream));
     const int grid = (int)std::min<int64_t>(n_rois, (int64_t)num_sms() * 8);
     if (bins == 59)
         lbp_hist_generic_kernel<59><<<grid, kGenericThreads, 0, stream>>>(
-            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status, skip_fast);
+            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status);
     else
         lbp_hist_generic_kernel<256><<<grid, kGenericThreads, 0, stream>>>(
-            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status, skip_fast);
+            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status);
     return launch_status(cudaGetLastError());
 }
 
@@ -99,8 +96,16 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, 
     if (n < 0 || dim < 1 || n_classes < 1) return LBP_E_ARG;
     if (n == 0) return LBP_OK;
     if (!desc || !W || !bias) return LBP_E_ARG;
-    (void)prepared;
     cudaStream_t stream = (cudaStream_t)stream_;
+    // Tensor-core path: exact integer digit-plane GEMM (needs svm_prepare()'s workspace).
+    SvmPrepHeader h;
+    if (prepared && svm_layout(n_classes, dim, &h) &&
+        (reinterpret_cast<uintptr_t>(desc) & 15) == 0) {
+        cudaError_t e = launch_svm_gemm(desc, n, dim, W, bias, h, (const uint8_t*)prepared, scores,
+                                        labels, top_score, reject_threshold, num_sms(), stream);
+        if (e != cudaErrorNotSupported) return launch_status(e);
+    }
+    // CUDA-core path: exact fp64 accumulation
     const int grid = (int)((n + kSvmRows - 1) / kSvmRows);
     const size_t smem = (size_t)kSvmRows * dim * sizeof(float);
     if (smem <= 200 * 1024) {
@@ -118,20 +123,19 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, 
 }
 
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim) {
-    (void)n_classes;
-    (void)dim;
-    return 0;
+    SvmPrepHeader h;
+    if (!svm_layout(n_classes, dim, &h)) return 0;
+    return svm_layout_bytes(h);
 }
 
 int32_t svm_prepare(const float* W, int32_t n_classes, int32_t dim, void* workspace,
                     size_t workspace_bytes, lbp_stream_t stream) {
-    (void)W;
-    (void)n_classes;
-    (void)dim;
-    (void)workspace;
-    (void)workspace_bytes;
-    (void)stream;
-    return LBP_E_UNSUPPORTED;
+    if (!W || !workspace || n_classes < 1 || dim < 1) return LBP_E_ARG;
+    SvmPrepHeader h;
+    if (!svm_layout(n_classes, dim, &h)) return LBP_E_UNSUPPORTED;
+    if (workspace_bytes < svm_layout_bytes(h)) return LBP_E_ARG;
+    svm_prepare_kernel<<<h.total_rows, 256, 0, (cudaStream_t)stream>>>(W, h, (uint8_t*)workspace);
+    return launch_status(cudaGetLastError());
 }
 
 // --------------------------------------------------------------------------

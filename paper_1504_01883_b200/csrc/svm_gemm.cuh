@@ -1,0 +1,374 @@
+// svm_gemm.cuh -- exact linear-SVM scoring on the 5th-gen tensor cores (tcgen05, TMEM, TMA).
+//
+// s[n][c] = b[c] + sum_d W[c][d] * x[n][d]  (P:142 hyperplane) as a GEMM
+// X (crops x D, u16 counts) * Q^T where Q holds W split into fixed-point INTEGER digit planes:
+//     W[c][d] ~= m_c * sum_{k<4} 2^-(7+8k) * q_k[c][d],  q_k in [-128, 128],  m_c = 2^e >= max|W[c]|
+// (svm_prepare).  Counts < 1024 and digits are exact in fp16, every product is an integer and
+// every partial sum stays below 2^24 while sum_d x_d < 2^17, so the fp32 tensor-core
+// accumulation is EXACT and order-independent.  The epilogue combines the four digit
+// accumulators in fp64 (exact), adds the bias and rounds once to fp32 -- the oracle's
+// definition up to the 2^-32 m_c quantisation of W.  Rows that break the
+// exactness preconditions (sum_d x_d >= 2^17, detected with an all-ones B row, or a count
+// >= 1024 in the tile) are recomputed in fp64 on CUDA cores by the epilogue thread.
+//
+// Kernel: persistent, one CTA per SM, 6 warps:
+//   warp 0  TMA producer: A = 128 x 64 u16 descriptor tile, B = rows x 64 fp16 digit tile,
+//           both 128-B swizzled, into a ring of `stages` smem stages (mbarrier full/empty)
+//   warp 1  TMEM allocator + single-thread MMA issuer (tcgen05.mma kind::f16, M=128)
+//   warps 2-5  convert the A tile in place u16 -> fp16 (same swizzled byte layout), then
+//           run the epilogue: tcgen05.ld accumulators, fp64 digit combine, bias, argmax.
+// Classes are processed in TMEM passes of <= 124 classes (4 digits each + a ones block =
+// 512 fp32 columns); the running argmax of a crop lives in its epilogue thread's registers.
+#pragma once
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace lbpf {
+
+constexpr int kSvmDigits = 4;
+constexpr int kPassClasses = 124;
+constexpr int kGemmM = 128;
+constexpr int kGemmK = 64;
+constexpr int kBoxRows = 32;
+constexpr int kGemmThreads = 192;
+constexpr uint32_t kPrepMagic = 0x53564D31u;  // "SVM1"
+
+struct SvmPrepHeader {
+    uint32_t magic;
+    int32_t n_classes, dim, dim_pad, n_pass, rows_max, total_rows;
+    int32_t scale_off, q_off;  // byte offsets inside the workspace
+};
+
+__host__ __device__ inline int pass_classes(int C, int p) {
+    const int lo = p * kPassClasses;
+    return (C - lo) < kPassClasses ? (C - lo) : kPassClasses;
+}
+__host__ __device__ inline int pass_rows(int nc) { return ((4 * nc + 16) + 31) / 32 * 32; }
+
+inline bool svm_layout(int32_t C, int32_t D, SvmPrepHeader* h) {
+    if (C < 1 || D < 1 || (D % 8) != 0) return false;  // TMA row stride must be 16-B aligned
+    h->magic = kPrepMagic;
+    h->n_classes = C;
+    h->dim = D;
+    h->dim_pad = (D + kGemmK - 1) / kGemmK * kGemmK;
+    h->n_pass = (C + kPassClasses - 1) / kPassClasses;
+    h->rows_max = pass_rows(pass_classes(C, 0));
+    int rows = 0;
+    for (int p = 0; p < h->n_pass; ++p) rows += pass_rows(pass_classes(C, p));
+    h->total_rows = rows;
+    h->scale_off = 1024;
+    h->q_off = (1024 + 4 * C + 1023) / 1024 * 1024;
+    return true;
+}
+
+inline size_t svm_layout_bytes(const SvmPrepHeader& h) {
+    return (size_t)h.q_off + (size_t)h.total_rows * h.dim_pad * 2;
+}
+
+// ---------------------------------------------------------------------------- prepare
+
+// One block per Q row.  Class rows: digit k of W[c][.]; ones row; zero padding rows.
+__global__ void svm_prepare_kernel(const float* __restrict__ W, SvmPrepHeader h,
+                                   uint8_t* __restrict__ ws) {
+    __shared__ float red[32];
+    const int row = blockIdx.x;
+    if (row == 0 && threadIdx.x == 0) *reinterpret_cast<SvmPrepHeader*>(ws) = h;
+    // locate (pass, local row)
+    int p = 0, base = 0;
+    while (p < h.n_pass && row >= base + pass_rows(pass_classes(h.n_classes, p))) {
+        base += pass_rows(pass_classes(h.n_classes, p));
+        ++p;
+    }
+    const int nc = pass_classes(h.n_classes, p);
+    const int lr = row - base;
+    __half* q = reinterpret_cast<__half*>(ws + h.q_off) + (size_t)row * h.dim_pad;
+    if (lr >= 4 * nc) {  // ones row (column sum check) or zero padding
+        const float v = (lr == 4 * nc) ? 1.0f : 0.0f;
+        for (int d = threadIdx.x; d < h.dim_pad; d += blockDim.x)
+            q[d] = __float2half_rn(d < h.dim ? v : 0.0f);
+        return;
+    }
+    const int c = p * kPassClasses + lr / 4, k = lr % 4;
+    const float* w = W + (size_t)c * h.dim;
+    float mx = 0.0f;
+    for (int d = threadIdx.x; d < h.dim; d += blockDim.x) mx = fmaxf(mx, fabsf(w[d]));
+    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+        for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+        if (threadIdx.x == 0) red[0] = mx;
+    }
+    __syncthreads();
+    mx = red[0];
+    int e = 0;
+    if (mx > 0.0f) frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1) -> m = 2^e >= mx
+    const float m = ldexpf(1.0f, e);
+    if (k == 0 && threadIdx.x == 0) reinterpret_cast<float*>(ws + h.scale_off)[c] = m;
+    for (int d = threadIdx.x; d < h.dim_pad; d += blockDim.x) {
+        float v = d < h.dim ? (w[d] / m) * 128.0f : 0.0f;  // exact: power-of-two scalings
+        float qk = 0.0f;
+        for (int j = 0; j <= k; ++j) {
+            qk = rintf(v);            // in [-128, 128]
+            v = (v - qk) * 256.0f;    // exact residual
+        }
+        q[d] = __float2half_rn(qk);
+    }
+}
+
+// ---------------------------------------------------------------------------- GEMM kernel
+
+struct GemmSmem {
+    int stages, stage_bytes;
+    __device__ __forceinline__ uint8_t* a(uint8_t* base, int s) const { return base + s * stage_bytes; }
+    __device__ __forceinline__ uint8_t* b(uint8_t* base, int s) const {
+        return base + s * stage_bytes + kGemmM * kGemmK * 2;
+    }
+};
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap b_map,
+                const uint16_t* __restrict__ desc, int32_t n, const float* __restrict__ W,
+                const float* __restrict__ bias, const uint8_t* __restrict__ ws, SvmPrepHeader h,
+                int stages, int stage_bytes, float* __restrict__ scores,
+                int32_t* __restrict__ labels, float* __restrict__ top_score,
+                float reject_threshold) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    const GemmSmem L{stages, stage_bytes};
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+    uint64_t* conv = full + stages;
+    uint64_t* empty = conv + stages;
+    uint64_t* tmem_full = empty + stages;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int C = h.n_classes;
+    const int KC = h.dim_pad / kGemmK;
+    const int n_tiles = (n + kGemmM - 1) / kGemmM;
+    const float* scales = reinterpret_cast<const float*>(ws + h.scale_off);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], 4);   // one arrive per converter warp
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 128);
+        fence_mbar_init();
+        prefetch_tensormap(&a_map);
+        prefetch_tensormap(&b_map);
+    }
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                int row0 = 0;
+                for (int p = 0; p < h.n_pass; ++p) {
+                    const int rows = pass_rows(pass_classes(C, p));
+                    for (int kc = 0; kc < KC; ++kc) {
+                        mbar_wait(&empty[s], ph ^ 1);
+                        mbar_arrive_expect_tx(&full[s], kGemmM * kGemmK * 2 + rows * kGemmK * 2);
+                        tma_load_2d(L.a(smem, s), &a_map, &full[s], kc * kGemmK, t * kGemmM);
+                        for (int r = 0; r < rows; r += kBoxRows)
+                            tma_load_2d(L.b(smem, s) + r * 128, &b_map, &full[s], kc * kGemmK, row0 + r);
+                        if (++s == stages) { s = 0; ph ^= 1; }
+                    }
+                    row0 += rows;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (single thread)
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0, acc_ph = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                for (int p = 0; p < h.n_pass; ++p) {
+                    const int rows = pass_rows(pass_classes(C, p));
+                    const int nh = rows > 256 ? 2 : 1;
+                    const int nn = rows / nh;  // N per MMA (multiple of 16)
+                    const uint32_t idesc = idesc_f16_f32(kGemmM, nn);
+                    mbar_wait(tmem_empty, acc_ph ^ 1);  // epilogue drained the accumulators
+                    acc_ph ^= 1;
+                    tc_fence_after();
+                    for (int kc = 0; kc < KC; ++kc) {
+                        mbar_wait(&conv[s], ph);
+                        tc_fence_after();
+                        const uint32_t a_addr = smem_u32(L.a(smem, s));
+                        const uint32_t b_addr = smem_u32(L.b(smem, s));
+#pragma unroll
+                        for (int ks = 0; ks < kGemmK / 16; ++ks) {
+                            const uint64_t ad = umma_desc_sw128(a_addr + ks * 32);
+                            for (int hh = 0; hh < nh; ++hh) {
+                                const uint64_t bd = umma_desc_sw128(b_addr + hh * (nn / 8) * 1024 + ks * 32);
+                                mma_f16_ss(tmem_base + hh * nn, ad, bd, idesc, (kc | ks) != 0);
+                            }
+                        }
+                        mma_commit(&empty[s]);  // stage free once these MMAs complete
+                        if (++s == stages) { s = 0; ph ^= 1; }
+                    }
+                    mma_commit(tmem_full);  // accumulators of this pass complete
+                }
+            }
+        }
+    } else {
+        // ===================== converters + epilogue (warps 2..5, 128 threads)
+        const int et = threadIdx.x - 64;           // 0..127
+        const int quarter = warp & 3;              // TMEM lane quarter accessible by this warp
+        const int row = quarter * 32 + lane;       // accumulator row = crop within the tile
+        int s = 0;
+        uint32_t ph = 0, acc_ph = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const int64_t crop = (int64_t)t * kGemmM + row;
+            float best = 0.0f;
+            int best_c = -1;
+            int class0 = 0;
+            uint32_t flag_or = 0;
+            for (int p = 0; p < h.n_pass; ++p) {
+                const int nc = pass_classes(C, p);
+                for (int kc = 0; kc < KC; ++kc) {
+                    mbar_wait(&full[s], ph);
+                    // u16 counts -> fp16 in place (identical 128-B swizzled byte layout):
+                    // (x | 0x6400) is the fp16 1024 + x for x < 1024; subtract 1024 exactly.
+                    const uint32_t a_addr = smem_u32(L.a(smem, s));
+                    uint32_t big = 0;
+#pragma unroll
+                    for (int j = 0; j < (kGemmM * kGemmK * 2) / (16 * 128); ++j) {
+                        const uint32_t addr = a_addr + (j * 128 + et) * 16;
+                        uint4 v = ld_shared_u32x4(addr);
+                        big |= (v.x | v.y | v.z | v.w) & 0xFC00FC00u;
+                        v.x = u16x2_to_f16x2(v.x);
+                        v.y = u16x2_to_f16x2(v.y);
+                        v.z = u16x2_to_f16x2(v.z);
+                        v.w = u16x2_to_f16x2(v.w);
+                        st_shared_u32x4(addr, v);
+                    }
+                    flag_or |= big;
+                    fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&conv[s]);
+                    if (++s == stages) { s = 0; ph ^= 1; }
+                }
+                // ---- epilogue of this pass
+                const bool tile_big = named_barrier_or(1, 128, flag_or != 0);
+                mbar_wait(tmem_full, acc_ph);
+                acc_ph ^= 1;
+                tc_fence_after();
+                const uint32_t lane_addr = tmem_base + ((uint32_t)(quarter * 32) << 16);
+                // column sum sum_d x_d from the all-ones row (exactness precondition)
+                uint32_t v[16];
+                const uint32_t colsum_bits = tmem_ld1(lane_addr + (uint32_t)(4 * nc));
+                tmem_ld_wait();
+                const float colsum = __uint_as_float(colsum_bits);
+                const bool exact = (colsum < 131072.0f) && !tile_big;
+                for (int c4 = 0; c4 < nc; c4 += 4) {
+                    __syncwarp();
+                    tmem_ld16(lane_addr + (uint32_t)(4 * c4), v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int lc = c4 + j;
+                        if (lc >= nc) break;
+                        const int c = class0 + lc;
+                        double acc;
+                        if (exact) {
+                            const double q = (double)__uint_as_float(v[4 * j + 0]) * 0x1p-7 +
+                                             (double)__uint_as_float(v[4 * j + 1]) * 0x1p-15 +
+                                             (double)__uint_as_float(v[4 * j + 2]) * 0x1p-23 +
+                                             (double)__uint_as_float(v[4 * j + 3]) * 0x1p-31;
+                            acc = (double)__ldg(bias + c) + (double)__ldg(scales + c) * q;
+                        } else {  // fallback: exact fp64 on CUDA cores
+                            acc = (double)__ldg(bias + c);
+                            if (crop < n)
+                                for (int d = 0; d < h.dim; ++d)
+                                    acc += (double)__ldg(W + (size_t)c * h.dim + d) *
+                                           (double)desc[crop * h.dim + d];
+                        }
+                        const float sc = (float)acc;
+                        if (crop < n) {
+                            if (scores) scores[crop * C + c] = sc;
+                            if (best_c < 0 || sc > best) {
+                                best = sc;
+                                best_c = c;
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(tmem_empty);
+                class0 += nc;
+            }
+            if (crop < n) {
+                if (top_score) top_score[crop] = best;
+                if (labels) labels[crop] = (best < reject_threshold) ? -1 : best_c;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem_base, 512);
+}
+
+// ---------------------------------------------------------------------------- host side
+
+inline bool encode_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int esize,
+                      uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_inner,
+                      uint32_t box_outer) {
+    auto fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    (void)esize;
+    return fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline cudaError_t launch_svm_gemm(const uint16_t* desc, int32_t n, int32_t dim, const float* W,
+                                   const float* bias, const SvmPrepHeader& h, const uint8_t* ws,
+                                   float* scores, int32_t* labels, float* top, float reject,
+                                   int sms, cudaStream_t stream) {
+    CUtensorMap am, bm;
+    if (!encode_2d(&am, desc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (uint64_t)dim, (uint64_t)n,
+                   (uint64_t)dim * 2, kGemmK, kGemmM))
+        return cudaErrorNotSupported;
+    if (!encode_2d(&bm, ws + h.q_off, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (uint64_t)h.dim_pad,
+                   (uint64_t)h.total_rows, (uint64_t)h.dim_pad * 2, kGemmK, kBoxRows))
+        return cudaErrorNotSupported;
+    const int stage_bytes = kGemmM * kGemmK * 2 + h.rows_max * kGemmK * 2;
+    const int budget = 220 * 1024;
+    int stages = budget / stage_bytes;
+    stages = stages > 4 ? 4 : stages;
+    if (stages < 2) return cudaErrorNotSupported;
+    const int smem = stages * stage_bytes + 1024 + 256;
+    cudaError_t e = cudaFuncSetAttribute(svm_gemm_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    const int tiles = (n + kGemmM - 1) / kGemmM;
+    const int grid = tiles < sms ? tiles : sms;
+    svm_gemm_kernel<<<grid, kGemmThreads, smem, stream>>>(am, bm, desc, n, W, bias, ws, h, stages,
+                                                          stage_bytes, scores, labels, top, reject);
+    return cudaGetLastError();
+}
+
+}  // namespace lbpf

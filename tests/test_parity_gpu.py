@@ -126,6 +126,24 @@ def test_pitched_frames_config2(lb):
     assert np.array_equal(out.cpu().view(torch.int16).numpy().view(np.uint16), ref)
 
 
+def test_fast_kernel_mixed_rois(lb):
+    """8x8 grid on aligned frames -> the TMA kernel; it must also take clamped, odd-sized,
+    unaligned and invalid ROIs through its internal generic path."""
+    n_frames, H, W = 2, 480, 640
+    grey, depth = synthgen.face_crops(n_frames, H, W, seed=16)
+    rng = np.random.default_rng(7)
+    rois = []
+    for f in range(n_frames):
+        rois += [[f, 0, 0, 128, 128], [f, 16, 32, 128, 128], [f, 3, 5, 128, 128],
+                 [f, W - 100, 10, 128, 128], [f, -20, -20, 128, 128], [f, 50, 60, 100, 90],
+                 [f, 10, 10, 2, 128], [f, 700, 0, 128, 128], [f, 500, 340, 140, 140]]
+        for _ in range(20):
+            rois.append([f, int(rng.integers(0, W - 128)), int(rng.integers(0, H - 128)), 128, 128])
+    _check(lb, grey, depth, np.array(rois, np.int32), 600, 1400, 8, 8, 59)
+    _check(lb, grey, depth, np.array(rois, np.int32), 600, 1400, 8, 8, 256)
+    _check(lb, grey, None, np.array(rois, np.int32), 0, 0, 8, 8, 59)
+
+
 def test_empty_batch(lb):
     g = torch.zeros(1, 8, 8, dtype=torch.uint8, device=DEV)
     r = torch.zeros(0, 5, dtype=torch.int32, device=DEV)
@@ -210,3 +228,63 @@ def test_recognize_host_matches_device_path(lb):
     assert labels_agree_away_from_ties(s_ref, lab.numpy(), lab_ref, desc, W, b)
     ok, _ = svm_tolerance_ok(desc, W, b, top.numpy()[:, None], top_ref[:, None])
     assert ok
+
+
+def test_svm_prepare_digit_roundtrip(lb):
+    """Workspace digits reconstruct W: |m_c sum_k 2^-(7+8k) q_k - W| <= 2^-32 m_c."""
+    C, D = 7, 3776
+    W, _ = synthgen.svm_weights(C, D, seed=5)
+    W[3] = 0.0
+    W[4, 10] = 3.0  # exact power-of-two maximum
+    Wt = torch.from_numpy(W).to(DEV)
+    ws = lb.svm_prepare(Wt)
+    torch.cuda.synchronize()
+    raw = ws.cpu().numpy()
+    scale_off, q_off = 1024, (1024 + 4 * C + 1023) // 1024 * 1024
+    m = raw[scale_off:scale_off + 4 * C].view(np.float32)
+    rows = ((4 * C + 16) + 31) // 32 * 32
+    dpad = (D + 63) // 64 * 64
+    q = raw[q_off:q_off + rows * dpad * 2].view(np.float16).reshape(rows, dpad).astype(np.float64)
+    for c in range(C):
+        assert m[c] >= np.abs(W[c]).max() and np.log2(m[c]) == np.round(np.log2(m[c]))
+        rec = m[c] * sum(q[4 * c + k, :D] * 2.0 ** -(7 + 8 * k) for k in range(4))
+        assert np.abs(q[4 * c:4 * c + 4]).max() <= 128
+        assert np.abs(rec - W[c].astype(np.float64)).max() <= 2.0 ** -32 * m[c]
+    assert (q[4 * C, :D] == 1).all() and (q[4 * C, D:] == 0).all()
+
+
+@pytest.mark.parametrize("C", [130, 250])
+def test_svm_gemm_multi_pass(lb, C):
+    desc, W, b = _svm_inputs(300, C, seed=C)
+    s, lab, top = _gpu_svm(lb, desc, W, b, prepared=True)
+    s_ref, lab_ref, _ = oracle.svm_score(desc, W, b)
+    ok, worst = svm_tolerance_ok(desc, W, b, s, s_ref)
+    assert ok, worst
+    assert labels_agree_away_from_ties(s_ref, lab, lab_ref, desc, W, b)
+
+
+@pytest.mark.parametrize("kind", ["big_count", "big_sum"])
+def test_svm_gemm_exactness_fallback(lb, kind):
+    """Tiles breaking the exact-accumulation preconditions take the fp64 fallback."""
+    rng = np.random.default_rng(3)
+    n, D, C = 200, 3776, 20
+    if kind == "big_count":
+        desc = rng.integers(0, 40, (n, D)).astype(np.uint16)
+        desc[5, 17] = 5000
+        desc[150, 3] = 1024
+    else:
+        desc = rng.integers(0, 1000, (n, D)).astype(np.uint16)  # sum_d x_d >> 2^17
+    W, b = synthgen.svm_weights(C, D, seed=11)
+    s, lab, top = _gpu_svm(lb, desc, W, b, prepared=True)
+    s_ref, lab_ref, _ = oracle.svm_score(desc, W, b)
+    ok, worst = svm_tolerance_ok(desc, W, b, s, s_ref)
+    assert ok, worst
+
+
+def test_svm_single_crop_config1(lb):
+    desc, W, b = _svm_inputs(1, 2, seed=1)
+    for prepared in (False, True):
+        s, lab, top = _gpu_svm(lb, desc, W, b, prepared=prepared)
+        s_ref, lab_ref, _ = oracle.svm_score(desc, W, b)
+        assert svm_tolerance_ok(desc, W, b, s, s_ref)[0]
+        assert labels_agree_away_from_ties(s_ref, lab, lab_ref, desc, W, b)
