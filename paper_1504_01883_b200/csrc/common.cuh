@@ -96,10 +96,13 @@ __device__ __forceinline__ RoiGeom clamp_roi(const lbp_roi_t r, const lbp_images
     return o;
 }
 
-// ROIs handled by the TMA fast kernel: fully inside the image, exactly kFastTile square.
+// ROIs handled by the TMA fast kernel: fully inside the image, exactly kFastTile square, and
+// x a multiple of 16 px (a TMA box must start 16-B aligned in its innermost dimension:
+// tools/tma_probe.cu measured "illegal instruction" for unaligned starts on B200).
 constexpr int kFastTile = 128;
 __device__ __forceinline__ bool roi_is_fast(const lbp_roi_t& r, const lbp_images_t& g) {
     return r.w == kFastTile && r.h == kFastTile && r.img >= 0 && r.img < g.n_images && r.x >= 0 &&
+           (r.x & 15) == 0 &&
            r.y >= 0 && (int64_t)r.x + kFastTile <= g.width && (int64_t)r.y + kFastTile <= g.height;
 }
 
