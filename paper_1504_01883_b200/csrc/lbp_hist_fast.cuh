@@ -41,22 +41,35 @@ struct FastCfg {
     static constexpr int kGreyBytes = kFastTile * kFastTile;
     static constexpr int kDepthBytes = kFastTile * kFastTile * 2;
     static constexpr int kStageBytes = kGreyBytes + kDepthBytes;
-    static constexpr int kHistWords = kFastCells * kFastCells * BINS;
+    static constexpr int kDim = kFastCells * kFastCells * BINS;      // descriptor length
+    // packed histogram: u32 word (cell % 32, bin) holds cell c in its low half and cell c+32
+    // in its high half (counts <= 256 per cell for 128x128 crops, no carry between halves)
+    static constexpr int kHistWords = (kFastCells * kFastCells / 2) * BINS;
     static constexpr int kHistBytes = kHistWords * 4;
-    // per group: stages, histogram, a 128-B "trash" slot that absorbs invalid pixels
-    static constexpr int kGroupBytes = kStages * kStageBytes + kHistBytes + 128;
+    // per group: stages + two histogram buffers (double-buffered across crops)
+    static constexpr int kGroupBytes = kStages * kStageBytes + 2 * kHistBytes;
     static constexpr int kLutOff = kFastGroups * kGroupBytes;          // 256-aligned
     static constexpr int kBarOff = kLutOff + 256;
     static constexpr int kSmemBytes = kBarOff + kFastGroups * kStages * 8 + 1024;  // +align slack
+    static_assert(kLutOff % 256 == 0, "LUT must be 256-B aligned (PRMT address trick)");
+    static_assert(kHistBytes % 16 == 0, "vector epilogue");
 };
+
+// value the compiler must keep in a register (no rematerialisation inside the hot loop)
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
 
 struct FastRow {
     uint32_t h0, h1;   // fp16x2 (1024+g) of columns 4l..4l+1, 4l+2..4l+3
     uint32_t lh0, mh, rh1;  // shifted pairs: (4l-1,4l), (4l+1,4l+2), (4l+3,4l+4)
 };
 
-__device__ __forceinline__ FastRow make_row(uint32_t grey_row_addr, int lane) {
-    const uint32_t w = ld_shared_u32(grey_row_addr + 4 * lane);
+// grey_word_addr: smem address of this lane's 4 pixels (columns 4l..4l+3) of the row
+__device__ __forceinline__ FastRow make_row(uint32_t grey_word_addr, int lane) {
+    (void)lane;
+    const uint32_t w = ld_shared_u32(grey_word_addr);
     FastRow r;
     r.h0 = prmt(w, 0x64646464u, 0x5140);  // [g0, 0x64, g1, 0x64]
     r.h1 = prmt(w, 0x64646464u, 0x7362);  // [g2, 0x64, g3, 0x64]
@@ -68,19 +81,40 @@ __device__ __forceinline__ FastRow make_row(uint32_t grey_row_addr, int lane) {
     return r;
 }
 
-// Eq. 2 for the two pixels of fp16x2 centre `c`: bit p of each 16-bit half = [g_p >= g_c].
+__device__ __forceinline__ uint32_t hfma2_sat(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("fma.rn.sat.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+// Eq. 2 for the two pixels of fp16x2 centre `c` (values 1024+g).  Returns per 16-bit half
+// 0x64 | code (code = sum_p [g_p >= g_c] 2^p, Fig. 7 weights).  Half of the eight
+// comparisons run on the FMA pipe as sat(g_p - g_c + 1) in {0,1} accumulated with the weight
+// onto 1024.0 (exact small integers in fp16), half on the ALU pipe as HSET2 masks merged
+// with LOP3, which balances the two pipes.
 __device__ __forceinline__ uint32_t code2(uint32_t c, uint32_t tl, uint32_t t, uint32_t tr,
                                           uint32_t r, uint32_t br, uint32_t b, uint32_t bl,
                                           uint32_t l) {
-    uint32_t acc = hge2_mask(tl, c) & 0x00010001u;
-    acc |= hge2_mask(t, c) & 0x00020002u;
-    acc |= hge2_mask(tr, c) & 0x00040004u;
-    acc |= hge2_mask(r, c) & 0x00080008u;
-    acc |= hge2_mask(br, c) & 0x00100010u;
-    acc |= hge2_mask(b, c) & 0x00200020u;
-    acc |= hge2_mask(bl, c) & 0x00400040u;
-    acc |= hge2_mask(l, c) & 0x00800080u;
+    constexpr uint32_t kOne = 0x3C003C00u, kMinusOne = 0xBC00BC00u, k1024 = 0x64006400u;
+    const uint32_t negc1 = hfma2(c, kMinusOne, kOne);  // 1 - g_c
+    uint32_t acc = hfma2(hfma2_sat(tl, kOne, negc1), kOne, k1024);         // TL  1
+    acc = hfma2(hfma2_sat(t, kOne, negc1), 0x40004000u, acc);              // T   2
+    acc = hfma2(hfma2_sat(tr, kOne, negc1), 0x44004400u, acc);             // TR  4
+    acc = hfma2(hfma2_sat(r, kOne, negc1), 0x48004800u, acc);              // R   8
+    acc |= hge2_mask(br, c) & 0x00100010u;                                 // BR  16
+    acc |= hge2_mask(b, c) & 0x00200020u;                                  // B   32
+    acc |= hge2_mask(bl, c) & 0x00400040u;                                 // BL  64
+    acc |= hge2_mask(l, c) & 0x00800080u;                                  // L   128
     return acc;
+}
+
+__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 template <int BINS, bool HAS_DEPTH>
@@ -101,13 +135,13 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
     const int gtid = tid % kFastGroupThreads;
     const int warp = gtid >> 5, lane = gtid & 31;
     uint8_t* gbase = smem + group * Cfg::kGroupBytes;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(gbase + S * Cfg::kStageBytes);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(gbase + S * Cfg::kStageBytes);  // 2 buffers
     uint8_t* lut = smem + Cfg::kLutOff;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff) + group * S;
 
     // ---- one-time setup
     if (tid < 256) lut[tid] = (BINS == 59) ? (uint8_t)(kUniformLutDev.v[tid] * 4) : (uint8_t)tid;
-    for (int i = gtid; i < Cfg::kHistWords; i += kFastGroupThreads) hist[i] = 0;
+    for (int i = gtid; i < 2 * Cfg::kHistWords; i += kFastGroupThreads) hist[i] = 0;
     if (gtid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
@@ -129,24 +163,30 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (HAS_DEPTH) tma_load_3d(st + Cfg::kGreyBytes, &depth_map, &bars[s], r.x, r.y, r.img);
     };
 
-    // per-lane constants: cell byte offsets and border masks of the 4 columns 4l..4l+3
+    // per-lane constants of the 4 columns 4l..4l+3: packed-histogram word offset of the cell,
+    // depth-window bounds (border columns get an empty window: no code exists there)
+    // increment of a valid pixel: +1 in the low half (cell rows 0..3) or the high half (4..7);
+    // 0 for the 1-px ROI border (no code there) and for an empty depth window
+    const uint32_t half_mult = (warp >= 4) ? 0x10000u : 1u;
     uint32_t cell_off[4];
-    uint32_t lo_k[4];
-    bool inner[4];
+    uint32_t mult[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int x = 4 * lane + k;             // column inside the ROI
-        inner[k] = (x != 0) && (x != kFastTile - 1);  // the 1-px ROI border has no code
-        const int cx = inner[k] ? (8 * x - 1) / (kFastTile - 2) : 0;  // ((j+1)*Kx-1)/W', j=x-1
-        cell_off[k] = (uint32_t)((warp * kFastCells + cx) * BINS * 4);
-        // border / empty window: make (d - lo) wrap above any span
-        lo_k[k] = (!inner[k] || win.none_valid) ? 0x80000000u : win.lo;
+        const bool inner = (x != 0) && (x != kFastTile - 1);
+        const int cx = inner ? (8 * x - 1) / (kFastTile - 2) : 0;  // ((j+1)*Kx-1)/W', j=x-1
+        cell_off[k] = (uint32_t)(((warp & 3) * kFastCells + cx) * BINS * 4);
+        mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? half_mult : 0u);
     }
+    // depth window on a u16 held in either half of a word w = d_hi:d_lo:
+    //   lo <= d_lo <= lo+span  <=>  (w << 16) - (lo << 16)  <= (span << 16) | 0xFFFF  (u32)
+    //   lo <= d_hi <= lo+span  <=>   w        - (lo << 16)  <= (span << 16) | 0xFFFF  (u32)
+    const uint32_t lo16 = win.lo << 16;
+    const uint32_t span16 = (win.span << 16) | 0xFFFFu;
     const int i0 = (warp * (kFastTile - 2)) / kFastCells;        // first interior row
     const int i1 = ((warp + 1) * (kFastTile - 2)) / kFastCells;  // end
-    const uint32_t hist_addr = smem_u32(hist);
+    const uint32_t hist_addr0 = smem_u32(hist);
     const uint32_t lut_addr = smem_u32(lut);
-    const uint32_t trash_addr = hist_addr + Cfg::kHistBytes;
 
     // prologue: fill the pipeline
     int32_t next_issue = gid;  // next crop index to be loaded (in this group's sequence)
@@ -159,6 +199,7 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
     }
     uint32_t phase_bits = 0;
     int stage = 0;
+    int hbuf = 0;
 
     struct GroupSync {
         uint32_t id;
@@ -167,9 +208,11 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
     for (int32_t n = gid; n < n_rois; n += n_groups) {
         const lbp_roi_t r = rois[n];
         if (!roi_is_fast(r, geom)) {  // clamped / odd-sized ROI: generic path, same group
+            named_barrier_sync(bar_id, kFastGroupThreads);  // previous epilogue finished
             extract_roi_generic<BINS, kFastGroupThreads>(
                 grey, HAS_DEPTH ? depth : nullptr, geom, r, n, win, kFastCells, kFastCells, desc,
-                roi_status, hist, Cfg::kHistWords, lut, BINS == 59 ? 2 : 0, gtid, GroupSync{bar_id});
+                roi_status, hist, 2 * Cfg::kHistWords, lut, BINS == 59 ? 2 : 0, gtid,
+                GroupSync{bar_id});
             named_barrier_sync(bar_id, kFastGroupThreads);
             continue;
         }
@@ -178,43 +221,53 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
         const uint8_t* st = gbase + stage * Cfg::kStageBytes;
         const uint32_t g_addr = smem_u32(st);
         const uint32_t d_addr = smem_u32(st + Cfg::kGreyBytes);
+        const uint32_t hist_addr = hist_addr0 + hbuf * Cfg::kHistBytes;
 
-        // ---- hot loop: rows of this warp's cell row
-        FastRow top = make_row(g_addr + i0 * kFastTile, lane);
-        FastRow mid = make_row(g_addr + (i0 + 1) * kFastTile, lane);
-        const uint32_t row_hist = hist_addr;
-#pragma unroll 2
-        for (int i = i0; i < i1; ++i) {
-            const FastRow bot = make_row(g_addr + (i + 2) * kFastTile, lane);
+        // ---- hot loop: rows of this warp's cell row (15 or 16 rows; fully unrolled so the
+        // three rolling rows never move between registers)
+        const uint32_t h_addr = opaque(hist_addr);
+        uint32_t cell_addr[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cell_addr[k] = opaque(h_addr + cell_off[k]);
+        const uint32_t g0 = opaque(g_addr + i0 * kFastTile + 4 * lane);   // this lane's word, row i0
+        const uint32_t d_row = opaque(d_addr + (i0 + 1) * (kFastTile * 2) + 8 * lane);
+        auto do_row = [&](const FastRow& top, const FastRow& mid, const FastRow& bot, int i) {
             // left pixel pair (4l, 4l+1) and right pair (4l+2, 4l+3)
             const uint32_t a0 = code2(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
                                       bot.lh0, mid.lh0);
             const uint32_t a1 = code2(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
                                       bot.mh, mid.mh);
-            bool valid[4];
+            uint32_t val[4];
             if (HAS_DEPTH) {
-                const uint2 d = ld_shared_u32x2(d_addr + (i + 1) * (kFastTile * 2) + 8 * lane);
-                valid[0] = ((d.x & 0xFFFFu) - lo_k[0]) <= win.span;
-                valid[1] = ((d.x >> 16) - lo_k[1]) <= win.span;
-                valid[2] = ((d.y & 0xFFFFu) - lo_k[2]) <= win.span;
-                valid[3] = ((d.y >> 16) - lo_k[3]) <= win.span;
+                const uint2 d = ld_shared_u32x2(d_row + (i - i0) * (kFastTile * 2));
+                const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
+                                       d.y - lo16};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) val[k] = (x[k] <= span16) ? mult[k] : 0u;
             } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) valid[k] = inner[k];
+                for (int k = 0; k < 4; ++k) val[k] = mult[k];
             }
             const uint32_t codes[4] = {prmt(a0, lut_addr, 0x7650), prmt(a0, lut_addr, 0x7652),
                                        prmt(a1, lut_addr, 0x7650), prmt(a1, lut_addr, 0x7652)};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                // invalid (masked / border) pixels go to the trash word: unpredicated ATOMS,
-                // same-address increments are aggregated by the hardware (ATOMS.POPC.INC)
+                // masked / border pixels add 0 (no branch, no predicate)
                 const uint32_t off = (BINS == 59) ? ld_shared_u8(codes[k]) : (codes[k] & 0xFFu) * 4;
-                red_shared_inc(valid[k] ? row_hist + cell_off[k] + off : trash_addr);
+                red_shared_add(cell_addr[k] + off, val[k]);
             }
-            top = mid;
-            mid = bot;
+        };
+        FastRow r0 = make_row(g0, lane), r1 = make_row(g0 + kFastTile, lane), r2;
+        const int nrows = i1 - i0;  // 15 or 16, warp-uniform
+#pragma unroll
+        for (int j = 0; j < 16; j += 3) {
+            if (j < nrows) { r2 = make_row(g0 + (j + 2) * kFastTile, lane); do_row(r0, r1, r2, i0 + j); }
+            if (j + 1 < nrows) { r0 = make_row(g0 + (j + 3) * kFastTile, lane); do_row(r1, r2, r0, i0 + j + 1); }
+            if (j + 2 < nrows) { r1 = make_row(g0 + (j + 4) * kFastTile, lane); do_row(r2, r0, r1, i0 + j + 2); }
         }
-        named_barrier_sync(bar_id, kFastGroupThreads);  // stage consumed, all increments done
+        // stage consumed, all increments of this crop done; also guarantees the epilogue of
+        // the previous crop (other histogram buffer) has finished everywhere
+        named_barrier_sync(bar_id, kFastGroupThreads);
 
         // refill this stage with the group's next fast crop
         if (gtid == 0) {
@@ -222,23 +275,23 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
             if (next_issue < n_rois) issue(next_issue, stage);
             next_issue += n_groups;
         }
-        // ---- epilogue: u32 -> u16 descriptor, 16-B stores, re-zero counters
-        uint4* out = reinterpret_cast<uint4*>(desc + (int64_t)n * Cfg::kHistWords);
+        // ---- epilogue: packed u16 halves -> descriptor (16-B stores), re-zero this buffer.
+        // Low halves are cells 0..31 (desc[0, 32*BINS)), high halves cells 32..63.
+        uint4* out_lo = reinterpret_cast<uint4*>(desc + (int64_t)n * Cfg::kDim);
+        uint4* out_hi = reinterpret_cast<uint4*>(desc + (int64_t)n * Cfg::kDim + Cfg::kHistWords);
         for (int c = gtid; c < Cfg::kHistWords / 8; c += kFastGroupThreads) {
-            const uint4 lo4 = ld_shared_u32x4(hist_addr + c * 32);
-            const uint4 hi4 = ld_shared_u32x4(hist_addr + c * 32 + 16);
-            uint4 v;
-            v.x = prmt(lo4.x, lo4.y, 0x5410);
-            v.y = prmt(lo4.z, lo4.w, 0x5410);
-            v.z = prmt(hi4.x, hi4.y, 0x5410);
-            v.w = prmt(hi4.z, hi4.w, 0x5410);
-            out[c] = v;
+            const uint4 w0 = ld_shared_u32x4(hist_addr + c * 32);
+            const uint4 w1 = ld_shared_u32x4(hist_addr + c * 32 + 16);
+            out_lo[c] = make_uint4(prmt(w0.x, w0.y, 0x5410), prmt(w0.z, w0.w, 0x5410),
+                                   prmt(w1.x, w1.y, 0x5410), prmt(w1.z, w1.w, 0x5410));
+            out_hi[c] = make_uint4(prmt(w0.x, w0.y, 0x7632), prmt(w0.z, w0.w, 0x7632),
+                                   prmt(w1.x, w1.y, 0x7632), prmt(w1.z, w1.w, 0x7632));
             st_shared_u32x4(hist_addr + c * 32, make_uint4(0, 0, 0, 0));
             st_shared_u32x4(hist_addr + c * 32 + 16, make_uint4(0, 0, 0, 0));
         }
         if (gtid == 0 && roi_status) roi_status[n] = LBP_OK;
-        named_barrier_sync(bar_id, kFastGroupThreads);  // counters zeroed before next crop
         stage = (stage + 1 == S) ? 0 : stage + 1;
+        hbuf ^= 1;
     }
 }
 

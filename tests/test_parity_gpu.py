@@ -231,7 +231,7 @@ def test_recognize_host_matches_device_path(lb):
 
 
 def test_svm_prepare_digit_roundtrip(lb):
-    """Workspace digits reconstruct W: |m_c sum_k 2^-(7+8k) q_k - W| <= 2^-32 m_c."""
+    """Workspace digits reconstruct W: |m_c sum_k 2^-(8+9k) q_k - W| <= 2^-36 m_c."""
     C, D = 7, 3776
     W, _ = synthgen.svm_weights(C, D, seed=5)
     W[3] = 0.0
@@ -247,9 +247,9 @@ def test_svm_prepare_digit_roundtrip(lb):
     q = raw[q_off:q_off + rows * dpad * 2].view(np.float16).reshape(rows, dpad).astype(np.float64)
     for c in range(C):
         assert m[c] >= np.abs(W[c]).max() and np.log2(m[c]) == np.round(np.log2(m[c]))
-        rec = m[c] * sum(q[4 * c + k, :D] * 2.0 ** -(7 + 8 * k) for k in range(4))
-        assert np.abs(q[4 * c:4 * c + 4]).max() <= 128
-        assert np.abs(rec - W[c].astype(np.float64)).max() <= 2.0 ** -32 * m[c]
+        rec = m[c] * sum(q[4 * c + k, :D] * 2.0 ** -(8 + 9 * k) for k in range(4))
+        assert np.abs(q[4 * c:4 * c + 4]).max() <= 256
+        assert np.abs(rec - W[c].astype(np.float64)).max() <= 2.0 ** -36 * m[c]
     assert (q[4 * C, :D] == 1).all() and (q[4 * C, D:] == 0).all()
 
 
