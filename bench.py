@@ -134,21 +134,13 @@ class ClockSampler:
 # --------------------------------------------------------------------------- CPU oracle
 
 def oracle_rate(grey, depth, rois, W, b, cx, cy, bins, budget_s, threads):
-    """Times the UNMODIFIED oracle (extraction + SVM) on T threads over disjoint shards.
+    """Times the UNMODIFIED oracle (extraction + SVM) on T threads over disjoint shards of the
+    sample, repeating passes over the sample until about `budget_s` seconds have elapsed.
 
-    Returns (crops/s, crops processed, seconds, descriptors, labels) for the sample."""
+    Returns (crops/s, crops processed, seconds, passes, descriptors, labels of one pass)."""
     import oracle
     n = grey.shape[0]
-    # calibrate on a few crops single-threaded
-    k = min(n, 8)
-    t0 = time.perf_counter()
-    d = oracle.lbp_extract(grey[:k], depth[:k] if depth is not None else None,
-                           _local_rois(rois[:k]), DMIN, DMAX, cx, cy, bins)
-    oracle.svm_score(d, W, b)
-    per_crop = (time.perf_counter() - t0) / k
-    m = int(max(threads, min(n, budget_s * threads / max(per_crop, 1e-9))))
-    m = min(m, n)
-    shards = np.array_split(np.arange(m), threads)
+    shards = np.array_split(np.arange(n), threads)
     out_desc = [None] * threads
     out_lab = [None] * threads
 
@@ -161,16 +153,20 @@ def oracle_rate(grey, depth, rois, W, b, cx, cy, bins, budget_s, threads):
         _, lab, _ = oracle.svm_score(dd, W, b)
         out_desc[i], out_lab[i] = dd, lab
 
-    ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
-    t0 = time.perf_counter()
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    dt = time.perf_counter() - t0
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        passes += 1
+        dt = time.perf_counter() - t0
+        if dt >= budget_s or passes >= 1000:
+            break
     desc = np.concatenate([x for x in out_desc if x is not None])
     lab = np.concatenate([x for x in out_lab if x is not None])
-    return m / dt, m, dt, desc, lab
+    return n * passes / dt, n * passes, dt, passes, desc, lab
 
 
 def _local_rois(rois):
@@ -421,10 +417,10 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
     g = grey[:m].cpu().numpy()
     d = depth[:m].cpu().view(torch.int16).numpy().view(np.uint16) if depth is not None else None
     r = rois[:m].cpu().numpy()
-    rate, done, secs, odesc, olab = oracle_rate(g, d, r, W_np, b_np, cx, cy, bins,
-                                                args.cpu_seconds, threads)
-    gdesc = desc[:done].cpu().view(torch.int16).numpy().view(np.uint16)
-    glab = labels[:done].cpu().numpy()
+    rate, done, secs, passes, odesc, olab = oracle_rate(g, d, r, W_np, b_np, cx, cy, bins,
+                                                        args.cpu_seconds, threads)
+    gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
+    glab = labels[:m].cpu().numpy()
     ok = bool(np.array_equal(gdesc, odesc))
     if ok:
         import oracle
@@ -433,8 +429,9 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
         clear = (srt[:, -1] - srt[:, -2]) > 1e-4 * np.maximum(np.abs(srt[:, -1]), 1e-3)
         ok = bool(np.array_equal(glab[clear], olab[clear]))
     cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
-           "sample": f"first {done} crops of this workload (extraction + SVM), {threads} threads "
-                     f"x unmodified single-threaded C oracle on disjoint shards, {secs:.1f} s",
+           "sample": f"first {m} crops of this workload x {passes} passes = {done} crops "
+                     f"(extraction + SVM), {threads} threads x unmodified single-threaded C "
+                     f"oracle on disjoint shards, {secs:.1f} s",
            "cpu": cpu_model(), "equivalence_gate": "pass" if ok else "FAIL"}
     return cpu, ok
 
