@@ -55,12 +55,6 @@ struct FastCfg {
     static_assert(kHistBytes % 16 == 0, "vector epilogue");
 };
 
-// value the compiler must keep in a register (no rematerialisation inside the hot loop)
-__device__ __forceinline__ uint32_t opaque(uint32_t v) {
-    asm volatile("mov.b32 %0, %0;" : "+r"(v));
-    return v;
-}
-
 struct FastRow {
     uint32_t h0, h1;   // fp16x2 (1024+g) of columns 4l..4l+1, 4l+2..4l+3
     uint32_t lh0, mh, rh1;  // shifted pairs: (4l-1,4l), (4l+1,4l+2), (4l+3,4l+4)
@@ -111,10 +105,6 @@ __device__ __forceinline__ uint32_t code2(uint32_t c, uint32_t tl, uint32_t t, u
     acc |= hge2_mask(bl, c) & 0x00400040u;                                 // BL  64
     acc |= hge2_mask(l, c) & 0x00800080u;                                  // L   128
     return acc;
-}
-
-__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 template <int BINS, bool HAS_DEPTH>

@@ -59,6 +59,16 @@ __device__ __forceinline__ void red_shared_inc(uint32_t addr) {
     asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 }
 
+__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// value the compiler must keep in a register (no rematerialisation inside the hot loop)
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+
 // predicated variant: no branch, the predicate guards the ATOMS itself
 __device__ __forceinline__ void red_shared_inc_if(uint32_t addr, bool pred) {
     asm volatile(
