@@ -6,7 +6,7 @@
 #include "common.cuh"
 #include "lbp_hist_generic.cuh"
 #include "lbp_hist_fast.cuh"
-#include "lbp_hist_fast59.cuh"
+#include "lbp_hist_lane59.cuh"
 #include "svm_fp64.cuh"
 #include "svm_gemm.cuh"
 
@@ -79,9 +79,6 @@ int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images
     // Fast path (8x8 cells, 16-B aligned rows): one TMA-staged persistent kernel; ROIs that
     // are not fully-inside 128x128 boxes take the generic code path inside it.
     if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc)) {
-        if (bins == 59)  // bank-conflict-free half-crop kernel
-            return launch_status(launch_lbp_hist_fast59(grey, depth, geom, rois, n_rois, win,
-                                                        desc, roi_status, num_sms(), stream));
         return launch_status(launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins,
                                                   desc, roi_status, num_sms(), stream));
     }
