@@ -79,6 +79,9 @@ int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images
     // Fast path (8x8 cells, 16-B aligned rows): one TMA-staged persistent kernel; ROIs that
     // are not fully-inside 128x128 boxes take the generic code path inside it.
     if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc)) {
+        if (bins == 59)  // conflict-free lane-private kernel (the headline configuration)
+            return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win,
+                                                        desc, roi_status, num_sms(), stream));
         return launch_status(launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins,
                                                   desc, roi_status, num_sms(), stream));
     }
