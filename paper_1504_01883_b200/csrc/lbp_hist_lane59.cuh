@@ -13,7 +13,7 @@
 //    so lane l reads bank l; the compare results are accumulated directly into that offset;
 //  * only grey is staged by TMA (16 KB per crop, 3 stages per group); depth is read straight
 //    from global memory, 8 B per lane per row (256 B coalesced per warp row), prefetched
-//    4 rows ahead in registers and across crop boundaries.
+//    8 rows ahead in registers and across crop boundaries.
 // Structure: persistent, 1 CTA/SM, 2 independent groups of 8 warps; warp w of a group owns
 // cell row w of its current crop; lane l owns columns 4l..4l+3.  One named barrier per crop
 // per group (counters double-buffered); the epilogue writes the 7,552-B descriptor into a
@@ -59,12 +59,11 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+// read-only 8-B global load; plain (non-volatile) so the compiler can keep the destination
+// in the prefetch-ring register (a volatile asm load was followed by a register move that
+// stalled on the load and defeated the prefetch)
 __device__ __forceinline__ uint2 ld_global_nc_v2(const void* p) {
-    uint2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
-                 : "=r"(v.x), "=r"(v.y)
-                 : "l"(p));
-    return v;
+    return __ldg(reinterpret_cast<const uint2*>(p));
 }
 __device__ __forceinline__ uint32_t f16_fma_sat(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r;
@@ -193,7 +192,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         return depth + (int64_t)r.img * geom.depth_img_stride +
                (int64_t)(r.y + i0 + 1 + j) * geom.depth_pitch + r.x + 4 * lane;
     };
-    uint2 dq[4];  // prefetch ring (rows j .. j+3)
+    constexpr int kPre = 8;  // depth prefetch distance (rows)
+    uint2 dq[kPre];  // prefetch ring (rows j .. j+kPre-1)
     bool prefetched = false;
 
     struct GroupSync {
@@ -229,7 +229,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         if (HAS_DEPTH && !prefetched) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dq[j] = ld_global_nc_v2(depth_row_ptr(roi, j));
+            for (int j = 0; j < kPre; ++j) dq[j] = ld_global_nc_v2(depth_row_ptr(roi, j));
         }
 
         mbar_wait(&bars[stage], (phase_bits >> stage) & 1u);
@@ -247,15 +247,16 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                                             bot.h1, bot.mh, mid.mh);
             uint32_t val[4];
             if (HAS_DEPTH) {
-                const uint2 d = dq[j & 3];
-                // refill the ring slot: row j+4 of this crop; in the last 4 rows (which cover all
-                // four slots) row (j & 3) of the group's next crop, consumed from slot j & 3
-                const int jn = j + 4;
-                if (jn < nrows) {
-                    dq[j & 3] = ld_global_nc_v2(depth_row_ptr(roi, jn));
-                } else if (next_ok) {
-                    dq[j & 3] = ld_global_nc_v2(depth_row_ptr(nroi, j & 3));
-                }
+                const uint2 d = dq[j % kPre];
+                // refill the ring slot: row j+kPre of this crop; in the last kPre rows (which
+                // cover every slot) row j % kPre of the group's next crop, read from that slot
+                // (one unconditional load from a selected address, so that the compiler writes
+                // the ring register directly; without a next crop it harmlessly re-reads row 0)
+                const int jn = j + kPre;
+                const uint16_t* src = (jn < nrows) ? depth_row_ptr(roi, jn)
+                                                   : depth_row_ptr(next_ok ? nroi : roi,
+                                                                   next_ok ? j % kPre : 0);
+                dq[j % kPre] = ld_global_nc_v2(src);
                 // depth window on a u16 in either half of a word
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
