@@ -171,7 +171,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
 
     // ---- per-lane / per-warp constants
     const uint32_t byte_mult = 1u << (8 * (warp & 3));
-    uint32_t col_off[4], mult[4];
+    uint32_t col_off[4], mult[4], mult_row[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int x = 4 * lane + k;
@@ -180,6 +180,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int col = (cx == (lane >> 2)) ? lane : 4 * cx;  // spill-over -> next cell's lane
         col_off[k] = (uint32_t)(((warp >> 2) * kBins * 32 + col) * 4);
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
+        mult_row[k] = mult[k];
     }
     const uint32_t lo16 = win.lo << 16;
     const uint32_t span16 = (win.span << 16) | 0xFFFFu;
@@ -252,19 +253,19 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 // cover every slot) row j % kPre of the group's next crop, read from that slot
                 // (one unconditional load from a selected address, so that the compiler writes
                 // the ring register directly; without a next crop it harmlessly re-reads row 0)
-                const int jn = j + kPre;
-                const uint16_t* src = (jn < nrows) ? depth_row_ptr(roi, jn)
-                                                   : depth_row_ptr(next_ok ? nroi : roi,
-                                                                   next_ok ? j % kPre : 0);
+                const int jn = j + kPre;  // compile-time: rows 0..15 of every crop
+                const uint16_t* src = (jn < 16) ? depth_row_ptr(roi, jn)
+                                                : depth_row_ptr(next_ok ? nroi : roi,
+                                                                next_ok ? j % kPre : 0);
                 dq[j % kPre] = ld_global_nc_v2(src);
                 // depth window on a u16 in either half of a word
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) val[k] = (x[k] <= span16) ? mult[k] : 0u;
+                for (int k = 0; k < 4; ++k) val[k] = (x[k] <= span16) ? mult_row[k] : 0u;
             } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) val[k] = mult[k];
+                for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
             }
             const uint32_t la[4] = {lut_lane + (t0 & 0xFFFFu), __umulhi(t0, 0x10000u) + lut_lane,
                                     lut_lane + (t1 & 0xFFFFu), __umulhi(t1, 0x10000u) + lut_lane};
@@ -274,13 +275,25 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 red_shared_add(colb[k] + bin * (32 * 4), val[k]);
             }
         };
+        // 16 rows, straight-line (no branches: a conditional row block made the compiler copy
+        // prefetched registers at the block end, stalling on the load).  Cell rows with 15
+        // rows run a 16th dummy row whose increments are 0 (its pixels belong to the next
+        // warp's cell row; the rows it touches exist inside the crop).
         LaneRow r0 = lane_row(g0), r1 = lane_row(g0 + kTile), r2;
 #pragma unroll
-        for (int j = 0; j < 16; j += 3) {
-            if (j < nrows) { r2 = lane_row(g0 + (j + 2) * kTile); do_row(r0, r1, r2, j); }
-            if (j + 1 < nrows) { r0 = lane_row(g0 + (j + 3) * kTile); do_row(r1, r2, r0, j + 1); }
-            if (j + 2 < nrows) { r1 = lane_row(g0 + (j + 4) * kTile); do_row(r2, r0, r1, j + 2); }
+        for (int j = 0; j < 15; j += 3) {
+            r2 = lane_row(g0 + (j + 2) * kTile); do_row(r0, r1, r2, j);
+            r0 = lane_row(g0 + (j + 3) * kTile); do_row(r1, r2, r0, j + 1);
+            r1 = lane_row(g0 + (j + 4) * kTile); do_row(r2, r0, r1, j + 2);
         }
+        if (nrows < 16) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
+        }
+        r2 = lane_row(g0 + 17 * kTile);
+        do_row(r0, r1, r2, 15);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
         prefetched = next_ok;
 
         // staging writes of the previous epilogue -> visible to the bulk-copy engine; the
