@@ -11,14 +11,14 @@
 //    lanes of a cell are summed in the epilogue (one 16-B load, a byte transpose, IDP4A);
 //  * the uniform-bin LUT is lane-banked: bin(c) lives at byte (c>>2)*128 + 4*lane + (c&3),
 //    so lane l reads bank l; the compare results are accumulated directly into that offset;
-//  * only grey is staged by TMA (16 KB per crop, 3 stages per group); depth is read straight
-//    from global memory, 8 B per lane per row (256 B coalesced per warp row), prefetched
-//    8 rows ahead in registers and across crop boundaries.
-// Structure: persistent, 1 CTA/SM, 2 independent groups of 8 warps; warp w of a group owns
-// cell row w of its current crop; lane l owns columns 4l..4l+3.  One named barrier per crop
-// per group (counters double-buffered); the epilogue writes the 7,552-B descriptor into a
-// smem staging buffer (double-buffered) and a bulk async copy stores it.  ROIs that are not
-// fully-inside 16-px-aligned 128x128 boxes take the generic path inside the same kernel.
+//  * grey and depth of a crop (48 KB) are staged by TMA into a ring of 3 stages shared by
+//    the CTA's two groups (crop position i of the CTA -> stage i%3, group i%2); the group
+//    that finishes position i refills its stage with position i+3.
+// Structure: persistent, 1 CTA/SM, 2 groups of 8 warps; warp w of a group owns cell row w
+// of its crop (with Ky = 8 the floor partition of the 126 interior rows is exactly the
+// warp's rows), lane l owns columns 4l..4l+3.  The epilogue writes the 7,552-B descriptor
+// into a smem staging buffer and a bulk async copy (cp.async.bulk) stores it.  ROIs that are
+// not fully-inside 16-px-aligned 128x128 boxes take the generic path inside the same kernel.
 #pragma once
 #include <cudaTypedefs.h>
 
@@ -36,15 +36,18 @@ constexpr int kTile = 128;
 constexpr int kBins = 59;
 constexpr int kStages = 3;
 constexpr int kGreyBytes = kTile * kTile;                      // 16,384
+constexpr int kStageBytes = kGreyBytes + 2 * kTile * kTile;    // + depth 32,768 = 49,152
 constexpr int kHistBytes = 2 * kBins * 32 * 4;                 // [g][bin][lane] = 15,104
 constexpr int kDescBytes = 64 * kBins * 2;                     // 7,552
-constexpr int kGroupBytes = kStages * kGreyBytes + 2 * kHistBytes + 2 * kDescBytes;  // 94,464
-constexpr int kLutOff = kGroups * kGroupBytes;                 // 188,928 (256-aligned)
+constexpr int kGroupOff = kStages * kStageBytes;               // 147,456
+constexpr int kGroupBytes = kHistBytes + kDescBytes;           // 22,656
+constexpr int kLutOff = kGroupOff + kGroups * kGroupBytes;     // 192,768 (256-aligned)
 constexpr int kLutBytes = 64 * 128;
 constexpr int kPlainLutOff = kLutOff + kLutBytes;
 constexpr int kBarOff = kPlainLutOff + 256;
-constexpr int kSmemBytes = kBarOff + kGroups * kStages * 8 + 1024;
+constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;        // + 128-B alignment slack
 static_assert(kGroupBytes % 128 == 0 && kLutOff % 256 == 0, "alignment");
+static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 }  // namespace l59
 
 __device__ __forceinline__ void bulk_store_s2g(void* gdst, uint32_t ssrc, uint32_t bytes) {
@@ -58,12 +61,6 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-// read-only 8-B global load; plain (non-volatile) so the compiler can keep the destination
-// in the prefetch-ring register (a volatile asm load was followed by a register move that
-// stalled on the load and defeated the prefetch)
-__device__ __forceinline__ uint2 ld_global_nc_v2(const void* p) {
-    return __ldg(reinterpret_cast<const uint2*>(p));
 }
 __device__ __forceinline__ uint32_t f16_fma_sat(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r;
@@ -118,67 +115,70 @@ __device__ __forceinline__ uint32_t lbp_offset2(uint32_t c, uint32_t tl, uint32_
 template <bool HAS_DEPTH>
 __global__ void __launch_bounds__(l59::kThreads, 1)
 lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
+                       const __grid_constant__ CUtensorMap depth_map,
                        const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
                        lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
                        DepthWindow win, uint16_t* __restrict__ desc,
                        int32_t* __restrict__ roi_status) {
     using namespace l59;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                               ~uintptr_t(127));
     const int tid = threadIdx.x;
     const int group = tid / kGroupThreads, gtid = tid % kGroupThreads;
     const int warp = gtid >> 5, lane = gtid & 31;
-    uint8_t* gbase = smem + group * kGroupBytes;
-    const uint32_t stage0 = smem_u32(gbase);
-    const uint32_t hist0 = stage0 + kStages * kGreyBytes;
-    const uint32_t staging0 = hist0 + 2 * kHistBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff) + group * kStages;
+    const uint32_t stages0 = smem_u32(smem);
+    const uint32_t hist0 = stages0 + kGroupOff + group * kGroupBytes;
+    const uint32_t staging = hist0 + kHistBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     const uint32_t bar_id = 1 + group;
 
-    // ---- one-time setup: LUTs, zero counters, barriers
+    // crop positions of this CTA: position i -> crop blockIdx.x + i * gridDim.x
+    const int n_pos = (n_rois > (int)blockIdx.x) ? (n_rois - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto crop_of = [&](int i) -> int32_t { return (int32_t)blockIdx.x + i * (int32_t)gridDim.x; };
+    // fill position i into stage i % 3: TMA for fast crops, a plain arrive otherwise (keeps the
+    // stage barrier's phase count in step with the positions)
+    auto issue = [&](int i) {
+        if (i >= n_pos) return;
+        const int s = i % kStages;
+        const lbp_roi_t r = rois[crop_of(i)];
+        if (roi_is_fast(r, geom)) {
+            mbar_arrive_expect_tx(&bars[s], HAS_DEPTH ? kStageBytes : kGreyBytes);
+            uint8_t* st = smem + s * kStageBytes;
+            tma_load_3d(st, &grey_map, &bars[s], r.x, r.y, r.img);
+            if (HAS_DEPTH) tma_load_3d(st + kGreyBytes, &depth_map, &bars[s], r.x, r.y, r.img);
+        } else {
+            mbar_arrive(&bars[s]);
+        }
+    };
+
+    // ---- one-time setup: LUTs, zero counters, barriers, first three positions
     for (int i = tid; i < kLutBytes; i += kThreads) {
         const int code = (i >> 7) * 4 + (i & 3);
         smem[kLutOff + i] = kUniformLutDev.v[code];
     }
     if (tid < 256) smem[kPlainLutOff + tid] = kUniformLutDev.v[tid];
-    for (int i = gtid; i < 2 * kHistBytes / 16; i += kGroupThreads)
+    for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
-    if (gtid == 0) {
+    if (tid == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         prefetch_tensormap(&grey_map);
+        if (HAS_DEPTH) prefetch_tensormap(&depth_map);
+        for (int i = 0; i < kStages; ++i) issue(i);
     }
     __syncthreads();
 
-    const int G = gridDim.x * kGroups;
-    const int gid = blockIdx.x * kGroups + group;
-    auto next_fast = [&](int32_t n) {
-        while (n < n_rois && !roi_is_fast(rois[n], geom)) n += G;
-        return n;
-    };
-    auto issue = [&](int32_t n, int s) {
-        const lbp_roi_t r = rois[n];
-        mbar_arrive_expect_tx(&bars[s], kGreyBytes);
-        tma_load_3d(gbase + s * kGreyBytes, &grey_map, &bars[s], r.x, r.y, r.img);
-    };
-    int32_t pn = next_fast(gid);  // producer cursor (used by gtid 0)
-    if (gtid == 0)
-        for (int s = 0; s < kStages && pn < n_rois; ++s) {
-            issue(pn, s);
-            pn = next_fast(pn + G);
-        }
-
     // ---- per-lane / per-warp constants
     const uint32_t byte_mult = 1u << (8 * (warp & 3));
-    uint32_t col_off[4], mult[4], mult_row[4];
+    uint32_t colb[4], mult[4], mult_row[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int x = 4 * lane + k;
         const bool inner = (x != 0) && (x != kTile - 1);  // the 1-px ROI border has no code
         const int cx = inner ? (8 * x - 1) / (kTile - 2) : (lane >> 2);
         const int col = (cx == (lane >> 2)) ? lane : 4 * cx;  // spill-over -> next cell's lane
-        col_off[k] = (uint32_t)(((warp >> 2) * kBins * 32 + col) * 4);
+        colb[k] = opaque(hist0 + (uint32_t)(((warp >> 2) * kBins * 32 + col) * 4));
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
         mult_row[k] = mult[k];
     }
@@ -188,15 +188,6 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const int i0 = (warp * (kTile - 2)) / 8;                   // first interior row of cell row
     const int nrows = ((warp + 1) * (kTile - 2)) / 8 - i0;     // 15 or 16
 
-    // depth rows of this warp for crop `roi`: image rows y+i0+1 .. y+i0+nrows, 8 B per lane
-    auto depth_row_ptr = [&](const lbp_roi_t& r, int j) -> const uint16_t* {
-        return depth + (int64_t)r.img * geom.depth_img_stride +
-               (int64_t)(r.y + i0 + 1 + j) * geom.depth_pitch + r.x + 4 * lane;
-    };
-    constexpr int kPre = 8;  // depth prefetch distance (rows)
-    uint2 dq[kPre];  // prefetch ring (rows j .. j+kPre-1)
-    bool prefetched = false;
-
     struct GroupSync {
         uint32_t id;
         __device__ __forceinline__ void operator()() const {
@@ -204,42 +195,24 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
     };
 
-    int stage = 0, hb = 0;  // grey stage, counter/staging buffer parity
-    uint32_t phase_bits = 0;
-    int32_t prev_n = -1;    // crop whose descriptor waits in staging[hb ^ 1]
-
-    for (int32_t n = gid; n < n_rois; n += G) {
+    int32_t pending = -1;  // last crop whose descriptor was bulk-stored
+    for (int i = group; i < n_pos; i += kGroups) {
+        const int32_t n = crop_of(i);
         const lbp_roi_t roi = rois[n];
+        const int s = i % kStages;
+        mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
         if (!roi_is_fast(roi, geom)) {
-            named_barrier_sync(bar_id, kGroupThreads);  // previous epilogue finished
+            if (gtid == 0) issue(i + kStages);  // stage s was never filled: release it at once
             extract_roi_generic<kBins, kGroupThreads>(
                 grey, HAS_DEPTH ? depth : nullptr, geom, roi, n, win, 8, 8, desc, roi_status,
-                reinterpret_cast<uint32_t*>(smem + (hist0 - smem_u32(smem))), 2 * kHistBytes / 4,
+                reinterpret_cast<uint32_t*>(smem + (hist0 - stages0)), kHistBytes / 4,
                 smem + kPlainLutOff, 0, gtid, GroupSync{bar_id});
             named_barrier_sync(bar_id, kGroupThreads);
-            prefetched = false;
             continue;
         }
-        // next crop of this group, for the cross-crop depth prefetch
-        const int32_t nn = n + G;
-        lbp_roi_t nroi{};
-        bool next_ok = false;
-        if (HAS_DEPTH && nn < n_rois) {
-            nroi = rois[nn];
-            next_ok = roi_is_fast(nroi, geom);
-        }
-        if (HAS_DEPTH && !prefetched) {
-#pragma unroll
-            for (int j = 0; j < kPre; ++j) dq[j] = ld_global_nc_v2(depth_row_ptr(roi, j));
-        }
-
-        mbar_wait(&bars[stage], (phase_bits >> stage) & 1u);
-        phase_bits ^= 1u << stage;
-        const uint32_t g0 = opaque(stage0 + stage * kGreyBytes + i0 * kTile + 4 * lane);
-        const uint32_t hbuf = hist0 + hb * kHistBytes;
-        uint32_t colb[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) colb[k] = opaque(hbuf + col_off[k]);
+        const uint32_t st = stages0 + s * kStageBytes;
+        const uint32_t g0 = opaque(st + i0 * kTile + 4 * lane);
+        const uint32_t d0 = opaque(st + kGreyBytes + (i0 + 1) * (kTile * 2) + 8 * lane);
 
         auto do_row = [&](const LaneRow& top, const LaneRow& mid, const LaneRow& bot, int j) {
             const uint32_t t0 = lbp_offset2(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
@@ -248,16 +221,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                                             bot.h1, bot.mh, mid.mh);
             uint32_t val[4];
             if (HAS_DEPTH) {
-                const uint2 d = dq[j % kPre];
-                // refill the ring slot: row j+kPre of this crop; in the last kPre rows (which
-                // cover every slot) row j % kPre of the group's next crop, read from that slot
-                // (one unconditional load from a selected address, so that the compiler writes
-                // the ring register directly; without a next crop it harmlessly re-reads row 0)
-                const int jn = j + kPre;  // compile-time: rows 0..15 of every crop
-                const uint16_t* src = (jn < 16) ? depth_row_ptr(roi, jn)
-                                                : depth_row_ptr(next_ok ? nroi : roi,
-                                                                next_ok ? j % kPre : 0);
-                dq[j % kPre] = ld_global_nc_v2(src);
+                const uint2 d = ld_shared_u32x2(d0 + j * (kTile * 2));
                 // depth window on a u16 in either half of a word
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
@@ -275,10 +239,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 red_shared_add(colb[k] + bin * (32 * 4), val[k]);
             }
         };
-        // 16 rows, straight-line (no branches: a conditional row block made the compiler copy
-        // prefetched registers at the block end, stalling on the load).  Cell rows with 15
-        // rows run a 16th dummy row whose increments are 0 (its pixels belong to the next
-        // warp's cell row; the rows it touches exist inside the crop).
+        // 16 rows, straight-line.  Cell rows with 15 rows run a 16th dummy row whose
+        // increments are 0 (its pixels belong to the next warp; its rows exist in the crop).
         LaneRow r0 = lane_row(g0), r1 = lane_row(g0 + kTile), r2;
 #pragma unroll
         for (int j = 0; j < 15; j += 3) {
@@ -294,29 +256,17 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         do_row(r0, r1, r2, 15);
 #pragma unroll
         for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
-        prefetched = next_ok;
 
-        // staging writes of the previous epilogue -> visible to the bulk-copy engine; the
-        // store issued one crop ago must be done reading before this epilogue reuses its buffer
-        fence_proxy_async_smem();
-        if (gtid == 0) bulk_wait_read_all();
-        named_barrier_sync(bar_id, kGroupThreads);  // stage free, counters of crop n complete
-
+        if (gtid == 0) bulk_wait_read_all();        // previous descriptor left the staging
+        named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
         if (gtid == 0) {
-            if (prev_n >= 0)
-                bulk_store_s2g(desc + (int64_t)prev_n * (64 * kBins), staging0 + (hb ^ 1) * kDescBytes,
-                               kDescBytes);
-            if (pn < n_rois) {
-                issue(pn, stage);
-                pn = next_fast(pn + G);
-            }
+            issue(i + kStages);
             if (roi_status) roi_status[n] = LBP_OK;
         }
         // ---- epilogue: quad q = (g, bin, cx) holds the 4 lane columns of cells (4g + j, cx),
         // j = byte.  Byte-transpose the 4 words and sum each byte column with IDP4A.
-        const uint32_t stg = staging0 + hb * kDescBytes;
         for (int q = gtid; q < 2 * kBins * 8; q += kGroupThreads) {
-            const uint32_t qa = hbuf + q * 16;
+            const uint32_t qa = hist0 + q * 16;
             const uint4 w = ld_shared_u32x4(qa);
             st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
             const uint32_t lo01 = prmt(w.x, w.y, 0x5140), hi01 = prmt(w.x, w.y, 0x7362);
@@ -327,42 +277,42 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             const uint32_t c3 = __dp4a(prmt(hi01, hi23, 0x7632), 0x01010101u, 0u);
             const int g = q / (kBins * 8), rem = q - g * (kBins * 8);
             const int bin = rem >> 3, cx = rem & 7;
-            const uint32_t o = stg + (((4 * g) * 8 + cx) * kBins + bin) * 2;  // cell (4g, cx)
-            constexpr uint32_t kRow = 8 * kBins * 2;                          // next cell row
+            const uint32_t o = staging + (((4 * g) * 8 + cx) * kBins + bin) * 2;  // cell (4g, cx)
+            constexpr uint32_t kRow = 8 * kBins * 2;                             // next cell row
             asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "h"((uint16_t)c0) : "memory");
             asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + kRow), "h"((uint16_t)c1) : "memory");
             asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 2 * kRow), "h"((uint16_t)c2) : "memory");
             asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 3 * kRow), "h"((uint16_t)c3) : "memory");
         }
-        prev_n = n;
-        hb ^= 1;
-        stage = (stage + 1 == kStages) ? 0 : stage + 1;
+        fence_proxy_async_smem();                   // staging writes -> async proxy
+        named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
+        if (gtid == 0) bulk_store_s2g(desc + (int64_t)n * (64 * kBins), staging, kDescBytes);
+        pending = n;
     }
-    // flush the last descriptor of this group
-    fence_proxy_async_smem();
-    named_barrier_sync(bar_id, kGroupThreads);
-    if (gtid == 0) {
-        if (prev_n >= 0)
-            bulk_store_s2g(desc + (int64_t)prev_n * (64 * kBins), staging0 + (hb ^ 1) * kDescBytes,
-                           kDescBytes);
-        bulk_wait_all();
-    }
+    if (gtid == 0 && pending >= 0) bulk_wait_all();
 }
 
 inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* depth,
                                           const lbp_images_t& geom, const lbp_roi_t* rois,
                                           int32_t n_rois, const DepthWindow& win, uint16_t* desc,
                                           int32_t* roi_status, int sms, cudaStream_t stream) {
-    CUtensorMap gm;
+    CUtensorMap gm, dm;
     if (!encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
                           geom.grey_img_stride))
         return cudaErrorNotSupported;
+    if (depth) {
+        if (!encode_stack_map(&dm, depth, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, geom,
+                              geom.depth_pitch, geom.depth_img_stride))
+            return cudaErrorNotSupported;
+    } else {
+        dm = gm;
+    }
     auto kern = depth ? lbp_hist_lane59_kernel<true> : lbp_hist_lane59_kernel<false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l59::kSmemBytes);
     if (e != cudaSuccess) return e;
-    const int grid = std::max(1, std::min(sms, (n_rois + l59::kGroups - 1) / l59::kGroups));
-    kern<<<grid, l59::kThreads, l59::kSmemBytes, stream>>>(gm, grey, depth, geom, rois, n_rois,
+    const int grid = std::max(1, std::min(sms, n_rois));
+    kern<<<grid, l59::kThreads, l59::kSmemBytes, stream>>>(gm, dm, grey, depth, geom, rois, n_rois,
                                                           win, desc, roi_status);
     return cudaGetLastError();
 }
