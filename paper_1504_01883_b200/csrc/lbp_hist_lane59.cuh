@@ -12,9 +12,10 @@
 //  * the uniform-bin LUT is lane-banked: bin(c) lives at byte (c>>2)*128 + 4*lane + (c&3),
 //    so lane l reads bank l; the compare results are accumulated directly into that offset;
 //  * grey and depth of a crop (48 KB) are staged by TMA into a ring of 3 stages shared by
-//    the CTA's two groups (crop position i of the CTA -> stage i%3, group i%2); the group
+//    the CTA's groups (crop position i of the CTA -> stage i%3, group i%kGroups); the group
 //    that finishes position i refills its stage with position i+3.
-// Structure: persistent, 1 CTA/SM, 2 groups of 8 warps; warp w of a group owns cell row w
+// Structure: persistent, 1 CTA/SM, 3 groups of 8 warps (24 warps hide each group's barrier
+// and load waits); warp w of a group owns cell row w
 // of its crop (with Ky = 8 the floor partition of the 126 interior rows is exactly the
 // warp's rows), lane l owns columns 4l..4l+3.  The epilogue writes the 7,552-B descriptor
 // into a smem staging buffer and a bulk async copy (cp.async.bulk) stores it.  ROIs that are
@@ -29,7 +30,7 @@
 namespace lbpf {
 
 namespace l59 {
-constexpr int kGroups = 2;
+constexpr int kGroups = 3;
 constexpr int kGroupThreads = 256;
 constexpr int kThreads = kGroups * kGroupThreads;
 constexpr int kTile = 128;
@@ -40,14 +41,15 @@ constexpr int kStageBytes = kGreyBytes + 2 * kTile * kTile;    // + depth 32,768
 constexpr int kHistBytes = 2 * kBins * 32 * 4;                 // [g][bin][lane] = 15,104
 constexpr int kDescBytes = 64 * kBins * 2;                     // 7,552
 constexpr int kGroupOff = kStages * kStageBytes;               // 147,456
-constexpr int kGroupBytes = kHistBytes + kDescBytes;           // 22,656
-constexpr int kLutOff = kGroupOff + kGroups * kGroupBytes;     // 192,768 (256-aligned)
+constexpr int kGroupBytes = (kHistBytes + kDescBytes + 255) / 256 * 256;  // 22,784
+constexpr int kLutOff = kGroupOff + kGroups * kGroupBytes;     // 215,808 (256-aligned)
 constexpr int kLutBytes = 64 * 128;
 constexpr int kPlainLutOff = kLutOff + kLutBytes;
 constexpr int kBarOff = kPlainLutOff + 256;
 constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;        // + 128-B alignment slack
 static_assert(kGroupBytes % 128 == 0 && kLutOff % 256 == 0, "alignment");
 static_assert(kSmemBytes <= 227 * 1024, "shared memory");
+static_assert(kStages >= kGroups, "every group needs a stage");
 }  // namespace l59
 
 __device__ __forceinline__ void bulk_store_s2g(void* gdst, uint32_t ssrc, uint32_t bytes) {
@@ -93,9 +95,10 @@ __device__ __forceinline__ LaneRow lane_row(uint32_t word_addr) {
 
 // Eq. 2 for the centre pair c as the lane-banked LUT offset, per 16-bit half:
 // 0x6400 + (code & 3) + 128 * (code >> 2) with the Fig. 7 bits (TL 1, T 2, TR 4, R 8,
-// BR 16, B 32, BL 64, L 128).  TL, T, TR, R: FMA pipe, sat(g_p - g_c + 1) in {0,1} scaled by
-// 1, 2, 128, 256 onto 1024.0 (exact fp16 integers); BR, B, BL, L: ALU pipe, HSET2 masks at
-// offsets 512..4096.  The bias 0x6400 is an arithmetic constant removed by the LUT base.
+// BR 16, B 32, BL 64, L 128).  TL, T, TR, R, BR: FMA pipe, sat(g_p - g_c + 1) in {0,1}
+// scaled by 1, 2, 128, 256, 512 onto 1024.0 (exact fp16 integers, sum <= 1923); B, BL, L:
+// ALU pipe, HSET2 masks at offsets 1024..4096.  The bias 0x6400 is an arithmetic constant
+// removed by the LUT base.
 __device__ __forceinline__ uint32_t lbp_offset2(uint32_t c, uint32_t tl, uint32_t t, uint32_t tr,
                                                 uint32_t r, uint32_t br, uint32_t b, uint32_t bl,
                                                 uint32_t l) {
@@ -105,8 +108,8 @@ __device__ __forceinline__ uint32_t lbp_offset2(uint32_t c, uint32_t tl, uint32_
     f = f16_fma(f16_fma_sat(t, kOne, negc1), 0x40004000u, f);          // T  +2
     f = f16_fma(f16_fma_sat(tr, kOne, negc1), 0x58005800u, f);         // TR +128
     f = f16_fma(f16_fma_sat(r, kOne, negc1), 0x5C005C00u, f);          // R  +256
-    uint32_t a = hge2_mask(br, c) & 0x02000200u;                       // BR +512
-    a |= hge2_mask(b, c) & 0x04000400u;                                // B  +1024
+    f = f16_fma(f16_fma_sat(br, kOne, negc1), 0x60006000u, f);         // BR +512 (<= 2047)
+    uint32_t a = hge2_mask(b, c) & 0x04000400u;                        // B  +1024
     a |= hge2_mask(bl, c) & 0x08000800u;                               // BL +2048
     a |= hge2_mask(l, c) & 0x10001000u;                                // L  +4096
     return f + a;  // no carry between halves (each half <= 0x6400 + 8067)
