@@ -44,7 +44,15 @@ WORKLOADS = {
                 "1000-identity SVM"),
     "config1": (1, 64, 64, 8, 8, 59, 2,
                 "BASELINE configs[0]: single 64x64 grey+depth crop, 8x8x59, 2-class SVM"),
+    "config2": (4, 128, 128, 8, 8, 59, 10,
+                "BASELINE configs[1]: 640x480 Kinect-shaped grey+depth frame stream, 4 tracked "
+                "faces (128x128 ROIs moving <= 20 px/frame), 10 identities"),
+    # crops = TOTAL database size (strong scaling: sharded over the ranks)
+    "config5": (262144, 128, 128, 8, 8, 59, 0,
+                "BASELINE configs[4]: online database build, 256k 128x128 crops sharded over the "
+                "GPUs, descriptors + int32 labels all-gathered (NCCL) into the training matrix"),
 }
+N_IDS = 100  # identities of the database build (label = crop index mod N_IDS)
 DMIN, DMAX = 600, 1400
 
 
@@ -254,6 +262,10 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "config5":
+        return run_dbbuild(args)
+    if args.workload in ("config1", "config2"):
+        return run_latency(args)
 
     import torch
     import torch.distributed as dist
@@ -365,6 +377,205 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_latency(args):
+    """Configs 1 and 2 are latency cases (one 64x64 crop; one 640x480 frame with 4 faces):
+    per-call device latency of extraction + SVM, eager (p50/p99 over calls, CUDA events) and
+    as a replayed CUDA graph of all calls (throughput).  Inputs are device-resident."""
+    import torch
+
+    import paper_1504_01883_b200 as lb
+    import synthgen
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n_per, H, Wd, cx, cy, bins, C, desc_txt = WORKLOADS[args.workload]
+    if args.workload == "config1":
+        n_calls = 256
+        g, d = synthgen.face_crops(n_calls, 64, 64, seed=args.seed)
+        rois_np = synthgen.full_rois(n_calls, 64, 64)
+        frame_bytes = 64 * 64 * 3
+    else:
+        n_calls = 240
+        g, d, rois_np = synthgen.kinect_frames(n_calls, seed=args.seed)
+        frame_bytes = 640 * 480 * 3
+    grey = torch.from_numpy(g).to(dev)
+    depth = torch.from_numpy(d.view(np.int16)).to(dev).view(torch.uint16)
+    rois = torch.from_numpy(rois_np).to(dev)
+    dim = cx * cy * bins
+    W_np, b_np = synthgen.svm_weights(C, dim, seed=args.seed)
+    W, b = torch.from_numpy(W_np).to(dev), torch.from_numpy(b_np).to(dev)
+    prepared = lb.svm_prepare(W)
+    desc = torch.empty((n_calls * n_per, dim), dtype=torch.uint16, device=dev)
+    labels = torch.empty(n_calls * n_per, dtype=torch.int32, device=dev)
+    top = torch.empty(n_calls * n_per, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)
+
+    def call(f):
+        r = rois[f * n_per:(f + 1) * n_per]
+        o = desc[f * n_per:(f + 1) * n_per]
+        lb.lbp_fused_extract(grey, depth, r, DMIN, DMAX, cx, cy, bins, out=o, stream=stream)
+        lb.svm_score(o, W, b, prepared=prepared, want_scores=False,
+                     labels=labels[f * n_per:(f + 1) * n_per],
+                     top_score=top[f * n_per:(f + 1) * n_per], stream=stream)
+
+    with torch.cuda.stream(stream):
+        for f in range(min(8, n_calls)):
+            call(f)
+    torch.cuda.synchronize()
+    # eager: one call at a time, events on the launching stream
+    lat = []
+    for f in range(n_calls):
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        call(f)
+        z.record(stream)
+        z.synchronize()
+        lat.append(a.elapsed_time(z))
+    lat = np.array(lat)
+    # graph: all calls captured once, replayed
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        for f in range(n_calls):
+            call(f)
+    graph.replay()
+    torch.cuda.synchronize()
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(args.steps // 10, 3)
+    with ClockSampler(0) as clk:
+        a.record(stream)
+        for _ in range(reps):
+            graph.replay()
+        z.record(stream)
+        torch.cuda.synchronize()
+    per_call_graph = a.elapsed_time(z) / reps / n_calls
+    line = {
+        "metric": METRIC, "value": n_per / (per_call_graph * 1e-3), "unit": UNIT, "n_gpus": 1,
+        "steps": reps * n_calls, "warmup": 8, "ms_per_step": per_call_graph,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {desc_txt}", "crops_per_call": n_per,
+                   "calls": n_calls, "classes": C, "l2": "inputs L2-resident (latency config)"},
+        "latency_us": {"eager_p50": float(np.percentile(lat, 50) * 1e3),
+                       "eager_p99": float(np.percentile(lat, 99) * 1e3),
+                       "graph_per_call": per_call_graph * 1e3},
+        "frame_h2d_bytes": frame_bytes, "gpu_launches": 2 * n_calls * reps, "clocks": clk.summary(),
+        "roofline": None, "cpu_baseline": latency_cpu_leg(args, g, d, rois_np, n_per, W_np, b_np,
+                                                          cx, cy, bins), "e2e": None,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def latency_cpu_leg(args, g, d, rois_np, n_per, W_np, b_np, cx, cy, bins):
+    """The oracle, single-threaded, on the first calls of the latency workload (ms per call)."""
+    if args.skip_cpu:
+        return None
+    import oracle
+    calls = 16
+    t0 = time.perf_counter()
+    for f in range(calls):
+        r = rois_np[f * n_per:(f + 1) * n_per]
+        dd = oracle.lbp_extract(g, d, r, DMIN, DMAX, cx, cy, bins)
+        oracle.svm_score(dd, W_np, b_np)
+    ms = (time.perf_counter() - t0) / calls * 1e3
+    return {"value": n_per / (ms * 1e-3), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "ms_per_call": ms, "sample": f"first {calls} calls, one thread", "cpu": cpu_model()}
+
+
+def run_dbbuild(args):
+    """Config 5: each rank extracts its shard of the database, then an all-gather over NCCL
+    assembles the full [N][dim] u16 training matrix and labels on every rank.  One step =
+    extraction + all-gather of all N crops; value = N / step time (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1504_01883_b200 as lb
+    import synthgen
+    from paper_1504_01883_b200.parallel import gather_database, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    else:  # the gather is a no-op copy; keep one code path with a 1-rank gloo group
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + (os.getpid() % 1000)))
+        dist.init_process_group("gloo" if not torch.cuda.is_available() else "nccl",
+                                rank=0, world_size=1, device_id=dev)
+    n_total, H, Wd, cx, cy, bins, _, desc_txt = WORKLOADS["config5"]
+    n_total = args.crops or n_total
+    first, count = shard_range(n_total, rank, world)
+    grey, depth = synthgen.gpu_face_crops(count, H, Wd, seed=args.seed, first_index=first,
+                                          dist=args.dist, device=dev)
+    rois = torch.from_numpy(synthgen.full_rois(count, H, Wd)).to(dev)
+    labels = (torch.arange(first, first + count, device=dev) % N_IDS).to(torch.int32)
+    dim = cx * cy * bins
+    desc = torch.empty((count, dim), dtype=torch.uint16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        lb.lbp_fused_extract(grey, depth, rois, DMIN, DMAX, cx, cy, bins, out=desc, stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
+        full, lab = gather_database(desc, labels, n_total)
+        if ev is not None:
+            ev[2].record(stream)
+        return full, lab
+
+    for _ in range(max(args.warmup, 3)):
+        full, lab = step()
+    torch.cuda.synchronize()
+    evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            full, lab = step(evs[k])
+        torch.cuda.synchronize()
+    dist.barrier()
+    ext = sum(a.elapsed_time(b) for a, b, _ in evs) / args.steps
+    gat = sum(b.elapsed_time(c) for _, b, c in evs) / args.steps
+    tot = evs[0][0].elapsed_time(evs[-1][2]) / args.steps
+    t = torch.tensor([tot, ext, gat], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot, ext, gat = (float(v) for v in t)
+    gathered = n_total * dim * 2 + n_total * 4
+    peak, peak_src = load_peaks()
+    bpc = bytes_per_crop(H, Wd, cx, cy, bins)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n_total / (tot * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": tot,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": f"config5: {desc_txt}", "crops_total": n_total,
+                       "crops_per_gpu": count, "crop": f"{H}x{Wd}", "cells": f"{cx}x{cy}",
+                       "bins": bins, "n_ids": N_IDS, "parallelism": f"crop-sharded dp{world} + "
+                       "all-gather"},
+            "extract_ms": ext, "allgather_ms": gat,
+            "allgather": {"bytes_out_per_rank": gathered,
+                          "algbw_GBps": gathered / (gat * 1e-3) / 1e9 if gat > 0 else None,
+                          "busbw_GBps": gathered * (world - 1) / world / (gat * 1e-3) / 1e9
+                          if gat > 0 else None},
+            "roofline": {"bound": "hbm", "kernel": "lbp_hist (extraction)",
+                         "achieved": bpc * count / (ext * 1e-3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bpc * count / (ext * 1e-3) / 1e9 / peak,
+                         "peak_source": peak_src, "traffic": None},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": args.steps, "clocks": clk.summary(),
+            "check": {"rows": int(full.shape[0]), "label_ok": bool(
+                (lab.cpu() == (torch.arange(n_total) % N_IDS).to(torch.int32)).all())},
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
     return 0
 
 

@@ -98,7 +98,7 @@ int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images
  *
  *   desc      u16 [n][dim]        W  fp32 [n_classes][dim] row-major   bias fp32 [n_classes]
  *   prepared  nullable: workspace filled by svm_prepare() for this W (enables the
- *             tensor-core path for large n_classes); NULL = CUDA-core path
+ *             tensor-core path for n >= 128); NULL = CUDA-core path
  *   scores    out, nullable fp32 [n][n_classes]
  *   labels    out, nullable int32 [n];  top_score out, nullable fp32 [n]
  */

@@ -102,9 +102,10 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, 
     if (n == 0) return LBP_OK;
     if (!desc || !W || !bias) return LBP_E_ARG;
     cudaStream_t stream = (cudaStream_t)stream_;
-    // Tensor-core path: exact integer digit-plane GEMM (needs svm_prepare()'s workspace).
+    // Tensor-core path: exact integer digit-plane GEMM (needs svm_prepare()'s workspace);
+    // below one 128-crop tile the CUDA-core kernel has the lower latency.
     SvmPrepHeader h;
-    if (prepared && svm_layout(n_classes, dim, &h) &&
+    if (prepared && n >= kGemmM && svm_layout(n_classes, dim, &h) &&
         (reinterpret_cast<uintptr_t>(desc) & 15) == 0) {
         cudaError_t e = launch_svm_gemm(desc, n, dim, W, bias, h, (const uint8_t*)prepared, scores,
                                         labels, top_score, reject_threshold, num_sms(), stream);

@@ -1,0 +1,68 @@
+"""Multi-GPU plumbing of the hot path: crop sharding and the database build.
+
+Crops are independent units, so recognition shards them across ranks with no data-path
+collective (weak scaling).  The only exchange step of the method is the online database
+build (BASELINE configs[4]): every rank extracts the descriptors of its shard
+and an all-gather (NCCL over NVLink on GPUs, gloo on CPU tests) assembles the full
+[N][dim] training matrix plus labels on every rank, in global crop order.
+
+Only `torch.distributed` plumbing lives here; the descriptors themselves come from the CUDA
+library (`lbpfused.lbp_fused_extract`).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous balanced shard of [0, n_total) for `rank`: (first index, count).
+
+    The first n_total % world ranks get one extra crop, so shards differ by at most 1 and
+    rank-major order equals global crop order."""
+    if world < 1 or not 0 <= rank < world or n_total < 0:
+        raise ValueError("bad shard arguments")
+    base, extra = divmod(n_total, world)
+    count = base + (1 if rank < extra else 0)
+    first = rank * base + min(rank, extra)
+    return first, count
+
+
+def gather_database(local_desc: torch.Tensor, local_labels: torch.Tensor, n_total: int,
+                    group=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """All-gather the per-rank descriptor shards (u16 [count][dim]) and int32 labels into the
+    full matrix [n_total][dim] / labels [n_total] on every rank, in global crop order.
+
+    Shards are padded to the largest shard size for the collective (all_gather_into_tensor
+    needs equal sizes) and the padding is dropped afterwards.  u16 rows travel as raw bytes
+    (uint8, supported by both NCCL and gloo)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    first, count = shard_range(n_total, rank, world)
+    if local_desc.shape[0] != count or local_labels.shape[0] != count:
+        raise ValueError(f"rank {rank}: shard has {local_desc.shape[0]} rows, expected {count}")
+    dim = local_desc.shape[1]
+    cap = -(-n_total // world)  # largest shard
+    dev = local_desc.device
+    send = torch.zeros((cap, 2 * dim), dtype=torch.uint8, device=dev)
+    send[:count] = local_desc.contiguous().view(torch.uint8)
+    send_lab = torch.full((cap,), -1, dtype=torch.int32, device=dev)
+    send_lab[:count] = local_labels
+    recv = torch.empty((world * cap, 2 * dim), dtype=torch.uint8, device=dev)
+    recv_lab = torch.empty((world * cap,), dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    dist.all_gather_into_tensor(recv_lab, send_lab, group=group)
+    keep = torch.cat([torch.arange(r * cap, r * cap + shard_range(n_total, r, world)[1])
+                      for r in range(world)]).to(dev)
+    return recv.index_select(0, keep).view(torch.uint16), recv_lab.index_select(0, keep)
+
+
+def build_database(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.Tensor,
+                   labels: torch.Tensor, n_total: int, dmin: int, dmax: int, cells_x: int,
+                   cells_y: int, bins: int, group=None, stream=None):
+    """Config 5 database build on this rank's shard (rois/labels of the shard, on the GPU):
+    extract its descriptors with the CUDA library, then all-gather the training matrix."""
+    from . import lbpfused
+    desc = lbpfused.lbp_fused_extract(grey, depth, rois, dmin, dmax, cells_x, cells_y, bins,
+                                      stream=stream)
+    return gather_database(desc, labels, n_total, group=group)

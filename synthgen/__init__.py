@@ -196,3 +196,48 @@ def gpu_face_crops(n: int, H: int, W: int, seed: int = 42, first_index: int = 0,
     if st != 0:
         raise RuntimeError(f"synth_face_crops failed ({st})")
     return grey, depth
+
+
+# --------------------------------------------------------------------------- Kinect frame stream
+def kinect_frames(n_frames: int, n_faces: int = 4, H: int = 480, W: int = 640, roi: int = 128,
+                  seed: int = 42, max_step: int = 20):
+    """BASELINE configs[1]: a 640x480 grey+depth frame stream with `n_faces` tracked faces.
+
+    Face k follows a seeded straight path (<= max_step px per frame per axis, bouncing at the
+    frame border, S:641's motion bound); its ROI is the roi x roi box at that position.  Grey =
+    the same 2-octave value noise as face_crops() over the whole frame; depth = background
+    2000..3000 mm with a face ellipse (semi-axes 0.36/0.43 roi, 900..1100 mm, nose relief) in
+    every ROI.  Returns grey u8 [n][H][W], depth u16 [n][H][W], rois int32 [n*n_faces][5]."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0xF2A]))
+    pos = np.stack([rng.integers(0, W - roi, n_faces), rng.integers(0, H - roi, n_faces)], 1)
+    vel = rng.integers(-max_step, max_step + 1, (n_faces, 2))
+    fd = rng.integers(900, 1101, n_faces)
+    rois = np.zeros((n_frames * n_faces, 5), np.int32)
+    grey = np.empty((n_frames, H, W), np.uint8)
+    depth = np.empty((n_frames, H, W), np.uint16)
+    y = np.arange(H, dtype=np.int64)[:, None]
+    x = np.arange(W, dtype=np.int64)[None, :]
+    a, b = (roi * 36) // 100, (roi * 43) // 100
+    a2, b2 = a * a, b * b
+    rn = max(roi // 8, 1)
+    for f in range(n_frames):
+        g, _ = face_crops(1, H, W, seed=seed, first_index=f)
+        grey[f] = g[0]
+        bg = 2000 + int(hash5(seed, f, 0, 0, 4) % 1001)
+        d = np.full((H, W), bg, np.int64)
+        for k in range(n_faces):
+            for ax, lim in ((0, W - roi), (1, H - roi)):
+                nxt = pos[k, ax] + vel[k, ax]
+                if nxt < 0 or nxt > lim:
+                    vel[k, ax] = -vel[k, ax]
+                    nxt = pos[k, ax] + vel[k, ax]
+                pos[k, ax] = nxt
+            x0, y0 = int(pos[k, 0]), int(pos[k, 1])
+            rois[f * n_faces + k] = (f, x0, y0, roi, roi)
+            dx, dy = x - (x0 + roi // 2), y - (y0 + roi // 2)
+            e = dx * dx * b2 + dy * dy * a2
+            r2 = dx * dx + dy * dy
+            relief = np.where(r2 < rn * rn, 40 - (40 * r2) // (rn * rn), 0)
+            d = np.where(e <= a2 * b2, fd[k] - relief, d)
+        depth[f] = d.astype(np.uint16)
+    return grey, depth, rois

@@ -1,0 +1,76 @@
+"""Multi-rank host logic on CPU (gloo): sharding arithmetic, rank-independent synthetic crops,
+and the database all-gather (config 5) against the oracle's single-process result."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synthgen
+from paper_1504_01883_b200.parallel import gather_database, shard_range
+
+
+def test_shard_range_covers_exactly():
+    for n in (0, 1, 7, 16, 1000, 1 << 20):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0
+            for (f0, c0), (f1, _) in zip(spans, spans[1:]):
+                assert f0 + c0 == f1
+            assert sum(c for _, c in spans) == n
+            assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+def test_crops_independent_of_sharding():
+    """Crop i is the same whichever rank draws it (weak-scaling invariant)."""
+    g_all, d_all = synthgen.face_crops(12, 64, 64, seed=5)
+    for world in (2, 3, 4):
+        for r in range(world):
+            first, count = shard_range(12, r, world)
+            g, d = synthgen.face_crops(count, 64, 64, seed=5, first_index=first)
+            assert np.array_equal(g, g_all[first:first + count])
+            assert np.array_equal(d, d_all[first:first + count])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n_total, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        first, count = shard_range(n_total, rank, world)
+        grey, depth = synthgen.face_crops(count, 64, 64, seed=9, first_index=first)
+        rois = synthgen.full_rois(count, 64, 64)
+        desc = oracle.lbp_extract(grey, depth, rois, 600, 1400, 8, 8, 59)  # stand-in extractor
+        labels = (np.arange(first, first + count) % 7).astype(np.int32)
+        full, lab = gather_database(torch.from_numpy(desc.view(np.int16)).view(torch.uint16),
+                                    torch.from_numpy(labels), n_total)
+        np.save(os.path.join(out_dir, f"desc{rank}.npy"), full.view(torch.int16).numpy())
+        np.save(os.path.join(out_dir, f"lab{rank}.npy"), lab.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_total", [(2, 10), (3, 11)])
+def test_gather_database_gloo(tmp_path, world, n_total):
+    mp.spawn(_worker, args=(world, _free_port(), n_total, str(tmp_path)), nprocs=world, join=True)
+    grey, depth = synthgen.face_crops(n_total, 64, 64, seed=9)
+    ref = oracle.lbp_extract(grey, depth, synthgen.full_rois(n_total, 64, 64), 600, 1400, 8, 8, 59)
+    for r in range(world):
+        got = np.load(tmp_path / f"desc{r}.npy").view(np.uint16)
+        lab = np.load(tmp_path / f"lab{r}.npy")
+        assert np.array_equal(got, ref)
+        assert np.array_equal(lab, np.arange(n_total) % 7)

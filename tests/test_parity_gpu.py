@@ -173,7 +173,7 @@ def _gpu_svm(lb, desc, W, b, reject=-math.inf, prepared=False):
 @pytest.mark.parametrize("C", [1, 2, 10, 100, 1000])
 @pytest.mark.parametrize("prepared", [False, True])
 def test_svm_random_within_tolerance(lb, C, prepared):
-    desc, W, b = _svm_inputs(70, C, seed=C)
+    desc, W, b = _svm_inputs(200 if prepared else 70, C, seed=C)  # >= 128 -> tensor cores
     s, lab, top = _gpu_svm(lb, desc, W, b, prepared=prepared)
     s_ref, lab_ref, top_ref = oracle.svm_score(desc, W, b)
     ok, worst = svm_tolerance_ok(desc, W, b, s, s_ref)
