@@ -443,8 +443,8 @@ def run_latency(args):
     torch.cuda.synchronize()
     a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = max(args.steps // 10, 3)
-    with ClockSampler(0) as clk:
-        a.record(stream)
+    with ClockSampler(0) as clk, torch.cuda.stream(stream):  # replay() launches on the
+        a.record(stream)                                     # current stream
         for _ in range(reps):
             graph.replay()
         z.record(stream)

@@ -41,6 +41,8 @@ def gather_database(local_desc: torch.Tensor, local_labels: torch.Tensor, n_tota
     first, count = shard_range(n_total, rank, world)
     if local_desc.shape[0] != count or local_labels.shape[0] != count:
         raise ValueError(f"rank {rank}: shard has {local_desc.shape[0]} rows, expected {count}")
+    if world == 1:
+        return local_desc, local_labels
     dim = local_desc.shape[1]
     cap = -(-n_total // world)  # largest shard
     dev = local_desc.device
@@ -52,6 +54,8 @@ def gather_database(local_desc: torch.Tensor, local_labels: torch.Tensor, n_tota
     recv_lab = torch.empty((world * cap,), dtype=torch.int32, device=dev)
     dist.all_gather_into_tensor(recv, send, group=group)
     dist.all_gather_into_tensor(recv_lab, send_lab, group=group)
+    if n_total % world == 0:  # equal shards: already contiguous in global order
+        return recv.view(torch.uint16), recv_lab
     keep = torch.cat([torch.arange(r * cap, r * cap + shard_range(n_total, r, world)[1])
                       for r in range(world)]).to(dev)
     return recv.index_select(0, keep).view(torch.uint16), recv_lab.index_select(0, keep)

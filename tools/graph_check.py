@@ -1,4 +1,6 @@
 """Does a CUDA graph captured with torch record the library's launches (cudart static)?"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
