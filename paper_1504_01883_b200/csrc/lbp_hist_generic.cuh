@@ -54,6 +54,13 @@ __device__ __forceinline__ void extract_roi_generic(
     const uint16_t* D = depth ? depth + (int64_t)r.img * geom.depth_img_stride : nullptr;
     const int32_t n_cells = cells_x * cells_y;
     const int32_t cells_per_chunk = cap / BINS;
+    // cell of interior column j: ((j+1)*Kx - 1) / W' -- in 32 bits when it cannot overflow
+    // (every realistic geometry), 64 bits otherwise
+    const bool narrow = (uint64_t)(r.wi + 1) * (uint64_t)cells_x < (1ull << 32);
+    auto cell_x = [&](int32_t j) -> int32_t {
+        return narrow ? (int32_t)(((uint32_t)(j + 1) * (uint32_t)cells_x - 1u) / (uint32_t)r.wi)
+                      : (int32_t)(((int64_t)(j + 1) * cells_x - 1) / r.wi);
+    };
 
     for (int32_t c0 = 0; c0 < n_cells; c0 += cells_per_chunk) {
         const int32_t c1 = min(n_cells, c0 + cells_per_chunk);
@@ -67,7 +74,7 @@ __device__ __forceinline__ void extract_roi_generic(
             const uint8_t* grow = G + yy * geom.grey_pitch + r.x0 + 1;
             const uint16_t* drow = D ? D + yy * geom.depth_pitch + r.x0 + 1 : nullptr;
             for (int32_t j = lane; j < r.wi; j += 32) {
-                const int32_t cx = (int32_t)(((int64_t)(j + 1) * cells_x - 1) / r.wi);
+                const int32_t cx = cell_x(j);
                 const int32_t cell = cy * cells_x + cx;
                 if (cell < c0 || cell >= c1) continue;
                 if (drow) {
