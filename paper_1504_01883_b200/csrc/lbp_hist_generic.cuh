@@ -18,16 +18,16 @@ constexpr int kGenericHistCap = 12032;  // u32 counters per chunk (47 KB, static
 
 // Eq. 2 with the Fig. 7 weights: TL 1, T 2, TR 4, R 8, BR 16, B 32, BL 64, L 128.
 __device__ __forceinline__ uint32_t lbp_code_scalar(const uint8_t* __restrict__ c, int64_t pitch) {
-    const uint32_t gc = c[0];
+    const uint32_t gc = __ldg(c);
     uint32_t code = 0;
-    code |= (uint32_t)(c[-pitch - 1] >= gc) << 0;
-    code |= (uint32_t)(c[-pitch] >= gc) << 1;
-    code |= (uint32_t)(c[-pitch + 1] >= gc) << 2;
-    code |= (uint32_t)(c[1] >= gc) << 3;
-    code |= (uint32_t)(c[pitch + 1] >= gc) << 4;
-    code |= (uint32_t)(c[pitch] >= gc) << 5;
-    code |= (uint32_t)(c[pitch - 1] >= gc) << 6;
-    code |= (uint32_t)(c[-1] >= gc) << 7;
+    code |= (uint32_t)(__ldg(c - pitch - 1) >= gc) << 0;
+    code |= (uint32_t)(__ldg(c - pitch) >= gc) << 1;
+    code |= (uint32_t)(__ldg(c - pitch + 1) >= gc) << 2;
+    code |= (uint32_t)(__ldg(c + 1) >= gc) << 3;
+    code |= (uint32_t)(__ldg(c + pitch + 1) >= gc) << 4;
+    code |= (uint32_t)(__ldg(c + pitch) >= gc) << 5;
+    code |= (uint32_t)(__ldg(c + pitch - 1) >= gc) << 6;
+    code |= (uint32_t)(__ldg(c - 1) >= gc) << 7;
     return code;
 }
 
@@ -73,16 +73,27 @@ __device__ __forceinline__ void extract_roi_generic(
             const int64_t yy = (int64_t)r.y0 + 1 + i;
             const uint8_t* grow = G + yy * geom.grey_pitch + r.x0 + 1;
             const uint16_t* drow = D ? D + yy * geom.depth_pitch + r.x0 + 1 : nullptr;
-            for (int32_t j = lane; j < r.wi; j += 32) {
-                const int32_t cx = cell_x(j);
-                const int32_t cell = cy * cells_x + cx;
-                if (cell < c0 || cell >= c1) continue;
-                if (drow) {
-                    const uint32_t d = drow[j];
-                    if (win.none_valid || (d - win.lo) > win.span) continue;
+            // 4 columns per lane per iteration: their 4 x 10 independent global loads are in
+            // flight together (latency-bound otherwise: one ROI per CTA, L2/DRAM latency)
+            for (int32_t j0 = lane; j0 < r.wi; j0 += 128) {
+                uint32_t code[4], ok[4];
+                int32_t cell[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int32_t j = j0 + 32 * u;
+                    const bool in = j < r.wi;
+                    const int32_t jj = in ? j : j0;
+                    cell[u] = cy * cells_x + cell_x(jj);
+                    ok[u] = in && cell[u] >= c0 && cell[u] < c1;
+                    if (drow) {
+                        const uint32_t d = __ldg(drow + jj);
+                        ok[u] = ok[u] && !win.none_valid && (d - win.lo) <= win.span;
+                    }
+                    code[u] = lbp_code_scalar(grow + jj, geom.grey_pitch);
                 }
-                const uint32_t code = lbp_code_scalar(grow + j, geom.grey_pitch);
-                atomicAdd(&hist[(cell - c0) * BINS + (lut[code] >> lut_shift)], 1u);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (ok[u]) atomicAdd(&hist[(cell[u] - c0) * BINS + (lut[code[u]] >> lut_shift)], 1u);
             }
         }
         sync();
@@ -109,7 +120,9 @@ lbp_hist_generic_kernel(const uint8_t* __restrict__ grey, const uint16_t* __rest
     __shared__ uint8_t lut[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
         lut[i] = (BINS == 59) ? kUniformLutDev.v[i] : (uint8_t)i;
-    for (int i = threadIdx.x; i < kGenericHistCap; i += blockDim.x) hist[i] = 0;
+    // only the counters of one chunk are ever used: (cap / BINS) cells, or the whole grid
+    const int used = min(kGenericHistCap / BINS, cells_x * cells_y) * BINS;
+    for (int i = threadIdx.x; i < used; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int32_t n = blockIdx.x; n < n_rois; n += gridDim.x) {
         extract_roi_generic<BINS, kGenericThreads>(grey, depth, geom, rois[n], n, win, cells_x,
