@@ -30,25 +30,31 @@ svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
                       int32_t n_classes, float* __restrict__ scores, int32_t* __restrict__ labels,
                       float* __restrict__ top_score, float reject_threshold) {
     extern __shared__ float xs[];  // [kSvmRows][dim]
-    __shared__ float wbest[kSvmThreads / 32][kSvmRows];
-    __shared__ int wbest_c[kSvmThreads / 32][kSvmRows];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kWarps = kSvmThreads / 32;
+    __shared__ float wbest[kWarps][kSvmRows];
+    __shared__ int wbest_c[kWarps][kSvmRows];
+    __shared__ double part[kWarps][kWarps][kSvmRows];  // [slice][class][row], few classes
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * kSvmRows;
     const int rows = (int)((n - row0) < kSvmRows ? (n - row0) : kSvmRows);
 
     if (kStage) {
-        for (int k = 0; k < kSvmRows; ++k)
-            for (int d = threadIdx.x; d < dim; d += blockDim.x)
-                xs[k * dim + d] = k < rows ? (float)desc[(row0 + k) * dim + d] : 0.0f;
+        const uint16_t* src = desc + row0 * dim;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < kSvmRows * dim; i += blockDim.x)
+            xs[i] = i < rows * dim ? (float)__ldg(src + i) : 0.0f;
         __syncthreads();
     }
     // unstaged: rows past the end re-read the last valid row (results discarded)
     auto x = [&](int k, int d) -> double {
         if (kStage) return (double)xs[k * dim + d];
-        return (double)desc[(row0 + min(k, rows - 1)) * dim + d];
+        return (double)__ldg(desc + (row0 + min(k, rows - 1)) * dim + d);
     };
 
+    // work items (class, slice of the dimension): with fewer classes than warps each class is
+    // split into S slices so that all warps work (latency-bound otherwise for small batches)
+    const int S = n_classes >= kWarps ? 1 : kWarps / n_classes;
+    const int items = n_classes * S;
     float best[kSvmRows];
     int best_c[kSvmRows];
 #pragma unroll
@@ -56,20 +62,35 @@ svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
         best[k] = -INFINITY;
         best_c[k] = 0x7FFFFFFF;
     }
-    for (int c = warp; c < n_classes; c += kWarps) {
+    for (int item = warp; item < items; item += kWarps) {
+        const int c = item / S, sl = item - c * S;
+        const int d0 = (int)((int64_t)sl * dim / S), d1 = (int)((int64_t)(sl + 1) * dim / S);
         const float* w = W + (int64_t)c * dim;
         double acc[kSvmRows];
 #pragma unroll
         for (int k = 0; k < kSvmRows; ++k) acc[k] = 0.0;
-        for (int d = lane; d < dim; d += 32) {
-            const double wd = (double)__ldg(w + d);
+        for (int d = d0 + lane; d < d1; d += 128) {
+            double wd[4];
 #pragma unroll
-            for (int k = 0; k < kSvmRows; ++k) acc[k] = fma(wd, x(k, d), acc[k]);
+            for (int u = 0; u < 4; ++u) wd[u] = d + 32 * u < d1 ? (double)__ldg(w + d + 32 * u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (d + 32 * u < d1) {
+#pragma unroll
+                    for (int k = 0; k < kSvmRows; ++k) acc[k] = fma(wd[u], x(k, d + 32 * u), acc[k]);
+                }
+            }
         }
 #pragma unroll
         for (int k = 0; k < kSvmRows; ++k) {
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xFFFFFFFFu, acc[k], off);
+        }
+        if (S > 1) {  // partial sums, combined below in slice order
+            if (lane == 0)
+#pragma unroll
+                for (int k = 0; k < kSvmRows; ++k) part[sl][c][k] = acc[k];
+            continue;
         }
         const double b = (double)__ldg(bias + c);
 #pragma unroll
@@ -81,6 +102,27 @@ svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
                 best_c[k] = c;
             }
         }
+    }
+    if (S > 1) {
+        __syncthreads();
+        if (threadIdx.x < rows) {
+            const int k = threadIdx.x;
+            float b = 0.0f;
+            int bc = 0;
+            for (int c = 0; c < n_classes; ++c) {
+                double acc = 0.0;
+                for (int sl = 0; sl < S; ++sl) acc += part[sl][c][k];
+                const float s = (float)(acc + (double)__ldg(bias + c));
+                if (scores) scores[(row0 + k) * n_classes + c] = s;
+                if (c == 0 || s > b) {
+                    b = s;
+                    bc = c;
+                }
+            }
+            if (top_score) top_score[row0 + k] = b;
+            if (labels) labels[row0 + k] = (b < reject_threshold) ? -1 : bc;
+        }
+        return;
     }
     if (lane == 0) {
 #pragma unroll
