@@ -111,18 +111,23 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, 
                                         labels, top_score, reject_threshold, num_sms(), stream);
         if (e != cudaErrorNotSupported) return launch_status(e);
     }
-    // CUDA-core path: exact fp64 accumulation
-    const int grid = (int)((n + kSvmRows - 1) / kSvmRows);
-    const size_t smem = (size_t)kSvmRows * dim * sizeof(float);
+    // CUDA-core path: exact fp64 accumulation; 8 crops per CTA, 1 for tiny batches
+    if (n < 8) {
+        svm_score_fp64_kernel<false, 1><<<n, kSvmThreads, 0, stream>>>(
+            desc, n, dim, W, bias, n_classes, scores, labels, top_score, reject_threshold);
+        return launch_status(cudaGetLastError());
+    }
+    const int grid = (int)((n + kSvmRowsMax - 1) / kSvmRowsMax);
+    const size_t smem = (size_t)kSvmRowsMax * dim * sizeof(float);
     if (smem <= 200 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(svm_score_fp64_kernel<true>,
+        cudaError_t e = cudaFuncSetAttribute(svm_score_fp64_kernel<true, kSvmRowsMax>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return launch_status(e);
-        svm_score_fp64_kernel<true><<<grid, kSvmThreads, smem, stream>>>(
+        svm_score_fp64_kernel<true, kSvmRowsMax><<<grid, kSvmThreads, smem, stream>>>(
             desc, n, dim, W, bias, n_classes, scores, labels, top_score, reject_threshold);
     } else {
-        svm_score_fp64_kernel<false><<<grid, kSvmThreads, 0, stream>>>(
+        svm_score_fp64_kernel<false, kSvmRowsMax><<<grid, kSvmThreads, 0, stream>>>(
             desc, n, dim, W, bias, n_classes, scores, labels, top_score, reject_threshold);
     }
     return launch_status(cudaGetLastError());

@@ -16,14 +16,14 @@
 namespace lbpf {
 
 constexpr int kSvmThreads = 256;
-constexpr int kSvmRows = 8;
+constexpr int kSvmRowsMax = 8;  // crops per CTA (1 for tiny batches: latency)
 
 __device__ __forceinline__ bool better(float s, int c, float best, int best_c) {
     // argmax over fp32 scores, ties -> lowest class index
     return s > best || (s == best && c < best_c);
 }
 
-template <bool kStage>
+template <bool kStage, int kSvmRows>
 __global__ void __launch_bounds__(kSvmThreads)
 svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
                       const float* __restrict__ W, const float* __restrict__ bias,
