@@ -12,16 +12,20 @@
 // exactness preconditions (sum_d x_d >= 2^16, detected with an all-ones B row, or a count
 // >= 1024 in the tile) are recomputed in fp64 on CUDA cores by the epilogue thread.
 //
-// Kernel: persistent, one CTA per SM, 6 warps:
-//   warp 0  TMA producer: A = 128 x 64 u16 descriptor tile, B = rows x 64 fp16 digit tile,
-//           both 128-B swizzled, into a ring of `stages` smem stages (mbarrier full/empty)
-//   warp 1  TMEM allocator + single-thread MMA issuer (tcgen05.mma kind::f16, M=128)
+// Kernel: persistent CTA PAIRS (clusters of 2, one CTA per SM), 6 warps per CTA, 256 crops
+// per pair tile:
+//   warp 0  TMA producer: A = this CTA's 128 x 64 u16 descriptor tile, B = this CTA's half
+//           (rows/2 x 64 fp16) of the pass's digit rows, both 128-B swizzled, into a ring of
+//           `stages` smem stages (mbarrier full/empty)
+//   warp 1  TMEM allocator (cta_group::2) + on the leader CTA the single-thread MMA issuer
+//           (tcgen05.mma.cta_group::2 kind::f16, M=256: both CTAs' A and B halves)
 //   warps 2-5  convert the A tile in place u16 -> fp16 (same swizzled byte layout), then
 //           run the epilogue: tcgen05.ld accumulators, fp64 digit combine, bias, argmax.
 // Classes are processed in TMEM passes of <= 124 classes (4 digits each + a ones block =
 // 512 fp32 columns); the running argmax of a crop lives in its epilogue thread's registers.
 #pragma once
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -70,7 +74,8 @@ inline size_t svm_layout_bytes(const SvmPrepHeader& h) {
 
 // ---------------------------------------------------------------------------- prepare
 
-// One block per Q row.  Class rows: digit k of W[c][.]; ones row; zero padding rows.
+// One block per Q row.  Natural rows of a pass: 4 digit rows per class (row 4c+k = digit k
+// of W[c][.]), the all-ones row, zero padding; stored in pair-major order (svm_gemm_kernel).
 __global__ void svm_prepare_kernel(const float* __restrict__ W, SvmPrepHeader h,
                                    uint8_t* __restrict__ ws) {
     __shared__ float red[32];
@@ -83,7 +88,11 @@ __global__ void svm_prepare_kernel(const float* __restrict__ W, SvmPrepHeader h,
         ++p;
     }
     const int nc = pass_classes(h.n_classes, p);
-    const int lr = row - base;
+    // pair-major storage: storage row sr of a pass of R rows belongs to CTA r = sr / (R/2) of
+    // the pair and to MMA half hh; its natural row (TMEM column) is hh*nn + r*nn/2 + j
+    const int R = pass_rows(nc), nh = R > 256 ? 2 : 1, nn = R / nh;
+    const int sr = row - base, cr = sr / (R / 2), within = sr % (R / 2);
+    const int lr = (within / (nn / 2)) * nn + cr * (nn / 2) + within % (nn / 2);
     __half* q = reinterpret_cast<__half*>(ws + h.q_off) + (size_t)row * h.dim_pad;
     if (lr >= 4 * nc) {  // ones row (column sum check) or zero padding
         const float v = (lr == 4 * nc) ? 1.0f : 0.0f;
@@ -130,8 +139,20 @@ struct GemmSmem {
     }
 };
 
-__global__ void __launch_bounds__(kGemmThreads, 1)
+// A CTA pair (cluster of 2) computes a 256-crop tile: CTA r stages crops [256t + 128r, +128)
+// as A and HALF of each pass's B rows (the pair-major storage order of svm_prepare), the
+// leader (rank 0) issues tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem and
+// writing both CTAs' TMEM.  Per CTA, B traffic from L2 is half of a 1-CTA M=128 kernel's.
+//
+// Barriers (same smem offsets in both CTAs):
+//   full[s]    local: this CTA's TMA bytes landed           (count 1, expect_tx)
+//   conv[s]    leader: both CTAs' A converted to fp16        (count 8 = 4 warps x 2 CTAs)
+//   empty[s]   both: pair MMAs reading stage s completed      (multicast commit)
+//   tmem_full  both: accumulators of the pass complete        (multicast commit)
+//   tmem_empty leader: both CTAs' epilogues drained TMEM      (count 8)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap b_map,
+                const __grid_constant__ CUtensorMap b_last_map,
                 const uint16_t* __restrict__ desc, int32_t n, const float* __restrict__ W,
                 const float* __restrict__ bias, const uint8_t* __restrict__ ws, SvmPrepHeader h,
                 int stages, int stage_bytes, float* __restrict__ scores,
@@ -149,47 +170,53 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = (int)cluster_id_x(), n_pairs_grid = (int)n_clusters_x();
     const int C = h.n_classes;
     const int KC = h.dim_pad / kGemmK;
-    const int n_tiles = (n + kGemmM - 1) / kGemmM;
+    const int n_tiles = (n + 2 * kGemmM - 1) / (2 * kGemmM);
     const float* scales = reinterpret_cast<const float*>(ws + h.scale_off);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&conv[s], 4);   // one arrive per converter warp
+            mbar_init(&conv[s], 8);
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 128);
+        mbar_init(tmem_empty, 8);
         fence_mbar_init();
         prefetch_tensormap(&a_map);
         prefetch_tensormap(&b_map);
+        prefetch_tensormap(&b_last_map);
     }
     if (warp == 1) {
-        tmem_alloc(tmem_slot, 512);
-        tmem_relinquish();
+        tmem_alloc_pair(tmem_slot, 512);
+        tmem_relinquish_pair();
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===================== TMA producer
+        // ===================== TMA producer (each CTA: its A rows and its half of B)
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            for (int t = pair; t < n_tiles; t += n_pairs_grid) {
                 int row0 = 0;
                 for (int p = 0; p < h.n_pass; ++p) {
                     const int rows = pass_rows(pass_classes(C, p));
+                    const int half = rows / 2;
+                    const CUtensorMap* bm = (p + 1 < h.n_pass || h.n_pass == 1) ? &b_map : &b_last_map;
                     for (int kc = 0; kc < KC; ++kc) {
                         mbar_wait(&empty[s], ph ^ 1);
-                        mbar_arrive_expect_tx(&full[s], kGemmM * kGemmK * 2 + rows * kGemmK * 2);
-                        tma_load_2d(L.a(smem, s), &a_map, &full[s], kc * kGemmK, t * kGemmM);
-                        for (int r = 0; r < rows; r += kBoxRows)
-                            tma_load_2d(L.b(smem, s) + r * 128, &b_map, &full[s], kc * kGemmK, row0 + r);
+                        mbar_arrive_expect_tx(&full[s], kGemmM * kGemmK * 2 + half * kGemmK * 2);
+                        tma_load_2d(L.a(smem, s), &a_map, &full[s], kc * kGemmK,
+                                    t * 2 * kGemmM + (int)rank * kGemmM);
+                        tma_load_2d(L.b(smem, s), bm, &full[s], kc * kGemmK, row0 + (int)rank * half);
                         if (++s == stages) { s = 0; ph ^= 1; }
                     }
                     row0 += rows;
@@ -197,17 +224,17 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer (single thread)
-        if (lane == 0) {
+        // ===================== MMA issuer (leader CTA, single thread)
+        if (rank == 0 && lane == 0) {
             int s = 0;
             uint32_t ph = 0, acc_ph = 0;
-            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            for (int t = pair; t < n_tiles; t += n_pairs_grid) {
                 for (int p = 0; p < h.n_pass; ++p) {
                     const int rows = pass_rows(pass_classes(C, p));
                     const int nh = rows > 256 ? 2 : 1;
-                    const int nn = rows / nh;  // N per MMA (multiple of 16)
-                    const uint32_t idesc = idesc_f16_f32(kGemmM, nn);
-                    mbar_wait(tmem_empty, acc_ph ^ 1);  // epilogue drained the accumulators
+                    const int nn = rows / nh;  // N per MMA (multiple of 16); nn/2 rows per CTA
+                    const uint32_t idesc = idesc_f16_f32(2 * kGemmM, nn);
+                    mbar_wait(tmem_empty, acc_ph ^ 1);  // both epilogues drained TMEM
                     acc_ph ^= 1;
                     tc_fence_after();
                     for (int kc = 0; kc < KC; ++kc) {
@@ -219,26 +246,29 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                         for (int ks = 0; ks < kGemmK / 16; ++ks) {
                             const uint64_t ad = umma_desc_sw128(a_addr + ks * 32);
                             for (int hh = 0; hh < nh; ++hh) {
-                                const uint64_t bd = umma_desc_sw128(b_addr + hh * (nn / 8) * 1024 + ks * 32);
-                                mma_f16_ss(tmem_base + hh * nn, ad, bd, idesc, (kc | ks) != 0);
+                                const uint64_t bd =
+                                    umma_desc_sw128(b_addr + hh * (nn / 2) * 128 + ks * 32);
+                                mma_f16_ss_pair(tmem_base + hh * nn, ad, bd, idesc, (kc | ks) != 0);
                             }
                         }
-                        mma_commit(&empty[s]);  // stage free once these MMAs complete
+                        mma_commit_pair(&empty[s], 0x3);  // stage free in both CTAs
                         if (++s == stages) { s = 0; ph ^= 1; }
                     }
-                    mma_commit(tmem_full);  // accumulators of this pass complete
+                    mma_commit_pair(tmem_full, 0x3);  // accumulators of this pass complete
                 }
             }
         }
     } else {
-        // ===================== converters + epilogue (warps 2..5, 128 threads)
+        // ===================== converters + epilogue (warps 2..5, 128 threads per CTA)
         const int et = threadIdx.x - 64;           // 0..127
         const int quarter = warp & 3;              // TMEM lane quarter accessible by this warp
-        const int row = quarter * 32 + lane;       // accumulator row = crop within the tile
+        const int row = quarter * 32 + lane;       // accumulator row = crop within the CTA's half
+        const uint32_t conv_leader = mapa_shared(smem_u32(conv), 0);
+        const uint32_t tmem_empty_leader = mapa_shared(smem_u32(tmem_empty), 0);
         int s = 0;
         uint32_t ph = 0, acc_ph = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const int64_t crop = (int64_t)t * kGemmM + row;
+        for (int t = pair; t < n_tiles; t += n_pairs_grid) {
+            const int64_t crop = (int64_t)t * 2 * kGemmM + (int64_t)rank * kGemmM + row;
             float best = 0.0f;
             int best_c = -1;
             int class0 = 0;
@@ -265,10 +295,11 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                     flag_or |= big;
                     fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&conv[s]);
+                    if (lane == 0) mbar_arrive_cluster(conv_leader + s * 8);
                     if (++s == stages) { s = 0; ph ^= 1; }
                 }
-                // ---- epilogue of this pass
+                // ---- epilogue of this pass (this CTA's 128 rows; its own count flag: the
+                // rows of the two CTAs are disjoint)
                 const bool tile_big = named_barrier_or(1, 128, flag_or != 0);
                 mbar_wait(tmem_full, acc_ph);
                 acc_ph ^= 1;
@@ -314,7 +345,8 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(tmem_empty);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tmem_empty_leader);
                 class0 += nc;
             }
             if (crop < n) {
@@ -325,7 +357,8 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem_base, 512);
+    cluster_sync();  // the peer's TMEM / smem are no longer used by the leader's MMAs
+    if (warp == 1) tmem_dealloc_pair(tmem_base, 512);
 }
 
 // ---------------------------------------------------------------------------- host side
@@ -349,26 +382,35 @@ inline cudaError_t launch_svm_gemm(const uint16_t* desc, int32_t n, int32_t dim,
                                    const float* bias, const SvmPrepHeader& h, const uint8_t* ws,
                                    float* scores, int32_t* labels, float* top, float reject,
                                    int sms, cudaStream_t stream) {
-    CUtensorMap am, bm;
+    CUtensorMap am, bm, blm;
+    const int rows_last = pass_rows(pass_classes(h.n_classes, h.n_pass - 1));
     if (!encode_2d(&am, desc, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (uint64_t)dim, (uint64_t)n,
                    (uint64_t)dim * 2, kGemmK, kGemmM))
         return cudaErrorNotSupported;
+    // one TMA box = one CTA's half of a pass (<= 256 rows)
     if (!encode_2d(&bm, ws + h.q_off, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (uint64_t)h.dim_pad,
-                   (uint64_t)h.total_rows, (uint64_t)h.dim_pad * 2, kGemmK, kBoxRows))
+                   (uint64_t)h.total_rows, (uint64_t)h.dim_pad * 2, kGemmK, h.rows_max / 2) ||
+        !encode_2d(&blm, ws + h.q_off, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (uint64_t)h.dim_pad,
+                   (uint64_t)h.total_rows, (uint64_t)h.dim_pad * 2, kGemmK, rows_last / 2))
         return cudaErrorNotSupported;
-    const int stage_bytes = kGemmM * kGemmK * 2 + h.rows_max * kGemmK * 2;
+    const int stage_bytes = kGemmM * kGemmK * 2 + (h.rows_max / 2) * kGemmK * 2;
     const int budget = 220 * 1024;
     int stages = budget / stage_bytes;
-    stages = stages > 4 ? 4 : stages;
+    stages = stages > 6 ? 6 : stages;
+    if (const char* env = getenv("LBPF_SVM_STAGES")) {  // tuning knob (tools/svm_time.py)
+        const int v = atoi(env);
+        if (v >= 2 && v < stages) stages = v;
+    }
     if (stages < 2) return cudaErrorNotSupported;
     const int smem = stages * stage_bytes + 1024 + 256;
     cudaError_t e = cudaFuncSetAttribute(svm_gemm_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    const int tiles = (n + kGemmM - 1) / kGemmM;
-    const int grid = tiles < sms ? tiles : sms;
-    svm_gemm_kernel<<<grid, kGemmThreads, smem, stream>>>(am, bm, desc, n, W, bias, ws, h, stages,
-                                                          stage_bytes, scores, labels, top, reject);
+    const int tiles = (n + 2 * kGemmM - 1) / (2 * kGemmM);
+    const int pairs = tiles < sms / 2 ? tiles : sms / 2;
+    svm_gemm_kernel<<<2 * pairs, kGemmThreads, smem, stream>>>(am, bm, blm, desc, n, W, bias, ws, h,
+                                                               stages, stage_bytes, scores, labels,
+                                                               top, reject);
     return cudaGetLastError();
 }
 

@@ -244,7 +244,16 @@ def test_svm_prepare_digit_roundtrip(lb):
     m = raw[scale_off:scale_off + 4 * C].view(np.float32)
     rows = ((4 * C + 16) + 31) // 32 * 32
     dpad = (D + 63) // 64 * 64
-    q = raw[q_off:q_off + rows * dpad * 2].view(np.float16).reshape(rows, dpad).astype(np.float64)
+    stored = raw[q_off:q_off + rows * dpad * 2].view(np.float16).reshape(rows, dpad)
+    # pair-major storage (svm_gemm.cuh): CTA r of the pair holds natural rows
+    # hh*nn + r*nn/2 + [0, nn/2) of MMA half hh, its half of the pass stored contiguously
+    nh = 2 if rows > 256 else 1
+    nn = rows // nh
+    q = np.empty((rows, dpad))
+    for sr in range(rows):
+        cr, within = divmod(sr, rows // 2)
+        hh, j = divmod(within, nn // 2)
+        q[hh * nn + cr * (nn // 2) + j] = stored[sr]
     for c in range(C):
         assert m[c] >= np.abs(W[c]).max() and np.log2(m[c]) == np.round(np.log2(m[c]))
         rec = m[c] * sum(q[4 * c + k, :D] * 2.0 ** -(8 + 9 * k) for k in range(4))
