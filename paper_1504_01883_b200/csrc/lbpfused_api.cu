@@ -238,3 +238,4 @@ int32_t lbp_recognize_host(const uint8_t* grey_h, const uint16_t* depth_h, lbp_i
 }
 
 }  // extern "C"
+

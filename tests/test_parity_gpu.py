@@ -272,15 +272,22 @@ def test_svm_gemm_multi_pass(lb, C):
     assert labels_agree_away_from_ties(s_ref, lab, lab_ref, desc, W, b)
 
 
-@pytest.mark.parametrize("kind", ["big_count", "big_sum"])
+@pytest.mark.parametrize("kind", ["big_count", "inf_bits", "mid_count", "big_sum"])
 def test_svm_gemm_exactness_fallback(lb, kind):
-    """Tiles breaking the exact-accumulation preconditions take the fp64 fallback."""
+    """Tiles breaking the exact-accumulation preconditions take the fp64 fallback; counts in
+    [1024, 2048) are still exact on the tensor-core path (fp16 exponent field 1)."""
     rng = np.random.default_rng(3)
-    n, D, C = 200, 3776, 20
-    if kind == "big_count":
-        desc = rng.integers(0, 40, (n, D)).astype(np.uint16)
-        desc[5, 17] = 5000
-        desc[150, 3] = 1024
+    n, D, C = 300, 3776, 20
+    if kind in ("big_count", "inf_bits", "mid_count"):
+        desc = rng.integers(0, 9, (n, D)).astype(np.uint16)  # row sums ~15k < 2^16
+        if kind == "big_count":
+            desc[5, 17] = 2048
+            desc[290, 3] = 40000
+        elif kind == "inf_bits":
+            desc[7, 100] = 0x7C00  # +Inf as fp16 bits; 0x7E00 = NaN
+            desc[260, 64] = 0x7E00
+        else:
+            desc[5, 17], desc[150, 3], desc[299, 3775] = 1024, 1500, 2047
     else:
         desc = rng.integers(0, 1000, (n, D)).astype(np.uint16)  # sum_d x_d >> 2^17
     W, b = synthgen.svm_weights(C, D, seed=11)

@@ -45,3 +45,4 @@ for n, C in zip(args[0::2], args[1::2]):
     ok = np.array_equal(ref.max(1), top.cpu().numpy()[idx])
     print(f"n={n} C={C}: svm_score {ms * 1e3:.1f} us  ({flops / ms / 1e9:.0f} TFLOP/s incl. "
           f"ones rows)  top spot-check exact={ok}", flush=True)
+
