@@ -22,6 +22,7 @@ _SRC = os.path.join(_HERE, "lbp_oracle.c")
 _LIB = os.path.join(_HERE, "liblbp_oracle.so")
 
 ORC_OK, ORC_E_ARG, ORC_E_ROI, ORC_E_GRID, ORC_E_OVERFLOW = 0, -1, -2, -3, -4
+SRC_GREY, SRC_DEPTH, SRC_FUSED = 0, 1, 2
 
 _lib = None
 
@@ -51,6 +52,9 @@ def lib():
         L.oracle_lbp_extract.argtypes = [P, P, i32, i32, i32, i64, i64, i64, i64, P, i32,
                                          u16, u16, i32, i32, i32, P, P]
         L.oracle_lbp_extract.restype = i32
+        L.oracle_lbp_extract_src.argtypes = [P, P, i32, i32, i32, i64, i64, i64, i64, P, i32,
+                                             u16, u16, i32, i32, i32, i32, P, P]
+        L.oracle_lbp_extract_src.restype = i32
         L.oracle_svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, f32]
         L.oracle_svm_score.restype = i32
         _lib = L
@@ -84,32 +88,37 @@ def lbp_map_u8(img: np.ndarray) -> np.ndarray:
     return out
 
 
-def lbp_extract(grey: np.ndarray, depth, rois, dmin: int, dmax: int,
-                cells_x: int, cells_y: int, bins: int, *, return_status: bool = False):
+def lbp_extract(grey, depth, rois, dmin: int, dmax: int,
+                cells_x: int, cells_y: int, bins: int, *, source: int = SRC_GREY,
+                return_status: bool = False):
     """Descriptors for ROIs of a [n_images][H][W] grey (+ optional depth) stack.
 
-    rois: int32 [n][5] = (img, x, y, w, h).  Returns uint16 [n][cells_y*cells_x*bins]
-    (and int32 per-ROI status when return_status).
+    rois: int32 [n][5] = (img, x, y, w, h).  source: SRC_GREY (codes on grey), SRC_DEPTH
+    (codes on the u16 depth plane) or SRC_FUSED (grey block then depth block).  Returns
+    uint16 [n][(1 or 2)*cells_y*cells_x*bins] (and int32 per-ROI status when return_status).
     """
-    grey = np.ascontiguousarray(grey, dtype=np.uint8)
-    if grey.ndim == 2:
-        grey = grey[None]
-    n_img, H, W = grey.shape
+    if grey is not None:
+        grey = np.ascontiguousarray(grey, dtype=np.uint8)
+        if grey.ndim == 2:
+            grey = grey[None]
     if depth is not None:
         depth = np.ascontiguousarray(depth, dtype=np.uint16)
         if depth.ndim == 2:
             depth = depth[None]
-        assert depth.shape == grey.shape
+        if grey is not None:
+            assert depth.shape == grey.shape
+    ref = grey if grey is not None else depth
+    n_img, H, W = ref.shape
     rois = np.ascontiguousarray(np.asarray(rois, dtype=np.int32).reshape(-1, 5))
     n = rois.shape[0]
-    dim = cells_x * cells_y * bins
+    dim = cells_x * cells_y * bins * (2 if source == SRC_FUSED else 1)
     desc = np.zeros((n, dim), dtype=np.uint16)
     status = np.zeros(n, dtype=np.int32)
-    st = lib().oracle_lbp_extract(_ptr(grey), _ptr(depth), n_img, H, W, W, W, H * W, H * W,
-                                  _ptr(rois), n, dmin, dmax, cells_x, cells_y, bins,
-                                  _ptr(desc), _ptr(status))
+    st = lib().oracle_lbp_extract_src(_ptr(grey), _ptr(depth), n_img, H, W, W, W, H * W, H * W,
+                                      _ptr(rois), n, dmin, dmax, cells_x, cells_y, bins, source,
+                                      _ptr(desc), _ptr(status))
     if st != ORC_OK:
-        raise ValueError(f"oracle_lbp_extract status {st}")
+        raise ValueError(f"oracle_lbp_extract_src status {st}")
     return (desc, status) if return_status else desc
 
 

@@ -114,40 +114,52 @@ int32_t oracle_lbp_map_u8(const uint8_t* img, int32_t h, int32_t w, int64_t pitc
 /*     concatenation of the cells (Eq. 3: K sub-histograms).     */
 /*  4. valid = (depth == NULL) or (d != 0 and dmin <= d <= dmax), d = depth */
 /*     at the CENTRE pixel (P:49-63 mask; S:37 0 = no reading).             */
-/*  5. code = Eq. 2 above on the grey 3x3 neighbourhood.            */
+/*  5. code = Eq. 2 above on the 3x3 neighbourhood of the SOURCE plane      */
+/*     (P:115): the grey image, or -- SURVEY §8f-1, Table 1's "Depth Image" */
+/*     row -- the u16 depth image itself (S:559 source: depth). */
 /*  6. bin = code (bins = 256, "ranging from 0 to 255") or           */
 /*     U[code] (bins = 59, uniform patterns, J.north_star).                 */
 /*  7. hist[(cy*Kx+cx)*bins + bin] += 1 (Eq. 3, f = indicator).             */
+/* source = ORC_SRC_FUSED writes the grey descriptor then the depth one     */
+/* (the "fusion of RGB and depth" of the title): row length 2*dim.    */
 /* ------------------------------------------------------------------------ */
-int32_t oracle_lbp_extract(const uint8_t* grey, const uint16_t* depth,
-                           int32_t n_images, int32_t height, int32_t width,
-                           int64_t grey_pitch, int64_t depth_pitch,
-                           int64_t grey_img_stride, int64_t depth_img_stride,
-                           const int32_t* rois /* [n_rois][5] = img,x,y,w,h */, int32_t n_rois,
-                           uint16_t dmin, uint16_t dmax,
-                           int32_t cells_x, int32_t cells_y, int32_t bins,
-                           uint16_t* desc /* [n_rois][cells_y*cells_x*bins] */,
-                           int32_t* roi_status /* nullable [n_rois] */)
+enum { ORC_SRC_GREY = 0, ORC_SRC_DEPTH = 1, ORC_SRC_FUSED = 2 };
+
+int32_t oracle_lbp_extract_src(const uint8_t* grey, const uint16_t* depth,
+                               int32_t n_images, int32_t height, int32_t width,
+                               int64_t grey_pitch, int64_t depth_pitch,
+                               int64_t grey_img_stride, int64_t depth_img_stride,
+                               const int32_t* rois /* [n_rois][5] = img,x,y,w,h */,
+                               int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                               int32_t cells_x, int32_t cells_y, int32_t bins, int32_t source,
+                               uint16_t* desc /* [n_rois][(1 or 2)*cells_y*cells_x*bins] */,
+                               int32_t* roi_status /* nullable [n_rois] */)
 {
     if (n_rois < 0) return ORC_E_ARG;
+    if (source != ORC_SRC_GREY && source != ORC_SRC_DEPTH && source != ORC_SRC_FUSED)
+        return ORC_E_ARG;
     if (n_rois == 0) return ORC_OK;
-    if (!grey || !rois || !desc) return ORC_E_ARG;
+    if (!rois || !desc) return ORC_E_ARG;
+    if (source != ORC_SRC_DEPTH && !grey) return ORC_E_ARG;
+    if (source != ORC_SRC_GREY && !depth) return ORC_E_ARG;
     if (bins != 59 && bins != 256) return ORC_E_ARG;
     if (cells_x < 1 || cells_y < 1) return ORC_E_ARG;
     if (dmin > dmax) return ORC_E_ARG;
     if (n_images < 1 || height < 1 || width < 1) return ORC_E_ARG;
-    if (grey_pitch < width || grey_img_stride < grey_pitch * (height - 1) + width) return ORC_E_ARG;
+    if (grey && (grey_pitch < width || grey_img_stride < grey_pitch * (height - 1) + width))
+        return ORC_E_ARG;
     if (depth && (depth_pitch < width || depth_img_stride < depth_pitch * (height - 1) + width))
         return ORC_E_ARG;
     int64_t dim = (int64_t)cells_x * cells_y * bins;
-    if (dim > 0x7FFFFFFF) return ORC_E_ARG;
+    int64_t row = (source == ORC_SRC_FUSED) ? 2 * dim : dim;
+    if (row > 0x7FFFFFFF) return ORC_E_ARG;
 
     uint8_t U[256];
     oracle_uniform_table(U);
 
     for (int32_t n = 0; n < n_rois; ++n) {
-        uint16_t* h = desc + (int64_t)n * dim;
-        for (int64_t d = 0; d < dim; ++d) h[d] = 0;
+        uint16_t* h = desc + (int64_t)n * row;
+        for (int64_t d = 0; d < row; ++d) h[d] = 0;
         int32_t status = ORC_OK;
 
         const int32_t* roi = rois + (int64_t)n * 5;
@@ -180,45 +192,72 @@ int32_t oracle_lbp_extract(const uint8_t* grey, const uint16_t* depth,
         if (roi_status) roi_status[n] = status;
         if (status != ORC_OK) continue;
 
-        const uint8_t* G = grey + img * grey_img_stride;
+        const uint8_t* G = grey ? grey + img * grey_img_stride : NULL;
         const uint16_t* D = depth ? depth + img * depth_img_stride : NULL;
 
-        /* step 3: loop over blocks with their floor ranges */
-        for (int32_t cy = 0; cy < cells_y; ++cy) {
-            int64_t i_begin = ((int64_t)cy * Hi) / cells_y;
-            int64_t i_end = ((int64_t)(cy + 1) * Hi) / cells_y;
-            for (int32_t cx = 0; cx < cells_x; ++cx) {
-                int64_t j_begin = ((int64_t)cx * Wi) / cells_x;
-                int64_t j_end = ((int64_t)(cx + 1) * Wi) / cells_x;
-                uint32_t count[256];
-                for (int b = 0; b < 256; ++b) count[b] = 0;
-                for (int64_t i = i_begin; i < i_end; ++i)
-                    for (int64_t j = j_begin; j < j_end; ++j) {
-                        int64_t yy = y0 + 1 + i, xx = x0 + 1 + j; /* image pixel */
-                        /* step 4: depth window at the centre pixel */
-                        int valid = 1;
-                        if (D) {
-                            uint16_t d = D[yy * depth_pitch + xx];
-                            valid = (d != 0) && (d >= dmin) && (d <= dmax);
+        /* one pass per source plane: grey block first, then depth (fused) */
+        for (int pass = 0; pass < 2; ++pass) {
+            int use_depth;
+            if (source == ORC_SRC_FUSED) use_depth = pass;
+            else if (pass == 0) use_depth = (source == ORC_SRC_DEPTH);
+            else break;
+            uint16_t* hb = h + (int64_t)pass * dim;
+
+            /* step 3: loop over blocks with their floor ranges */
+            for (int32_t cy = 0; cy < cells_y; ++cy) {
+                int64_t i_begin = ((int64_t)cy * Hi) / cells_y;
+                int64_t i_end = ((int64_t)(cy + 1) * Hi) / cells_y;
+                for (int32_t cx = 0; cx < cells_x; ++cx) {
+                    int64_t j_begin = ((int64_t)cx * Wi) / cells_x;
+                    int64_t j_end = ((int64_t)(cx + 1) * Wi) / cells_x;
+                    uint32_t count[256];
+                    for (int b = 0; b < 256; ++b) count[b] = 0;
+                    for (int64_t i = i_begin; i < i_end; ++i)
+                        for (int64_t j = j_begin; j < j_end; ++j) {
+                            int64_t yy = y0 + 1 + i, xx = x0 + 1 + j; /* image pixel */
+                            /* step 4: depth window at the centre pixel */
+                            int valid = 1;
+                            if (D) {
+                                uint16_t d = D[yy * depth_pitch + xx];
+                                valid = (d != 0) && (d >= dmin) && (d <= dmax);
+                            }
+                            if (!valid) continue;
+                            /* step 5: Eq. 2 on the source plane */
+                            uint32_t win[9];
+                            for (int r = 0; r < 3; ++r)
+                                for (int c = 0; c < 3; ++c)
+                                    win[r * 3 + c] =
+                                        use_depth ? D[(yy - 1 + r) * depth_pitch + (xx - 1 + c)]
+                                                  : G[(yy - 1 + r) * grey_pitch + (xx - 1 + c)];
+                            int32_t code = oracle_lbp_code_window(win);
+                            /* step 6 */
+                            int32_t bin = (bins == 256) ? code : U[code];
+                            /* step 7 */
+                            count[bin] += 1;
                         }
-                        if (!valid) continue;
-                        /* step 5: Eq. 2 */
-                        uint32_t win[9];
-                        for (int r = 0; r < 3; ++r)
-                            for (int c = 0; c < 3; ++c)
-                                win[r * 3 + c] = G[(yy - 1 + r) * grey_pitch + (xx - 1 + c)];
-                        int32_t code = oracle_lbp_code_window(win);
-                        /* step 6 */
-                        int32_t bin = (bins == 256) ? code : U[code];
-                        /* step 7 */
-                        count[bin] += 1;
-                    }
-                for (int32_t b = 0; b < bins; ++b)
-                    h[((int64_t)cy * cells_x + cx) * bins + b] = (uint16_t)count[b];
+                    for (int32_t b = 0; b < bins; ++b)
+                        hb[((int64_t)cy * cells_x + cx) * bins + b] = (uint16_t)count[b];
+                }
             }
         }
     }
     return ORC_OK;
+}
+
+/* The grey-source descriptor (the headline configuration, J.north_star). */
+int32_t oracle_lbp_extract(const uint8_t* grey, const uint16_t* depth,
+                           int32_t n_images, int32_t height, int32_t width,
+                           int64_t grey_pitch, int64_t depth_pitch,
+                           int64_t grey_img_stride, int64_t depth_img_stride,
+                           const int32_t* rois, int32_t n_rois,
+                           uint16_t dmin, uint16_t dmax,
+                           int32_t cells_x, int32_t cells_y, int32_t bins,
+                           uint16_t* desc, int32_t* roi_status)
+{
+    if (n_rois > 0 && !grey) return ORC_E_ARG;
+    return oracle_lbp_extract_src(grey, depth, n_images, height, width, grey_pitch, depth_pitch,
+                                  grey_img_stride, depth_img_stride, rois, n_rois, dmin, dmax,
+                                  cells_x, cells_y, bins, ORC_SRC_GREY, desc, roi_status);
 }
 
 /* ------------------------------------------------------------------------ */
