@@ -87,6 +87,30 @@ int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images
                           int32_t cells_x, int32_t cells_y, int32_t bins, uint16_t* desc,
                           int32_t* roi_status, lbp_stream_t stream);
 
+/* Source plane of the LBP codes. */
+enum {
+    LBP_SRC_GREY = 0,  /* codes on the grey image (lbp_fused_extract; the headline) */
+    LBP_SRC_DEPTH = 1, /* codes on the u16 depth image itself (Table 1 "Depth Image") */
+    LBP_SRC_FUSED = 2  /* grey descriptor then depth descriptor, 2*dim per ROI (P:17 fusion) */
+};
+
+/*
+ * lbp_extract_source -- lbp_fused_extract with a selectable code source (SURVEY §8f-1,
+ * DESIGN.md reading R17): every step is as documented for lbp_fused_extract (clamp, border,
+ * depth-window mask on the CENTRE pixel from `depth`, floor cells, bins, statuses) except
+ * step 5, where Eq. 2 reads the 3x3 neighbourhood of the source plane:
+ *   LBP_SRC_GREY   grey (u8); depth optional (NULL = no mask); identical to lbp_fused_extract
+ *   LBP_SRC_DEPTH  depth (u16, required; grey may be NULL): S(d_p - d_c) = [d_p >= d_c] on
+ *                  the raw millimetre values, holes (0) included as neighbours
+ *   LBP_SRC_FUSED  grey and depth required; desc row n = [grey block (dim) | depth block
+ *                  (dim)], i.e. u16 [n_rois][2*dim]
+ * Returns LBP_OK or a host-detectable error (LBP_E_ARG for a bad source or a missing plane).
+ */
+int32_t lbp_extract_source(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                           const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                           int32_t cells_x, int32_t cells_y, int32_t bins, int32_t source,
+                           uint16_t* desc, int32_t* roi_status, lbp_stream_t stream);
+
 /*
  * svm_score -- SURVEY §8a step a7: linear one-vs-rest SVM decision ("a classifier
  * defined by a hyperplane"; A-vs-B training per identity):

@@ -114,7 +114,8 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
                      const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
                      lbp_images_t geom,
                      const lbp_roi_t* __restrict__ rois, int32_t n_rois, DepthWindow win,
-                     uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status) {
+                     uint16_t* __restrict__ desc, int64_t desc_stride,
+                     int32_t* __restrict__ roi_status) {
     using Cfg = FastCfg<BINS>;
     constexpr int S = Cfg::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -200,8 +201,9 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (!roi_is_fast(r, geom)) {  // clamped / odd-sized ROI: generic path, same group
             named_barrier_sync(bar_id, kFastGroupThreads);  // previous epilogue finished
             extract_roi_generic<BINS, kFastGroupThreads>(
-                grey, HAS_DEPTH ? depth : nullptr, geom, r, n, win, kFastCells, kFastCells, desc,
-                roi_status, hist, 2 * Cfg::kHistWords, lut, BINS == 59 ? 2 : 0, gtid,
+                CodePlane<uint8_t>{grey, geom.grey_pitch, geom.grey_img_stride},
+                HAS_DEPTH ? depth : nullptr, geom, r, n, win, kFastCells, kFastCells, desc,
+                desc_stride, roi_status, hist, 2 * Cfg::kHistWords, lut, BINS == 59 ? 2 : 0, gtid,
                 GroupSync{bar_id});
             named_barrier_sync(bar_id, kFastGroupThreads);
             continue;
@@ -267,8 +269,8 @@ lbp_hist_fast_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         // ---- epilogue: packed u16 halves -> descriptor (16-B stores), re-zero this buffer.
         // Low halves are cells 0..31 (desc[0, 32*BINS)), high halves cells 32..63.
-        uint4* out_lo = reinterpret_cast<uint4*>(desc + (int64_t)n * Cfg::kDim);
-        uint4* out_hi = reinterpret_cast<uint4*>(desc + (int64_t)n * Cfg::kDim + Cfg::kHistWords);
+        uint4* out_lo = reinterpret_cast<uint4*>(desc + (int64_t)n * desc_stride);
+        uint4* out_hi = reinterpret_cast<uint4*>(desc + (int64_t)n * desc_stride + Cfg::kHistWords);
         for (int c = gtid; c < Cfg::kHistWords / 8; c += kFastGroupThreads) {
             const uint4 w0 = ld_shared_u32x4(hist_addr + c * 32);
             const uint4 w1 = ld_shared_u32x4(hist_addr + c * 32 + 16);
@@ -337,23 +339,23 @@ template <int BINS, bool HAS_DEPTH>
 inline cudaError_t launch_fast_t(const CUtensorMap& gm, const CUtensorMap& dm, const uint8_t* grey,
                                  const uint16_t* depth,
                                  const lbp_images_t& geom, const lbp_roi_t* rois, int32_t n_rois,
-                                 const DepthWindow& win, uint16_t* desc, int32_t* roi_status,
-                                 int sms, cudaStream_t stream) {
+                                 const DepthWindow& win, uint16_t* desc, int64_t desc_stride,
+                                 int32_t* roi_status, int sms, cudaStream_t stream) {
     auto kern = lbp_hist_fast_kernel<BINS, HAS_DEPTH>;
     const int smem = FastCfg<BINS>::kSmemBytes;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(sms, (n_rois + kFastGroups - 1) / kFastGroups));
     kern<<<grid, kFastThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win, desc,
-                                               roi_status);
+                                               desc_stride, roi_status);
     return cudaGetLastError();
 }
 
 inline cudaError_t launch_lbp_hist_fast(const uint8_t* grey, const uint16_t* depth,
                                         const lbp_images_t& geom, const lbp_roi_t* rois,
                                         int32_t n_rois, const DepthWindow& win, int32_t bins,
-                                        uint16_t* desc, int32_t* roi_status, int sms,
-                                        cudaStream_t stream) {
+                                        uint16_t* desc, int64_t desc_stride, int32_t* roi_status,
+                                        int sms, cudaStream_t stream) {
     CUtensorMap gm, dm;
     if (!encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
                           geom.grey_img_stride))
@@ -366,10 +368,10 @@ inline cudaError_t launch_lbp_hist_fast(const uint8_t* grey, const uint16_t* dep
         dm = gm;
     }
     if (bins == 59)
-        return depth ? launch_fast_t<59, true>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, roi_status, sms, stream)
-                     : launch_fast_t<59, false>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, roi_status, sms, stream);
-    return depth ? launch_fast_t<256, true>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, roi_status, sms, stream)
-                 : launch_fast_t<256, false>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, roi_status, sms, stream);
+        return depth ? launch_fast_t<59, true>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, desc_stride, roi_status, sms, stream)
+                     : launch_fast_t<59, false>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, desc_stride, roi_status, sms, stream);
+    return depth ? launch_fast_t<256, true>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, desc_stride, roi_status, sms, stream)
+                 : launch_fast_t<256, false>(gm, dm, grey, depth, geom, rois, n_rois, win, desc, desc_stride, roi_status, sms, stream);
 }
 
 }  // namespace lbpf

@@ -17,7 +17,9 @@ constexpr int kGenericThreads = 256;
 constexpr int kGenericHistCap = 12032;  // u32 counters per chunk (47 KB, static smem)
 
 // Eq. 2 with the Fig. 7 weights: TL 1, T 2, TR 4, R 8, BR 16, B 32, BL 64, L 128.
-__device__ __forceinline__ uint32_t lbp_code_scalar(const uint8_t* __restrict__ c, int64_t pitch) {
+// T = uint8_t (grey source) or uint16_t (depth source); pitch in elements.
+template <typename T>
+__device__ __forceinline__ uint32_t lbp_code_scalar(const T* __restrict__ c, int64_t pitch) {
     const uint32_t gc = __ldg(c);
     uint32_t code = 0;
     code |= (uint32_t)(__ldg(c - pitch - 1) >= gc) << 0;
@@ -31,26 +33,35 @@ __device__ __forceinline__ uint32_t lbp_code_scalar(const uint8_t* __restrict__ 
     return code;
 }
 
+// The image plane the codes are computed on: grey (u8) or depth (u16), pitches in elements.
+template <typename T>
+struct CodePlane {
+    const T* base;
+    int64_t pitch, img_stride;
+};
+
 // One ROI (index n) by a group of NT threads (t = 0..NT-1), hist = `cap` u32 of smem
 // that is all-zero on entry and is all-zero again on return.  lut[code] >> lut_shift is
-// the bin.  `sync()` synchronises the group.
-template <int BINS, int NT, typename Sync>
+// the bin.  `sync()` synchronises the group.  The descriptor row of ROI n starts at
+// desc + n * desc_stride (desc_stride >= dim; the fused grey||depth layout passes 2 * dim and
+// a desc already offset to its block).
+template <int BINS, int NT, typename T, typename Sync>
 __device__ __forceinline__ void extract_roi_generic(
-    const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth, const lbp_images_t& geom,
+    const CodePlane<T> plane, const uint16_t* __restrict__ depth, const lbp_images_t& geom,
     const lbp_roi_t roi, int32_t n, const DepthWindow& win, int32_t cells_x, int32_t cells_y,
-    uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status, uint32_t* hist, int cap,
-    const uint8_t* lut, int lut_shift, int t, Sync sync) {
+    uint16_t* __restrict__ desc, int64_t desc_stride, int32_t* __restrict__ roi_status,
+    uint32_t* hist, int cap, const uint8_t* lut, int lut_shift, int t, Sync sync) {
     const int64_t dim = (int64_t)cells_x * cells_y * BINS;
     const int warp = t >> 5, lane = t & 31;
     constexpr int kWarps = NT / 32;
     const RoiGeom r = clamp_roi(roi, geom, cells_x, cells_y);
-    uint16_t* out = desc + (int64_t)n * dim;
+    uint16_t* out = desc + (int64_t)n * desc_stride;
     if (t == 0 && roi_status) roi_status[n] = r.status;
     if (r.status != LBP_OK) {
         for (int64_t i = t; i < dim; i += NT) out[i] = 0;
         return;
     }
-    const uint8_t* G = grey + (int64_t)r.img * geom.grey_img_stride;
+    const T* G = plane.base + (int64_t)r.img * plane.img_stride;
     const uint16_t* D = depth ? depth + (int64_t)r.img * geom.depth_img_stride : nullptr;
     const int32_t n_cells = cells_x * cells_y;
     const int32_t cells_per_chunk = cap / BINS;
@@ -71,7 +82,7 @@ __device__ __forceinline__ void extract_roi_generic(
         for (int32_t i = i_begin + warp; i < i_end; i += kWarps) {
             const int32_t cy = (int32_t)(((int64_t)(i + 1) * cells_y - 1) / r.hi);
             const int64_t yy = (int64_t)r.y0 + 1 + i;
-            const uint8_t* grow = G + yy * geom.grey_pitch + r.x0 + 1;
+            const T* grow = G + yy * plane.pitch + r.x0 + 1;
             const uint16_t* drow = D ? D + yy * geom.depth_pitch + r.x0 + 1 : nullptr;
             // 4 columns per lane per iteration: their 4 x 10 independent global loads are in
             // flight together (latency-bound otherwise: one ROI per CTA, L2/DRAM latency)
@@ -89,7 +100,7 @@ __device__ __forceinline__ void extract_roi_generic(
                         const uint32_t d = __ldg(drow + jj);
                         ok[u] = ok[u] && !win.none_valid && (d - win.lo) <= win.span;
                     }
-                    code[u] = lbp_code_scalar(grow + jj, geom.grey_pitch);
+                    code[u] = lbp_code_scalar(grow + jj, plane.pitch);
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -110,12 +121,13 @@ struct CtaSync {
     __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
 
-template <int BINS>
+template <int BINS, typename T>
 __global__ void __launch_bounds__(kGenericThreads)
-lbp_hist_generic_kernel(const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
+lbp_hist_generic_kernel(const CodePlane<T> plane, const uint16_t* __restrict__ depth,
                         lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
                         DepthWindow win, int32_t cells_x, int32_t cells_y,
-                        uint16_t* __restrict__ desc, int32_t* __restrict__ roi_status) {
+                        uint16_t* __restrict__ desc, int64_t desc_stride,
+                        int32_t* __restrict__ roi_status) {
     __shared__ uint32_t hist[kGenericHistCap];
     __shared__ uint8_t lut[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
@@ -125,8 +137,8 @@ lbp_hist_generic_kernel(const uint8_t* __restrict__ grey, const uint16_t* __rest
     for (int i = threadIdx.x; i < used; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int32_t n = blockIdx.x; n < n_rois; n += gridDim.x) {
-        extract_roi_generic<BINS, kGenericThreads>(grey, depth, geom, rois[n], n, win, cells_x,
-                                                   cells_y, desc, roi_status, hist,
+        extract_roi_generic<BINS, kGenericThreads>(plane, depth, geom, rois[n], n, win, cells_x,
+                                                   cells_y, desc, desc_stride, roi_status, hist,
                                                    kGenericHistCap, lut, 0, (int)threadIdx.x,
                                                    CtaSync{});
     }

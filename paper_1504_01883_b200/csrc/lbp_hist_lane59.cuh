@@ -121,7 +121,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const __grid_constant__ CUtensorMap depth_map,
                        const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
                        lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
-                       DepthWindow win, uint16_t* __restrict__ desc,
+                       DepthWindow win, uint16_t* __restrict__ desc, int64_t desc_stride,
                        int32_t* __restrict__ roi_status) {
     using namespace l59;
     extern __shared__ uint8_t smem_raw[];
@@ -207,7 +207,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (!roi_is_fast(roi, geom)) {
             if (gtid == 0) issue(i + kStages);  // stage s was never filled: release it at once
             extract_roi_generic<kBins, kGroupThreads>(
-                grey, HAS_DEPTH ? depth : nullptr, geom, roi, n, win, 8, 8, desc, roi_status,
+                CodePlane<uint8_t>{grey, geom.grey_pitch, geom.grey_img_stride},
+                HAS_DEPTH ? depth : nullptr, geom, roi, n, win, 8, 8, desc, desc_stride, roi_status,
                 reinterpret_cast<uint32_t*>(smem + (hist0 - stages0)), kHistBytes / 4,
                 smem + kPlainLutOff, 0, gtid, GroupSync{bar_id});
             named_barrier_sync(bar_id, kGroupThreads);
@@ -289,7 +290,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         fence_proxy_async_smem();                   // staging writes -> async proxy
         named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-        if (gtid == 0) bulk_store_s2g(desc + (int64_t)n * (64 * kBins), staging, kDescBytes);
+        if (gtid == 0) bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
         pending = n;
     }
     if (gtid == 0 && pending >= 0) bulk_wait_all();
@@ -298,7 +299,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
 inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* depth,
                                           const lbp_images_t& geom, const lbp_roi_t* rois,
                                           int32_t n_rois, const DepthWindow& win, uint16_t* desc,
-                                          int32_t* roi_status, int sms, cudaStream_t stream) {
+                                          int64_t desc_stride, int32_t* roi_status, int sms,
+                                          cudaStream_t stream) {
     CUtensorMap gm, dm;
     if (!encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
                           geom.grey_img_stride))
@@ -316,7 +318,7 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(sms, n_rois));
     kern<<<grid, l59::kThreads, l59::kSmemBytes, stream>>>(gm, dm, grey, depth, geom, rois, n_rois,
-                                                          win, desc, roi_status);
+                                                          win, desc, desc_stride, roi_status);
     return cudaGetLastError();
 }
 

@@ -21,9 +21,10 @@ int32_t launch_status(cudaError_t e) {
     return LBP_E_CUDA;
 }
 
-int32_t check_geometry(const lbp_images_t& g, bool has_depth) {
+int32_t check_geometry(const lbp_images_t& g, bool has_grey, bool has_depth) {
     if (g.n_images < 1 || g.height < 1 || g.width < 1 || g.reserved != 0) return LBP_E_ARG;
-    if (g.grey_pitch < g.width || g.grey_img_stride < g.grey_pitch * (g.height - 1) + g.width)
+    if (has_grey && (g.grey_pitch < g.width ||
+                     g.grey_img_stride < g.grey_pitch * (g.height - 1) + g.width))
         return LBP_E_ARG;
     if (has_depth && (g.depth_pitch < g.width ||
                       g.depth_img_stride < g.depth_pitch * (g.height - 1) + g.width))
@@ -61,38 +62,96 @@ const char* lbp_status_string(int32_t s) {
     }
 }
 
-int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
-                          const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
-                          int32_t cells_x, int32_t cells_y, int32_t bins, uint16_t* desc,
-                          int32_t* roi_status, lbp_stream_t stream_) {
+}  // extern "C"
+
+namespace {
+
+// One descriptor block: codes of `plane` (grey u8 or depth u16), depth-window mask from
+// `depth`, rows of desc_stride elements starting at `desc`.
+int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_source,
+                      const lbp_images_t& geom, const lbp_roi_t* rois, int32_t n_rois,
+                      const DepthWindow& win, int32_t cells_x, int32_t cells_y, int32_t bins,
+                      uint16_t* desc, int64_t desc_stride, int32_t* roi_status,
+                      cudaStream_t stream) {
+    if (!depth_source) {
+        // Fast path (8x8 cells, 16-B aligned rows): one TMA-staged persistent kernel; ROIs
+        // that are not fully-inside 128x128 boxes take the generic code path inside it.
+        if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc) &&
+            ((desc_stride * 2) & 15) == 0) {
+            if (bins == 59)  // conflict-free lane-private kernel (the headline configuration)
+                return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win,
+                                                            desc, desc_stride, roi_status,
+                                                            num_sms(), stream));
+            return launch_status(launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins,
+                                                      desc, desc_stride, roi_status, num_sms(),
+                                                      stream));
+        }
+    }
+    const int grid = (int)std::min<int64_t>(n_rois, (int64_t)num_sms() * 8);
+    if (depth_source) {
+        const CodePlane<uint16_t> plane{depth, geom.depth_pitch, geom.depth_img_stride};
+        if (bins == 59)
+            lbp_hist_generic_kernel<59><<<grid, kGenericThreads, 0, stream>>>(
+                plane, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, desc_stride,
+                roi_status);
+        else
+            lbp_hist_generic_kernel<256><<<grid, kGenericThreads, 0, stream>>>(
+                plane, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, desc_stride,
+                roi_status);
+    } else {
+        const CodePlane<uint8_t> plane{grey, geom.grey_pitch, geom.grey_img_stride};
+        if (bins == 59)
+            lbp_hist_generic_kernel<59><<<grid, kGenericThreads, 0, stream>>>(
+                plane, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, desc_stride,
+                roi_status);
+        else
+            lbp_hist_generic_kernel<256><<<grid, kGenericThreads, 0, stream>>>(
+                plane, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, desc_stride,
+                roi_status);
+    }
+    return launch_status(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t lbp_extract_source(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                           const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                           int32_t cells_x, int32_t cells_y, int32_t bins, int32_t source,
+                           uint16_t* desc, int32_t* roi_status, lbp_stream_t stream_) {
     if (n_rois < 0) return LBP_E_ARG;
+    if (source != LBP_SRC_GREY && source != LBP_SRC_DEPTH && source != LBP_SRC_FUSED)
+        return LBP_E_ARG;
     const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
     if (dim < 0) return dim;
+    if (source == LBP_SRC_FUSED && dim > 0x3FFFFFFF) return LBP_E_ARG;
     if (dmin > dmax) return LBP_E_ARG;
     if (n_rois == 0) return LBP_OK;
-    if (!grey || !rois || !desc) return LBP_E_ARG;
-    int32_t st = check_geometry(geom, depth != nullptr);
+    const bool need_grey = source != LBP_SRC_DEPTH, need_depth = source != LBP_SRC_GREY;
+    if (!rois || !desc || (need_grey && !grey) || (need_depth && !depth)) return LBP_E_ARG;
+    int32_t st = check_geometry(geom, need_grey, depth != nullptr);
     if (st != LBP_OK) return st;
     cudaStream_t stream = (cudaStream_t)stream_;
     const DepthWindow win = make_window(dmin, dmax);
-
-    // Fast path (8x8 cells, 16-B aligned rows): one TMA-staged persistent kernel; ROIs that
-    // are not fully-inside 128x128 boxes take the generic code path inside it.
-    if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc)) {
-        if (bins == 59)  // conflict-free lane-private kernel (the headline configuration)
-            return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win,
-                                                        desc, roi_status, num_sms(), stream));
-        return launch_status(launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins,
-                                                  desc, roi_status, num_sms(), stream));
+    const int64_t stride = source == LBP_SRC_FUSED ? 2 * (int64_t)dim : dim;
+    if (need_grey) {
+        st = extract_block(grey, depth, false, geom, rois, n_rois, win, cells_x, cells_y, bins,
+                           desc, stride, roi_status, stream);
+        if (st != LBP_OK) return st;
     }
-    const int grid = (int)std::min<int64_t>(n_rois, (int64_t)num_sms() * 8);
-    if (bins == 59)
-        lbp_hist_generic_kernel<59><<<grid, kGenericThreads, 0, stream>>>(
-            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status);
-    else
-        lbp_hist_generic_kernel<256><<<grid, kGenericThreads, 0, stream>>>(
-            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, roi_status);
-    return launch_status(cudaGetLastError());
+    if (need_depth)
+        st = extract_block(grey, depth, true, geom, rois, n_rois, win, cells_x, cells_y, bins,
+                           desc + (source == LBP_SRC_FUSED ? dim : 0), stride, roi_status, stream);
+    return st;
+}
+
+int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                          const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                          int32_t cells_x, int32_t cells_y, int32_t bins, uint16_t* desc,
+                          int32_t* roi_status, lbp_stream_t stream) {
+    return lbp_extract_source(grey, depth, geom, rois, n_rois, dmin, dmax, cells_x, cells_y, bins,
+                              LBP_SRC_GREY, desc, roi_status, stream);
 }
 
 int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, const float* bias,
@@ -191,7 +250,7 @@ RecognizeLayout recognize_layout(const lbp_images_t& g, bool has_depth, int32_t 
 size_t lbp_recognize_workspace_bytes(lbp_images_t geom, int32_t has_depth, int32_t n_rois,
                                      int32_t cells_x, int32_t cells_y, int32_t bins) {
     const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
-    if (dim < 0 || n_rois < 0 || check_geometry(geom, has_depth != 0) != LBP_OK) return 0;
+    if (dim < 0 || n_rois < 0 || check_geometry(geom, true, has_depth != 0) != LBP_OK) return 0;
     return recognize_layout(geom, has_depth != 0, n_rois, dim).total;
 }
 
@@ -207,7 +266,7 @@ int32_t lbp_recognize_host(const uint8_t* grey_h, const uint16_t* depth_h, lbp_i
     if (dmin > dmax) return LBP_E_ARG;
     if (n_rois == 0) return LBP_OK;
     if (!grey_h || !rois_h || !W || !bias || !workspace) return LBP_E_ARG;
-    int32_t st = check_geometry(geom, depth_h != nullptr);
+    int32_t st = check_geometry(geom, true, depth_h != nullptr);
     if (st != LBP_OK) return st;
     const RecognizeLayout L = recognize_layout(geom, depth_h != nullptr, n_rois, dim);
     if (workspace_bytes < L.total) return LBP_E_ARG;

@@ -17,6 +17,7 @@ from . import build as _build
 
 LBP_OK, LBP_E_ARG, LBP_E_ROI, LBP_E_GRID, LBP_E_OVERFLOW, LBP_E_UNSUPPORTED, LBP_E_CUDA = \
     0, -1, -2, -3, -4, -5, -6
+LBP_SRC_GREY, LBP_SRC_DEPTH, LBP_SRC_FUSED = 0, 1, 2
 
 
 class LbpError(RuntimeError):
@@ -51,6 +52,9 @@ def lib():
         L.lbp_status_string.restype = ctypes.c_char_p
         L.lbp_fused_extract.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, P, P, P]
         L.lbp_fused_extract.restype = i32
+        L.lbp_extract_source.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, i32,
+                                         P, P, P]
+        L.lbp_extract_source.restype = i32
         L.svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, P, f32, P]
         L.svm_score.restype = i32
         L.svm_workspace_bytes.argtypes = [i32, i32]
@@ -90,8 +94,14 @@ def _stack3(t: torch.Tensor) -> torch.Tensor:
     return t.unsqueeze(0) if t.dim() == 2 else t
 
 
-def images_geometry(grey: torch.Tensor, depth: torch.Tensor | None) -> lbp_images_t:
+def images_geometry(grey: torch.Tensor | None, depth: torch.Tensor | None) -> lbp_images_t:
     """lbp_images_t from [n_images][H][W] (or [H][W]) tensors with unit column stride."""
+    if grey is None:  # depth-only stack (LBP_SRC_DEPTH)
+        d = _stack3(depth)
+        if d.stride(2) != 1:
+            raise ValueError("depth rows must be contiguous")
+        n, H, W = d.shape
+        return lbp_images_t(n, H, W, 0, W, d.stride(1), n * H * W, d.stride(0))
     g = _stack3(grey)
     if g.stride(2) != 1:
         raise ValueError("grey rows must be contiguous")
@@ -131,6 +141,35 @@ def lbp_fused_extract(grey: torch.Tensor, depth: torch.Tensor | None, rois: torc
                                  _ptr(roi_status), _stream(stream))
     if st != LBP_OK:
         raise LbpError(st, "lbp_fused_extract")
+    return out
+
+
+def lbp_extract_source(grey: torch.Tensor | None, depth: torch.Tensor | None,
+                       rois: torch.Tensor, dmin: int, dmax: int, cells_x: int, cells_y: int,
+                       bins: int, source: int, out: torch.Tensor | None = None,
+                       roi_status: torch.Tensor | None = None,
+                       stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Descriptors with the code source selectable (LBP_SRC_GREY / _DEPTH / _FUSED): u16
+    [n_rois][dim] (grey or depth) or [n_rois][2*dim] (fused: grey block then depth block)."""
+    _check_cuda(grey, depth, rois, out, roi_status)
+    assert grey is None or grey.dtype == torch.uint8
+    assert depth is None or depth.dtype == torch.uint16
+    assert rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5
+    if grey is None and depth is None:
+        raise LbpError(LBP_E_ARG, "lbp_extract_source: no image plane")
+    n = rois.shape[0]
+    dim = lbp_descriptor_dim(cells_x, cells_y, bins) * (2 if source == LBP_SRC_FUSED else 1)
+    dev = (grey if grey is not None else depth).device
+    if out is None:
+        out = torch.empty((n, dim), dtype=torch.uint16, device=dev)
+    assert out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim
+    if roi_status is not None:
+        assert roi_status.dtype == torch.int32 and roi_status.numel() >= n
+    st = lib().lbp_extract_source(_ptr(grey), _ptr(depth), images_geometry(grey, depth),
+                                  _ptr(rois), n, dmin, dmax, cells_x, cells_y, bins, source,
+                                  _ptr(out), _ptr(roi_status), _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_extract_source")
     return out
 
 

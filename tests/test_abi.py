@@ -78,6 +78,29 @@ def test_extract_argument_errors_enqueue_nothing(L):
     assert call(geom=bad) == lb.LBP_E_ARG
 
 
+def test_extract_source_argument_errors(L):
+    """lbp_extract_source: bad source, missing plane for the source, grey-free depth source
+    validated on the depth geometry only."""
+    from paper_1504_01883_b200 import lbpfused as lb
+    P = ctypes.c_void_p
+    dummy = P(0x1000)
+    g = _geom(lb)
+
+    def call(source, grey=dummy, depth=dummy, n=1, geom=g):
+        return L.lbp_extract_source(grey, depth, geom, dummy, n, 0, 10, 2, 2, 59, source, dummy,
+                                    None, None)
+    assert call(3) == lb.LBP_E_ARG
+    assert call(-1) == lb.LBP_E_ARG
+    assert call(lb.LBP_SRC_DEPTH, depth=None) == lb.LBP_E_ARG
+    assert call(lb.LBP_SRC_FUSED, depth=None) == lb.LBP_E_ARG
+    assert call(lb.LBP_SRC_FUSED, grey=None) == lb.LBP_E_ARG
+    assert call(lb.LBP_SRC_GREY, grey=None) == lb.LBP_E_ARG
+    assert call(lb.LBP_SRC_DEPTH, n=0) == lb.LBP_OK
+    bad = _geom(lb)
+    bad.depth_pitch = 7
+    assert call(lb.LBP_SRC_DEPTH, grey=None, geom=bad) == lb.LBP_E_ARG
+
+
 def test_svm_argument_errors(L):
     from paper_1504_01883_b200 import lbpfused as lb
     P = ctypes.c_void_p
