@@ -56,6 +56,9 @@ N_IDS = 100  # identities of the database build (label = crop index mod N_IDS)
 DMIN, DMAX = 600, 1400
 
 
+SOURCES = {"grey": 0, "depth": 1, "fused": 2}  # LBP_SRC_* of include/lbpfused.h
+
+
 def bytes_per_crop(H, W, cx, cy, bins):
     """Algorithmic HBM bytes of the extraction kernel per crop:
     grey u8 + depth u16 read once, u16 descriptor written once."""
@@ -73,6 +76,9 @@ def parse():
     p.add_argument("--dist", default="face", choices=["face", "constant", "noise"])
     p.add_argument("--no-depth", action="store_true")
     p.add_argument("--bins", type=int, default=0)
+    p.add_argument("--source", default="grey", choices=sorted(SOURCES),
+                   help="LBP code plane (configs 3/4): grey (headline), depth, or fused "
+                        "grey||depth descriptor (SURVEY §8f-1)")
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 10)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
@@ -141,7 +147,7 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- CPU oracle
 
-def oracle_rate(grey, depth, rois, W, b, cx, cy, bins, budget_s, threads):
+def oracle_rate(grey, depth, rois, W, b, cx, cy, bins, budget_s, threads, source=0):
     """Times the UNMODIFIED oracle (extraction + SVM) on T threads over disjoint shards of the
     sample, repeating passes over the sample until about `budget_s` seconds have elapsed.
 
@@ -157,7 +163,7 @@ def oracle_rate(grey, depth, rois, W, b, cx, cy, bins, budget_s, threads):
         if idx.size == 0:
             return
         dd = oracle.lbp_extract(grey[idx], depth[idx] if depth is not None else None,
-                                _local_rois(rois[idx]), DMIN, DMAX, cx, cy, bins)
+                                _local_rois(rois[idx]), DMIN, DMAX, cx, cy, bins, source=source)
         _, lab, _ = oracle.svm_score(dd, W, b)
         out_desc[i], out_lab[i] = dd, lab
 
@@ -251,6 +257,7 @@ def workload_config(args, n, H, W, cx, cy, bins, C, desc_txt):
     return {"workload": f"{args.workload}: {desc_txt}", "crops_per_gpu": n, "crop": f"{H}x{W}",
             "cells": f"{cx}x{cy}", "bins": bins, "classes": C, "dist": args.dist,
             "depth_mask": not args.no_depth, "depth_window_mm": [DMIN, DMAX],
+            "source": getattr(args, "source", "grey"),
             "parallelism": f"crop-sharded dp{args.gpus}",
             "l2": "inputs larger than L2 (no flush needed)" if n * H * W * 3 > 126e6 else
                   "inputs L2-resident (latency config)"}
@@ -284,7 +291,10 @@ def main():
     n, H, Wd, cx, cy, bins, C, desc_txt = WORKLOADS[args.workload]
     n = args.crops or n
     bins = args.bins or bins
-    dim = cx * cy * bins
+    source = SOURCES[args.source]
+    if source != 0 and args.no_depth:
+        raise SystemExit("--source depth/fused needs the depth plane")
+    dim = cx * cy * bins * (2 if source == 2 else 1)
     first = rank * n  # global crop indices of this rank: [rank*n, (rank+1)*n)
 
     grey, depth = synthgen.gpu_face_crops(n, H, Wd, seed=args.seed, first_index=first,
@@ -304,13 +314,18 @@ def main():
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        lb.lbp_fused_extract(grey, depth, rois, DMIN, DMAX, cx, cy, bins, out=desc, stream=stream)
+        if source == 0:
+            lb.lbp_fused_extract(grey, depth, rois, DMIN, DMAX, cx, cy, bins, out=desc,
+                                 stream=stream)
+        else:
+            lb.lbp_extract_source(grey, depth, rois, DMIN, DMAX, cx, cy, bins, source, out=desc,
+                                  stream=stream)
         if ev is not None:
             ev[1].record(stream)
         lb.svm_score(desc, W, b, prepared=prepared, want_scores=False, labels=labels,
                      top_score=top, stream=stream)
 
-    launches_per_step = 2
+    launches_per_step = 3 if source == 2 else 2  # extraction kernel(s) + svm_gemm
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -340,19 +355,27 @@ def main():
     value = n * world / (ms_per_step * 1e-3)
 
     # ---- end to end through the public C ABI from pinned HOST buffers
-    e2e = run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins, W, b,
-                  prepared, n)
+    e2e = None
+    if source == 0:  # lbp_recognize_host computes the grey-source descriptor
+        e2e = run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins, W, b,
+                      prepared, n)
 
     # ---- roofline of the dominant kernel (lbp_hist): algorithmic bytes / avg launch time
     peaks = load_peaks()
-    bpc = bytes_per_crop(H, Wd, cx, cy, bins) if depth is not None else H * Wd + dim * 2
+    if source == 0:
+        bpc = bytes_per_crop(H, Wd, cx, cy, bins) if depth is not None else H * Wd + dim * 2
+    elif source == 1:
+        bpc = H * Wd * 2 + dim * 2  # depth read once (mask + codes), descriptor written
+    else:
+        bpc = H * Wd * 3 + dim * 2  # grey + depth read once, both blocks written
     achieved = bpc * n / (ext_ms * 1e-3) / 1e9
     peak, peak_src = peaks
-    roofline = {"bound": "hbm", "kernel": "lbp_hist (extraction)", "achieved": achieved,
+    roofline = {"bound": "hbm", "kernel": "lbp_hist (extraction)" if source == 0 else
+                "extraction (" + args.source + " source)", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
                 "peak_source": peak_src, "bytes_per_crop": bpc,
                 "kernel_ms": ext_ms, "kernel_share_of_step": ext_ms / ms_per_step,
-                "traffic": load_traffic(args.workload)}
+                "traffic": load_traffic(args.workload) if source == 0 else None}
 
     # ---- CPU oracle baseline (rank 0, N=1 only) + equivalence gate on its sample
     cpu = None
@@ -629,7 +652,8 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
     d = depth[:m].cpu().view(torch.int16).numpy().view(np.uint16) if depth is not None else None
     r = rois[:m].cpu().numpy()
     rate, done, secs, passes, odesc, olab = oracle_rate(g, d, r, W_np, b_np, cx, cy, bins,
-                                                        args.cpu_seconds, threads)
+                                                        args.cpu_seconds, threads,
+                                                        SOURCES[args.source])
     gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
     glab = labels[:m].cpu().numpy()
     ok = bool(np.array_equal(gdesc, odesc))
