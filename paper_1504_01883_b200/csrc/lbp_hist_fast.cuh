@@ -296,13 +296,15 @@ inline bool fast_path_applicable(const lbp_images_t& g, const uint8_t* grey, con
     if (reinterpret_cast<uintptr_t>(desc) & 15) return false;
     if (bins != 59 && bins != 256) return false;
     if (g.width < kFastTile || g.height < kFastTile) return false;
-    if ((reinterpret_cast<uintptr_t>(grey) & 15) || (g.grey_pitch & 15) || (g.grey_img_stride & 15))
-        return false;
+    if (grey && ((reinterpret_cast<uintptr_t>(grey) & 15) || (g.grey_pitch & 15) ||
+                 (g.grey_img_stride & 15)))
+        return false;  // (grey == NULL: depth-source launch, grey unused)
     if (depth && ((reinterpret_cast<uintptr_t>(depth) & 15) || ((g.depth_pitch * 2) & 15) ||
                   ((g.depth_img_stride * 2) & 15)))
         return false;
     // TMA: strides < 2^40 bytes
-    if (g.grey_img_stride >= (int64_t(1) << 39) || g.depth_img_stride >= (int64_t(1) << 38))
+    if ((grey && g.grey_img_stride >= (int64_t(1) << 39)) ||
+        (depth && g.depth_img_stride >= (int64_t(1) << 38)))
         return false;
     return true;
 }

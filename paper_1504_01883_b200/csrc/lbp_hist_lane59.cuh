@@ -115,7 +115,61 @@ __device__ __forceinline__ uint32_t lbp_offset2(uint32_t c, uint32_t tl, uint32_
     return f + a;  // no carry between halves (each half <= 0x6400 + 8067)
 }
 
-template <bool HAS_DEPTH>
+// ---- depth source: codes on the u16 depth plane.  A u16 d <= 0x7BFF read as
+// fp16 bits is a non-negative finite half, and the bit order of those halves is their value
+// order, so HSET2 on the raw bits is an exact unsigned compare.  Every depth word is clamped
+// to 0x7BFF first (VIMNMX.U16x2); this is exact for the codes that are counted when
+// dmax <= 0x7BFE: a counted centre c <= dmax < 0x7BFF, so min(n, 0x7BFF) >= c iff n >= c
+// (the host takes the generic kernel otherwise).
+struct DepthRow {
+    uint32_t h0, h1;        // clamped (4l, 4l+1), (4l+2, 4l+3)
+    uint32_t lh0, mh, rh1;  // (4l-1, 4l), (4l+1, 4l+2), (4l+3, 4l+4)
+    uint32_t raw0, raw1;    // unclamped words, for the depth-window test of centre rows
+};
+
+__device__ __forceinline__ uint32_t vmin_u16x2(uint32_t a, uint32_t b) {
+    return __vminu2(a, b);  // VIMNMX.U16x2
+}
+
+__device__ __forceinline__ DepthRow depth_row(uint32_t addr) {
+    const uint2 w = ld_shared_u32x2(addr);
+    DepthRow r;
+    r.raw0 = w.x;
+    r.raw1 = w.y;
+    r.h0 = vmin_u16x2(w.x, 0x7BFF7BFFu);
+    r.h1 = vmin_u16x2(w.y, 0x7BFF7BFFu);
+    const uint32_t left = __shfl_up_sync(0xFFFFFFFFu, r.h1, 1);
+    const uint32_t right = __shfl_down_sync(0xFFFFFFFFu, r.h0, 1);
+    r.lh0 = prmt(left, r.h0, 0x5432);
+    r.mh = prmt(r.h0, r.h1, 0x5432);
+    r.rh1 = prmt(r.h1, right, 0x5432);
+    return r;
+}
+
+__device__ __forceinline__ uint32_t hge2_one(uint32_t a, uint32_t b) {
+    uint32_t r;  // 1.0 / 0.0 per half
+    asm("set.ge.f16x2.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+// Same LUT offset as lbp_offset2, every bit from an exact compare: TL, T, TR, R, BR as
+// 1.0/0.0 halves accumulated by HFMA2 onto 1024.0 (weights 1, 2, 128, 256, 512; exact
+// fp16 integers <= 1923), B, BL, L as HSET2 masks at 1024..4096.
+__device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uint32_t t,
+                                                    uint32_t tr, uint32_t r, uint32_t br,
+                                                    uint32_t b, uint32_t bl, uint32_t l) {
+    uint32_t f = f16_fma(hge2_one(tl, c), 0x3C003C00u, 0x64006400u);  // TL +1
+    f = f16_fma(hge2_one(t, c), 0x40004000u, f);                       // T  +2
+    f = f16_fma(hge2_one(tr, c), 0x58005800u, f);                      // TR +128
+    f = f16_fma(hge2_one(r, c), 0x5C005C00u, f);                       // R  +256
+    f = f16_fma(hge2_one(br, c), 0x60006000u, f);                      // BR +512
+    uint32_t a = hge2_mask(b, c) & 0x04000400u;                        // B  +1024
+    a |= hge2_mask(bl, c) & 0x08000800u;                               // BL +2048
+    a |= hge2_mask(l, c) & 0x10001000u;                                // L  +4096
+    return f + a;
+}
+
+template <bool HAS_DEPTH, bool DEPTH_SRC>
 __global__ void __launch_bounds__(l59::kThreads, 1)
 lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const __grid_constant__ CUtensorMap depth_map,
@@ -146,9 +200,10 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int s = i % kStages;
         const lbp_roi_t r = rois[crop_of(i)];
         if (roi_is_fast(r, geom)) {
-            mbar_arrive_expect_tx(&bars[s], HAS_DEPTH ? kStageBytes : kGreyBytes);
+            mbar_arrive_expect_tx(&bars[s], DEPTH_SRC ? kStageBytes - kGreyBytes
+                                                      : HAS_DEPTH ? kStageBytes : kGreyBytes);
             uint8_t* st = smem + s * kStageBytes;
-            tma_load_3d(st, &grey_map, &bars[s], r.x, r.y, r.img);
+            if (!DEPTH_SRC) tma_load_3d(st, &grey_map, &bars[s], r.x, r.y, r.img);
             if (HAS_DEPTH) tma_load_3d(st + kGreyBytes, &depth_map, &bars[s], r.x, r.y, r.img);
         } else {
             mbar_arrive(&bars[s]);
@@ -206,6 +261,13 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
         if (!roi_is_fast(roi, geom)) {
             if (gtid == 0) issue(i + kStages);  // stage s was never filled: release it at once
+            if (DEPTH_SRC)
+                extract_roi_generic<kBins, kGroupThreads>(
+                    CodePlane<uint16_t>{depth, geom.depth_pitch, geom.depth_img_stride}, depth, geom,
+                    roi, n, win, 8, 8, desc, desc_stride, roi_status,
+                    reinterpret_cast<uint32_t*>(smem + (hist0 - stages0)), kHistBytes / 4,
+                    smem + kPlainLutOff, 0, gtid, GroupSync{bar_id});
+            else
             extract_roi_generic<kBins, kGroupThreads>(
                 CodePlane<uint8_t>{grey, geom.grey_pitch, geom.grey_img_stride},
                 HAS_DEPTH ? depth : nullptr, geom, roi, n, win, 8, 8, desc, desc_stride, roi_status,
@@ -215,17 +277,35 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             continue;
         }
         const uint32_t st = stages0 + s * kStageBytes;
-        const uint32_t g0 = opaque(st + i0 * kTile + 4 * lane);
+        // code plane rows: grey u8 (128 B per row) or depth u16 (256 B per row, DEPTH_SRC)
+        constexpr uint32_t kRowStep = DEPTH_SRC ? kTile * 2 : kTile;
+        const uint32_t g0 = DEPTH_SRC ? opaque(st + kGreyBytes + i0 * (kTile * 2) + 8 * lane)
+                                      : opaque(st + i0 * kTile + 4 * lane);
         const uint32_t d0 = opaque(st + kGreyBytes + (i0 + 1) * (kTile * 2) + 8 * lane);
+        auto load_row = [&](uint32_t addr) {
+            if constexpr (DEPTH_SRC) return depth_row(addr);
+            else return lane_row(addr);
+        };
+        using Row = decltype(load_row(0u));
 
-        auto do_row = [&](const LaneRow& top, const LaneRow& mid, const LaneRow& bot, int j) {
-            const uint32_t t0 = lbp_offset2(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
-                                            bot.lh0, mid.lh0);
-            const uint32_t t1 = lbp_offset2(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1,
-                                            bot.h1, bot.mh, mid.mh);
+        auto do_row = [&](const Row& top, const Row& mid, const Row& bot, int j) {
+            uint32_t t0, t1;
+            if constexpr (DEPTH_SRC) {
+                t0 = lbp_offset2_cmp(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
+                                     bot.lh0, mid.lh0);
+                t1 = lbp_offset2_cmp(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
+                                     bot.mh, mid.mh);
+            } else {
+                t0 = lbp_offset2(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
+                                 bot.lh0, mid.lh0);
+                t1 = lbp_offset2(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
+                                 bot.mh, mid.mh);
+            }
             uint32_t val[4];
             if (HAS_DEPTH) {
-                const uint2 d = ld_shared_u32x2(d0 + j * (kTile * 2));
+                uint2 d;
+                if constexpr (DEPTH_SRC) d = make_uint2(mid.raw0, mid.raw1);  // centre row
+                else d = ld_shared_u32x2(d0 + j * (kTile * 2));
                 // depth window on a u16 in either half of a word
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
@@ -245,18 +325,18 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         };
         // 16 rows, straight-line.  Cell rows with 15 rows run a 16th dummy row whose
         // increments are 0 (its pixels belong to the next warp; its rows exist in the crop).
-        LaneRow r0 = lane_row(g0), r1 = lane_row(g0 + kTile), r2;
+        Row r0 = load_row(g0), r1 = load_row(g0 + kRowStep), r2;
 #pragma unroll
         for (int j = 0; j < 15; j += 3) {
-            r2 = lane_row(g0 + (j + 2) * kTile); do_row(r0, r1, r2, j);
-            r0 = lane_row(g0 + (j + 3) * kTile); do_row(r1, r2, r0, j + 1);
-            r1 = lane_row(g0 + (j + 4) * kTile); do_row(r2, r0, r1, j + 2);
+            r2 = load_row(g0 + (j + 2) * kRowStep); do_row(r0, r1, r2, j);
+            r0 = load_row(g0 + (j + 3) * kRowStep); do_row(r1, r2, r0, j + 1);
+            r1 = load_row(g0 + (j + 4) * kRowStep); do_row(r2, r0, r1, j + 2);
         }
         if (nrows < 16) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
         }
-        r2 = lane_row(g0 + 17 * kTile);
+        r2 = load_row(g0 + 17 * kRowStep);
         do_row(r0, r1, r2, 15);
 #pragma unroll
         for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
@@ -300,9 +380,10 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
                                           const lbp_images_t& geom, const lbp_roi_t* rois,
                                           int32_t n_rois, const DepthWindow& win, uint16_t* desc,
                                           int64_t desc_stride, int32_t* roi_status, int sms,
-                                          cudaStream_t stream) {
+                                          cudaStream_t stream, bool depth_source = false) {
     CUtensorMap gm, dm;
-    if (!encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
+    if (!depth_source &&
+        !encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
                           geom.grey_img_stride))
         return cudaErrorNotSupported;
     if (depth) {
@@ -312,7 +393,10 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     } else {
         dm = gm;
     }
-    auto kern = depth ? lbp_hist_lane59_kernel<true> : lbp_hist_lane59_kernel<false>;
+    if (depth_source) gm = dm;  // grey is not read
+    auto kern = depth_source ? lbp_hist_lane59_kernel<true, true>
+                : depth      ? lbp_hist_lane59_kernel<true, false>
+                             : lbp_hist_lane59_kernel<false, false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l59::kSmemBytes);
     if (e != cudaSuccess) return e;

@@ -87,6 +87,14 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
                                                       stream));
         }
     }
+    // depth source, headline geometry: the same TMA kernel with the codes on the depth tile
+    // (exact while dmax <= 0x7BFE, see lbp_hist_lane59.cuh)
+    if (depth_source && bins == 59 && win.span + win.lo <= 0x7BFEu && !win.none_valid &&
+        fast_path_applicable(geom, nullptr, depth, cells_x, cells_y, bins, desc) &&
+        ((desc_stride * 2) & 15) == 0)
+        return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win, desc,
+                                                    desc_stride, roi_status, num_sms(), stream,
+                                                    true));
     const int grid = (int)std::min<int64_t>(n_rois, (int64_t)num_sms() * 8);
     if (depth_source) {
         const CodePlane<uint16_t> plane{depth, geom.depth_pitch, geom.depth_img_stride};

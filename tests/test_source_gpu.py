@@ -115,3 +115,17 @@ def test_errors(lb):
         lb.lbp_extract_source(g, None, r, 0, 10, 2, 2, 59, lb.LBP_SRC_DEPTH)
     with pytest.raises(lb.LbpError):
         lb.lbp_extract_source(g, _dev_u16(depth), r, 0, 10, 2, 2, 59, 7)
+
+
+@pytest.mark.parametrize("dmax", [31742, 31743, 65535])
+def test_depth_source_128_full_range(lb, dmax):
+    """128x128 crops (the TMA depth-source kernel while dmax <= 0x7BFE, the generic kernel
+    above) with neighbours over the whole u16 range: the clamp to 0x7BFF must be exact."""
+    rng = np.random.default_rng(dmax)
+    vals = np.array([0, 1, 900, 901, 2047, 2048, 31741, 31742, 31743, 31744, 40000, 65535],
+                    np.uint16)
+    depth = vals[rng.integers(0, len(vals), (12, 128, 128))]
+    grey = rng.integers(0, 256, (12, 128, 128)).astype(np.uint8)
+    rois = synthgen.full_rois(12, 128, 128)
+    for source in (1, 2):
+        _check(lb, grey, depth, rois, 1, dmax, 8, 8, 59, source)
