@@ -14,7 +14,7 @@
 namespace lbpf {
 
 constexpr int kGenericThreads = 256;
-constexpr int kGenericHistCap = 12032;  // u32 counters per chunk (47 KB, static smem)
+constexpr int kGenericHistCap = 4096;  // u32 counters per chunk (16 KB static smem)
 
 // Eq. 2 with the Fig. 7 weights: TL 1, T 2, TR 4, R 8, BR 16, B 32, BL 64, L 128.
 // T = uint8_t (grey source) or uint16_t (depth source); pitch in elements.
@@ -45,25 +45,28 @@ struct CodePlane {
 // the bin.  `sync()` synchronises the group.  The descriptor row of ROI n starts at
 // desc + n * desc_stride (desc_stride >= dim; the fused grey||depth layout passes 2 * dim and
 // a desc already offset to its block).
+// Only the cells [cell_begin, cell_end) (row-major cell indices) are computed and written;
+// the whole grid by default.  The unit holding cell 0 writes roi_status.
 template <int BINS, int NT, typename T, typename Sync>
 __device__ __forceinline__ void extract_roi_generic(
     const CodePlane<T> plane, const uint16_t* __restrict__ depth, const lbp_images_t& geom,
     const lbp_roi_t roi, int32_t n, const DepthWindow& win, int32_t cells_x, int32_t cells_y,
     uint16_t* __restrict__ desc, int64_t desc_stride, int32_t* __restrict__ roi_status,
-    uint32_t* hist, int cap, const uint8_t* lut, int lut_shift, int t, Sync sync) {
-    const int64_t dim = (int64_t)cells_x * cells_y * BINS;
+    uint32_t* hist, int cap, const uint8_t* lut, int lut_shift, int t, Sync sync,
+    int32_t cell_begin = 0, int32_t cell_end = -1) {
+    if (cell_end < 0) cell_end = cells_x * cells_y;
     const int warp = t >> 5, lane = t & 31;
     constexpr int kWarps = NT / 32;
     const RoiGeom r = clamp_roi(roi, geom, cells_x, cells_y);
     uint16_t* out = desc + (int64_t)n * desc_stride;
-    if (t == 0 && roi_status) roi_status[n] = r.status;
+    if (t == 0 && roi_status && cell_begin == 0) roi_status[n] = r.status;
     if (r.status != LBP_OK) {
-        for (int64_t i = t; i < dim; i += NT) out[i] = 0;
+        for (int64_t i = (int64_t)cell_begin * BINS + t; i < (int64_t)cell_end * BINS; i += NT)
+            out[i] = 0;
         return;
     }
     const T* G = plane.base + (int64_t)r.img * plane.img_stride;
     const uint16_t* D = depth ? depth + (int64_t)r.img * geom.depth_img_stride : nullptr;
-    const int32_t n_cells = cells_x * cells_y;
     const int32_t cells_per_chunk = cap / BINS;
     // cell of interior column j: ((j+1)*Kx - 1) / W' -- in 32 bits when it cannot overflow
     // (every realistic geometry), 64 bits otherwise
@@ -73,8 +76,8 @@ __device__ __forceinline__ void extract_roi_generic(
                       : (int32_t)(((int64_t)(j + 1) * cells_x - 1) / r.wi);
     };
 
-    for (int32_t c0 = 0; c0 < n_cells; c0 += cells_per_chunk) {
-        const int32_t c1 = min(n_cells, c0 + cells_per_chunk);
+    for (int32_t c0 = cell_begin; c0 < cell_end; c0 += cells_per_chunk) {
+        const int32_t c1 = min(cell_end, c0 + cells_per_chunk);
         // interior rows covered by cell rows [c0/Kx, (c1-1)/Kx]
         const int32_t cy_a = c0 / cells_x, cy_b = (c1 - 1) / cells_x;
         const int32_t i_begin = (int32_t)(((int64_t)cy_a * r.hi) / cells_y);
@@ -121,6 +124,10 @@ struct CtaSync {
     __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
 
+// One CTA per (ROI, cell row) unit: the rows of one cell row of one ROI, all its cells.
+// Cell rows are disjoint in the descriptor, so units never share a counter and no global
+// atomics are needed; a handful of ROIs (the frame-stream and single-crop configs) still
+// spread over cells_y times as many SMs.
 template <int BINS, typename T>
 __global__ void __launch_bounds__(kGenericThreads)
 lbp_hist_generic_kernel(const CodePlane<T> plane, const uint16_t* __restrict__ depth,
@@ -132,15 +139,17 @@ lbp_hist_generic_kernel(const CodePlane<T> plane, const uint16_t* __restrict__ d
     __shared__ uint8_t lut[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
         lut[i] = (BINS == 59) ? kUniformLutDev.v[i] : (uint8_t)i;
-    // only the counters of one chunk are ever used: (cap / BINS) cells, or the whole grid
-    const int used = min(kGenericHistCap / BINS, cells_x * cells_y) * BINS;
+    // only the counters of one chunk are ever used: (cap / BINS) cells, or one cell row
+    const int used = min(kGenericHistCap / BINS, cells_x) * BINS;
     for (int i = threadIdx.x; i < used; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    for (int32_t n = blockIdx.x; n < n_rois; n += gridDim.x) {
+    const int64_t n_units = (int64_t)n_rois * cells_y;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int32_t n = (int32_t)(u / cells_y), cy = (int32_t)(u - (int64_t)n * cells_y);
         extract_roi_generic<BINS, kGenericThreads>(plane, depth, geom, rois[n], n, win, cells_x,
                                                    cells_y, desc, desc_stride, roi_status, hist,
                                                    kGenericHistCap, lut, 0, (int)threadIdx.x,
-                                                   CtaSync{});
+                                                   CtaSync{}, cy * cells_x, (cy + 1) * cells_x);
     }
 }
 

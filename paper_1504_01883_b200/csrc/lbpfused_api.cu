@@ -73,7 +73,10 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
                       const DepthWindow& win, int32_t cells_x, int32_t cells_y, int32_t bins,
                       uint16_t* desc, int64_t desc_stride, int32_t* roi_status,
                       cudaStream_t stream) {
-    if (!depth_source) {
+    // Small batches (the frame-stream and single-crop configs): the band kernel spreads every
+    // ROI over cells_y CTAs; the persistent TMA kernel would give each ROI one 8-warp group.
+    const bool small_batch = n_rois < num_sms();
+    if (!depth_source && !small_batch) {
         // Fast path (8x8 cells, 16-B aligned rows): one TMA-staged persistent kernel; ROIs
         // that are not fully-inside 128x128 boxes take the generic code path inside it.
         if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc) &&
@@ -89,13 +92,15 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
     }
     // depth source, headline geometry: the same TMA kernel with the codes on the depth tile
     // (exact while dmax <= 0x7BFE, see lbp_hist_lane59.cuh)
-    if (depth_source && bins == 59 && win.span + win.lo <= 0x7BFEu && !win.none_valid &&
+    if (depth_source && !small_batch && bins == 59 && win.span + win.lo <= 0x7BFEu &&
+        !win.none_valid &&
         fast_path_applicable(geom, nullptr, depth, cells_x, cells_y, bins, desc) &&
         ((desc_stride * 2) & 15) == 0)
         return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win, desc,
                                                     desc_stride, roi_status, num_sms(), stream,
                                                     true));
-    const int grid = (int)std::min<int64_t>(n_rois, (int64_t)num_sms() * 8);
+    // one CTA per (ROI, cell row) unit, grid-strided
+    const int grid = (int)std::min<int64_t>((int64_t)n_rois * cells_y, (int64_t)num_sms() * 8);
     if (depth_source) {
         const CodePlane<uint16_t> plane{depth, geom.depth_pitch, geom.depth_img_stride};
         if (bins == 59)
@@ -180,7 +185,7 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, 
     }
     // CUDA-core path: exact fp64 accumulation; 8 crops per CTA, 1 for tiny batches
     if (n < 8) {
-        svm_score_fp64_kernel<false, 1><<<n, kSvmThreads, 0, stream>>>(
+        svm_score_fp64_kernel<false, 1, 1024><<<n, 1024, 0, stream>>>(
             desc, n, dim, W, bias, n_classes, scores, labels, top_score, reject_threshold);
         return launch_status(cudaGetLastError());
     }

@@ -6,10 +6,12 @@
 // fp32 rounding -- the oracle's definition up to summation order (SURVEY §8c
 // step 8, "Score precision" reading).
 //
-// CTA = kSvmRows crops; its warps take classes round-robin; each lane strides
-// the descriptor dimension and keeps kSvmRows fp64 partial sums, reduced with
-// warp shuffles.  The descriptors of the CTA's crops are staged in shared
-// memory as fp32 (counts <= 65535 are exact in fp32).
+// CTA = kSvmRows crops; its warps take (class, dimension slice) items round-robin; each
+// lane strides the slice and keeps kSvmRows fp64 partial sums, reduced with warp shuffles;
+// with few classes every class is split into slices so that all warps have loads in flight
+// (a latency-bound kernel for the frame-stream / single-crop configs).  The descriptors of
+// the CTA's crops are staged in shared memory as fp32 (counts <= 65535 are exact in fp32).
+// Tiny batches use 1 crop and 1,024 threads per CTA.
 #pragma once
 #include "common.cuh"
 
@@ -23,17 +25,18 @@ __device__ __forceinline__ bool better(float s, int c, float best, int best_c) {
     return s > best || (s == best && c < best_c);
 }
 
-template <bool kStage, int kSvmRows>
-__global__ void __launch_bounds__(kSvmThreads)
+template <bool kStage, int kSvmRows, int NT = kSvmThreads>
+__global__ void __launch_bounds__(NT)
 svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
                       const float* __restrict__ W, const float* __restrict__ bias,
                       int32_t n_classes, float* __restrict__ scores, int32_t* __restrict__ labels,
                       float* __restrict__ top_score, float reject_threshold) {
     extern __shared__ float xs[];  // [kSvmRows][dim]
-    constexpr int kWarps = kSvmThreads / 32;
+    constexpr int kWarps = NT / 32;
+    constexpr int kItems = 2 * kWarps;  // (class, slice) items when classes are few
     __shared__ float wbest[kWarps][kSvmRows];
     __shared__ int wbest_c[kWarps][kSvmRows];
-    __shared__ double part[kWarps][kWarps][kSvmRows];  // [slice][class][row], few classes
+    __shared__ double part[kItems][kSvmRows];  // [slice * C + class][row], few classes
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * kSvmRows;
     const int rows = (int)((n - row0) < kSvmRows ? (n - row0) : kSvmRows);
@@ -51,9 +54,9 @@ svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
         return (double)__ldg(desc + (row0 + min(k, rows - 1)) * dim + d);
     };
 
-    // work items (class, slice of the dimension): with fewer classes than warps each class is
-    // split into S slices so that all warps work (latency-bound otherwise for small batches)
-    const int S = n_classes >= kWarps ? 1 : kWarps / n_classes;
+    // work items (class, slice of the dimension): with fewer classes than 2x the warps each
+    // class is split into S slices so that every warp has loads in flight
+    const int S = n_classes >= kWarps ? 1 : kItems / n_classes;
     const int items = n_classes * S;
     float best[kSvmRows];
     int best_c[kSvmRows];
@@ -89,7 +92,7 @@ svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
         if (S > 1) {  // partial sums, combined below in slice order
             if (lane == 0)
 #pragma unroll
-                for (int k = 0; k < kSvmRows; ++k) part[sl][c][k] = acc[k];
+                for (int k = 0; k < kSvmRows; ++k) part[sl * n_classes + c][k] = acc[k];
             continue;
         }
         const double b = (double)__ldg(bias + c);
@@ -111,7 +114,7 @@ svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
             int bc = 0;
             for (int c = 0; c < n_classes; ++c) {
                 double acc = 0.0;
-                for (int sl = 0; sl < S; ++sl) acc += part[sl][c][k];
+                for (int sl = 0; sl < S; ++sl) acc += part[sl * n_classes + c][k];
                 const float s = (float)(acc + (double)__ldg(bias + c));
                 if (scores) scores[(row0 + k) * n_classes + c] = s;
                 if (c == 0 || s > b) {

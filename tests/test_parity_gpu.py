@@ -47,8 +47,10 @@ def _check(lb, grey, depth, rois, dmin, dmax, kx, ky, bins):
 @pytest.mark.parametrize("bins", [59, 256])
 @pytest.mark.parametrize("dist", ["face", "constant", "noise"])
 def test_crops_128_bitexact(lb, bins, dist):
-    grey, depth = synthgen.face_crops(48, 128, 128, seed=21, dist=dist)
-    _check(lb, grey, depth, synthgen.full_rois(48, 128, 128), 600, 1400, 8, 8, bins)
+    # >= 148 ROIs: the persistent TMA kernels (smaller batches take the band kernel)
+    grey, depth = synthgen.face_crops(160, 128, 128, seed=21, dist=dist)
+    _check(lb, grey, depth, synthgen.full_rois(160, 128, 128), 600, 1400, 8, 8, bins)
+    _check(lb, grey[:20], depth[:20], synthgen.full_rois(20, 128, 128), 600, 1400, 8, 8, bins)
 
 
 def test_crop_64_config1(lb):
@@ -58,8 +60,9 @@ def test_crop_64_config1(lb):
 
 @pytest.mark.parametrize("bins", [59, 256])
 def test_no_depth_mask(lb, bins):
-    grey, _ = synthgen.face_crops(8, 128, 128, seed=2)
-    _check(lb, grey, None, synthgen.full_rois(8, 128, 128), 0, 0, 8, 8, bins)
+    grey, _ = synthgen.face_crops(150, 128, 128, seed=2)  # TMA kernels without depth
+    _check(lb, grey, None, synthgen.full_rois(150, 128, 128), 0, 0, 8, 8, bins)
+    _check(lb, grey[:8], None, synthgen.full_rois(8, 128, 128), 0, 0, 8, 8, bins)
 
 
 @pytest.mark.parametrize("H,W,kx,ky", [(37, 53, 5, 3), (20, 131, 7, 9), (9, 9, 7, 1),
@@ -129,7 +132,7 @@ def test_pitched_frames_config2(lb):
 def test_fast_kernel_mixed_rois(lb):
     """8x8 grid on aligned frames -> the TMA kernel; it must also take clamped, odd-sized,
     unaligned and invalid ROIs through its internal generic path."""
-    n_frames, H, W = 2, 480, 640
+    n_frames, H, W = 6, 480, 640  # 174 ROIs: the persistent TMA kernel
     grey, depth = synthgen.face_crops(n_frames, H, W, seed=16)
     rng = np.random.default_rng(7)
     rois = []

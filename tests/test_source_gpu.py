@@ -49,8 +49,11 @@ def _check(lb, grey, depth, rois, dmin, dmax, kx, ky, bins, source, grey_none=Fa
 @pytest.mark.parametrize("source", [1, 2])
 @pytest.mark.parametrize("bins", [59, 256])
 def test_crops_128(lb, source, bins):
-    grey, depth = synthgen.face_crops(40, 128, 128, seed=31)
-    _check(lb, grey, depth, synthgen.full_rois(40, 128, 128), 600, 1400, 8, 8, bins, source)
+    # >= 148 ROIs: the persistent TMA kernels (smaller batches take the band kernel)
+    grey, depth = synthgen.face_crops(160, 128, 128, seed=31)
+    _check(lb, grey, depth, synthgen.full_rois(160, 128, 128), 600, 1400, 8, 8, bins, source)
+    _check(lb, grey[:16], depth[:16], synthgen.full_rois(16, 128, 128), 600, 1400, 8, 8, bins,
+           source)
 
 
 def test_depth_source_without_grey(lb):
@@ -80,7 +83,7 @@ def test_full_u16_range_and_holes(lb):
 
 
 def test_pitched_frames_mixed_rois(lb):
-    n_frames, H, W = 2, 480, 640
+    n_frames, H, W = 9, 480, 640  # 153 ROIs: the persistent TMA kernels
     grey, depth = synthgen.face_crops(n_frames, H, W, seed=33)
     rng = np.random.default_rng(8)
     rois = []
@@ -124,8 +127,8 @@ def test_depth_source_128_full_range(lb, dmax):
     rng = np.random.default_rng(dmax)
     vals = np.array([0, 1, 900, 901, 2047, 2048, 31741, 31742, 31743, 31744, 40000, 65535],
                     np.uint16)
-    depth = vals[rng.integers(0, len(vals), (12, 128, 128))]
-    grey = rng.integers(0, 256, (12, 128, 128)).astype(np.uint8)
-    rois = synthgen.full_rois(12, 128, 128)
+    depth = vals[rng.integers(0, len(vals), (150, 128, 128))]
+    grey = rng.integers(0, 256, (150, 128, 128)).astype(np.uint8)
+    rois = synthgen.full_rois(150, 128, 128)
     for source in (1, 2):
         _check(lb, grey, depth, rois, 1, dmax, 8, 8, 59, source)
