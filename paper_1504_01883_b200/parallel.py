@@ -61,6 +61,92 @@ def gather_database(local_desc: torch.Tensor, local_labels: torch.Tensor, n_tota
     return recv.index_select(0, keep).view(torch.uint16), recv_lab.index_select(0, keep)
 
 
+def gather_database_chunked(extract_chunk, local_labels: torch.Tensor, n_total: int, dim: int,
+                            chunks: int, group=None, device=None,
+                            comm_stream: torch.cuda.Stream | None = None
+                            ) -> tuple[torch.Tensor, torch.Tensor]:
+    """Overlapped database build (way 1): the local shard is produced in `chunks`
+    row chunks; chunk k's all-gather runs on `comm_stream` while chunk k+1 is being extracted
+    on the current stream.  The result equals gather_database's (global crop order).
+
+    extract_chunk(lo, hi) -> u16 [hi - lo][dim]: descriptors of local rows [lo, hi), enqueued
+    on the current stream (on CPU / gloo it simply returns them).  Every rank uses the same
+    chunk row count (ceil of the largest shard / chunks), padding short chunks for the
+    collective; the padding is dropped when the chunk is copied into place."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    first, count = shard_range(n_total, rank, world)
+    if local_labels.shape[0] != count:
+        raise ValueError(f"rank {rank}: {local_labels.shape[0]} labels, expected {count}")
+    if world == 1:  # nothing to exchange: the shard is the database
+        return extract_chunk(0, count), local_labels
+    chunks = max(1, int(chunks))
+    cap = -(-n_total // world)
+    rpc = max(1, -(-cap // chunks))  # rows per chunk, identical on every rank
+    dev = device if device is not None else local_labels.device
+    cuda = dev.type == "cuda"
+    spans = [shard_range(n_total, r, world) for r in range(world)]
+    out = torch.empty((n_total, 2 * dim), dtype=torch.uint8, device=dev)
+    if cuda and comm_stream is None:
+        comm_stream = torch.cuda.Stream(dev)
+    pending = []
+    for k in range(chunks):
+        lo, hi = min(k * rpc, count), min((k + 1) * rpc, count)
+        part = extract_chunk(lo, hi) if hi > lo else None
+        if part is not None and hi - lo == rpc and part.is_contiguous():
+            send = part.view(torch.uint8)  # full chunk: sent in place
+        else:  # short or empty chunk: padded copy
+            send = torch.zeros((rpc, 2 * dim), dtype=torch.uint8, device=dev)
+            if part is not None:
+                send[:hi - lo] = part.contiguous().view(torch.uint8)
+        recv = torch.empty((world * rpc, 2 * dim), dtype=torch.uint8, device=dev)
+        if cuda:
+            ready = torch.cuda.Event()
+            ready.record()
+            comm_stream.wait_event(ready)
+            with torch.cuda.stream(comm_stream):
+                send.record_stream(comm_stream)
+                recv.record_stream(comm_stream)
+                work = dist.all_gather_into_tensor(recv, send, group=group, async_op=True)
+        else:
+            work = dist.all_gather_into_tensor(recv, send, group=group, async_op=True)
+        pending.append((k, recv, work))
+        # place the chunks whose collectives were issued earlier (keeps at most 2 in flight)
+        while len(pending) > 1:
+            _place(pending.pop(0), out, spans, rpc, comm_stream if cuda else None)
+    while pending:
+        _place(pending.pop(0), out, spans, rpc, comm_stream if cuda else None)
+    if cuda:
+        torch.cuda.current_stream(dev).wait_stream(comm_stream)
+    # labels: one small all-gather (4 B per crop)
+    lab_send = torch.full((cap,), -1, dtype=torch.int32, device=dev)
+    lab_send[:count] = local_labels
+    lab_recv = torch.empty((world * cap,), dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(lab_recv, lab_send, group=group)
+    labels = torch.cat([lab_recv[r * cap:r * cap + spans[r][1]] for r in range(world)])
+    return out.view(torch.uint16), labels
+
+
+def _place(item, out, spans, rpc, stream):
+    """Copy chunk k of every rank from the gathered buffer to its global rows."""
+    k, recv, work = item
+    ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
+    with ctx:
+        work.wait()
+        for r, (first, count) in enumerate(spans):
+            lo, hi = min(k * rpc, count), min((k + 1) * rpc, count)
+            if hi > lo:
+                out[first + lo:first + hi] = recv[r * rpc:r * rpc + (hi - lo)]
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def build_database(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.Tensor,
                    labels: torch.Tensor, n_total: int, dmin: int, dmax: int, cells_x: int,
                    cells_y: int, bins: int, group=None, stream=None):

@@ -11,7 +11,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synthgen
-from paper_1504_01883_b200.parallel import gather_database, shard_range
+from paper_1504_01883_b200.parallel import gather_database, gather_database_chunked, shard_range
 
 
 def test_shard_range_covers_exactly():
@@ -74,3 +74,37 @@ def test_gather_database_gloo(tmp_path, world, n_total):
         lab = np.load(tmp_path / f"lab{r}.npy")
         assert np.array_equal(got, ref)
         assert np.array_equal(lab, np.arange(n_total) % 7)
+
+
+def _worker_chunked(rank, world, port, n_total, chunks, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        first, count = shard_range(n_total, rank, world)
+        grey, depth = synthgen.face_crops(count, 32, 32, seed=9, first_index=first)
+
+        def extract_chunk(lo, hi):  # stand-in extractor on CPU: the oracle
+            d = oracle.lbp_extract(grey[lo:hi], depth[lo:hi], synthgen.full_rois(hi - lo, 32, 32),
+                                   600, 1400, 4, 4, 59)
+            return torch.from_numpy(d.view(np.int16)).view(torch.uint16)
+        labels = torch.from_numpy((np.arange(first, first + count) % 5).astype(np.int32))
+        full, lab = gather_database_chunked(extract_chunk, labels, n_total, 4 * 4 * 59, chunks,
+                                            device=torch.device("cpu"))
+        np.save(os.path.join(out_dir, f"desc{rank}.npy"), full.view(torch.int16).numpy())
+        np.save(os.path.join(out_dir, f"lab{rank}.npy"), lab.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_total,chunks", [(2, 10, 3), (3, 11, 4), (2, 7, 1), (3, 5, 6)])
+def test_gather_database_chunked_gloo(tmp_path, world, n_total, chunks):
+    """Overlapped (chunked) database build == the serial one == the oracle, uneven shards and
+    more chunks than rows included."""
+    mp.spawn(_worker_chunked, args=(world, _free_port(), n_total, chunks, str(tmp_path)),
+             nprocs=world, join=True)
+    grey, depth = synthgen.face_crops(n_total, 32, 32, seed=9)
+    ref = oracle.lbp_extract(grey, depth, synthgen.full_rois(n_total, 32, 32), 600, 1400, 4, 4, 59)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"desc{r}.npy").view(np.uint16), ref)
+        assert np.array_equal(np.load(tmp_path / f"lab{r}.npy"), np.arange(n_total) % 5)
