@@ -55,6 +55,13 @@ def lib():
         L.oracle_lbp_extract_src.argtypes = [P, P, i32, i32, i32, i64, i64, i64, i64, P, i32,
                                              u16, u16, i32, i32, i32, i32, P, P]
         L.oracle_lbp_extract_src.restype = i32
+        L.oracle_resize_grey.argtypes = [P, i32, i32, i64, i32, i32, P]
+        L.oracle_resize_grey.restype = i32
+        L.oracle_resize_depth.argtypes = [P, i32, i32, i64, i32, i32, P]
+        L.oracle_resize_depth.restype = i32
+        L.oracle_lbp_extract_resized.argtypes = [P, P, i32, i32, i32, i64, i64, i64, i64, P, i32,
+                                                 i32, u16, u16, i32, i32, i32, i32, P, P]
+        L.oracle_lbp_extract_resized.restype = i32
         L.oracle_svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, f32]
         L.oracle_svm_score.restype = i32
         _lib = L
@@ -119,6 +126,53 @@ def lbp_extract(grey, depth, rois, dmin: int, dmax: int,
                                       _ptr(desc), _ptr(status))
     if st != ORC_OK:
         raise ValueError(f"oracle_lbp_extract_src status {st}")
+    return (desc, status) if return_status else desc
+
+
+def resize_grey(img: np.ndarray, out_h: int, out_w: int) -> np.ndarray:
+    """Bilinear, half-pixel centres, round half up, exact integer arithmetic."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    h, w = img.shape
+    out = np.zeros((out_h, out_w), np.uint8)
+    st = lib().oracle_resize_grey(_ptr(img), h, w, w, out_h, out_w, _ptr(out))
+    if st != ORC_OK:
+        raise ValueError(f"oracle_resize_grey status {st}")
+    return out
+
+
+def resize_depth(img: np.ndarray, out_h: int, out_w: int) -> np.ndarray:
+    """Nearest neighbour, half-pixel centres, ties toward the smaller index."""
+    img = np.ascontiguousarray(img, dtype=np.uint16)
+    h, w = img.shape
+    out = np.zeros((out_h, out_w), np.uint16)
+    st = lib().oracle_resize_depth(_ptr(img), h, w, w, out_h, out_w, _ptr(out))
+    if st != ORC_OK:
+        raise ValueError(f"oracle_resize_depth status {st}")
+    return out
+
+
+def lbp_extract_resized(grey, depth, rois, size: int, dmin: int, dmax: int, cells_x: int,
+                        cells_y: int, bins: int, *, source: int = SRC_GREY,
+                        return_status: bool = False):
+    """Descriptors of ROIs cropped (clamped) and resized to size x size."""
+    if grey is not None:
+        grey = np.ascontiguousarray(grey, dtype=np.uint8)
+        grey = grey[None] if grey.ndim == 2 else grey
+    if depth is not None:
+        depth = np.ascontiguousarray(depth, dtype=np.uint16)
+        depth = depth[None] if depth.ndim == 2 else depth
+    ref = grey if grey is not None else depth
+    n_img, H, W = ref.shape
+    rois = np.ascontiguousarray(np.asarray(rois, dtype=np.int32).reshape(-1, 5))
+    n = rois.shape[0]
+    dim = cells_x * cells_y * bins * (2 if source == SRC_FUSED else 1)
+    desc = np.zeros((n, dim), dtype=np.uint16)
+    status = np.zeros(n, dtype=np.int32)
+    st = lib().oracle_lbp_extract_resized(_ptr(grey), _ptr(depth), n_img, H, W, W, W, H * W,
+                                          H * W, _ptr(rois), n, size, dmin, dmax, cells_x,
+                                          cells_y, bins, source, _ptr(desc), _ptr(status))
+    if st != ORC_OK:
+        raise ValueError(f"oracle_lbp_extract_resized status {st}")
     return (desc, status) if return_status else desc
 
 

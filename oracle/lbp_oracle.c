@@ -18,6 +18,7 @@
  * header comment of each function for the pins that cover it.
  */
 #include <stdint.h>
+#include <stdlib.h>
 #include <stddef.h>
 #include <string.h>
 #include <math.h>
@@ -258,6 +259,143 @@ int32_t oracle_lbp_extract(const uint8_t* grey, const uint16_t* depth,
     return oracle_lbp_extract_src(grey, depth, n_images, height, width, grey_pitch, depth_pitch,
                                   grey_img_stride, depth_img_stride, rois, n_rois, dmin, dmax,
                                   cells_x, cells_y, bins, ORC_SRC_GREY, desc, roi_status);
+}
+
+/* ------------------------------------------------------------------------ */
+/* ROI resize ("The detected face ... is resized to 200x200 pixels";  */
+/* SURVEY §8f-2; S:91-99 resize):                                           */
+/*  grey : bilinear with half-pixel centres, rounded half up.  Output pixel */
+/*         (ox, oy) of an out_w x out_h image samples the source at         */
+/*         sx = (ox + 1/2) * w / out_w - 1/2 (likewise sy), clamped below   */
+/*         at 0; x0 = floor(sx), x1 = min(x0 + 1, w - 1), fx = sx - x0;     */
+/*         v = (1-fx)(1-fy) p00 + fx(1-fy) p10 + (1-fx) fy p01 + fx fy p11, */
+/*         result floor(v + 1/2).  Written in exact integers: with D = 2    */
+/*         out_w, sx = N / D for N = (2 ox + 1) w - out_w, so fx = (N mod   */
+/*         D) / D and every weight is an integer over Dx * Dy.              */
+/*  depth: nearest neighbour with half-pixel centres, ties toward the       */
+/*         smaller index: x = ceil((sx + 1/2)) - 1 = floor(((2 ox + 1) w -  */
+/*         1) / (2 out_w)), clamped to [0, w - 1] -- no 0 (hole) is ever    */
+/*         blended into a fabricated depth.                                 */
+/* src: h x w samples, row pitch `pitch` (elements); dst: out_h x out_w.    */
+/* ------------------------------------------------------------------------ */
+static int64_t floor_div(int64_t a, int64_t b) { /* b > 0 */
+    int64_t q = a / b;
+    return (a % b != 0 && a < 0) ? q - 1 : q;
+}
+
+int32_t oracle_resize_grey(const uint8_t* src, int32_t h, int32_t w, int64_t pitch,
+                           int32_t out_h, int32_t out_w, uint8_t* dst)
+{
+    if (!src || !dst || h < 1 || w < 1 || out_h < 1 || out_w < 1 || pitch < w) return ORC_E_ARG;
+    int64_t Dx = 2 * (int64_t)out_w, Dy = 2 * (int64_t)out_h;
+    for (int32_t oy = 0; oy < out_h; ++oy) {
+        int64_t Ny = (2 * (int64_t)oy + 1) * h - out_h;
+        if (Ny < 0) Ny = 0;                         /* clamp sy at 0 */
+        int64_t y0 = floor_div(Ny, Dy), ry = Ny - y0 * Dy;
+        if (y0 > h - 1) { y0 = h - 1; ry = 0; }     /* (cannot happen: sy < h - 1/2) */
+        int64_t y1 = y0 + 1 < h ? y0 + 1 : h - 1;
+        for (int32_t ox = 0; ox < out_w; ++ox) {
+            int64_t Nx = (2 * (int64_t)ox + 1) * w - out_w;
+            if (Nx < 0) Nx = 0;
+            int64_t x0 = floor_div(Nx, Dx), rx = Nx - x0 * Dx;
+            if (x0 > w - 1) { x0 = w - 1; rx = 0; }
+            int64_t x1 = x0 + 1 < w ? x0 + 1 : w - 1;
+            int64_t p00 = src[y0 * pitch + x0], p10 = src[y0 * pitch + x1];
+            int64_t p01 = src[y1 * pitch + x0], p11 = src[y1 * pitch + x1];
+            int64_t num = (Dx - rx) * (Dy - ry) * p00 + rx * (Dy - ry) * p10 +
+                          (Dx - rx) * ry * p01 + rx * ry * p11;
+            int64_t den = Dx * Dy;
+            dst[(int64_t)oy * out_w + ox] = (uint8_t)floor_div(2 * num + den, 2 * den);
+        }
+    }
+    return ORC_OK;
+}
+
+int32_t oracle_resize_depth(const uint16_t* src, int32_t h, int32_t w, int64_t pitch,
+                            int32_t out_h, int32_t out_w, uint16_t* dst)
+{
+    if (!src || !dst || h < 1 || w < 1 || out_h < 1 || out_w < 1 || pitch < w) return ORC_E_ARG;
+    for (int32_t oy = 0; oy < out_h; ++oy) {
+        int64_t y = floor_div((2 * (int64_t)oy + 1) * h - 1, 2 * (int64_t)out_h);
+        if (y < 0) y = 0;
+        if (y > h - 1) y = h - 1;
+        for (int32_t ox = 0; ox < out_w; ++ox) {
+            int64_t x = floor_div((2 * (int64_t)ox + 1) * w - 1, 2 * (int64_t)out_w);
+            if (x < 0) x = 0;
+            if (x > w - 1) x = w - 1;
+            dst[(int64_t)oy * out_w + ox] = src[y * pitch + x];
+        }
+    }
+    return ORC_OK;
+}
+
+/* Resized-ROI descriptor: per ROI n, crop = clamp(roi, image) (empty  */
+/* -> ORC_E_ROI), resize the crop to size x size (grey bilinear, depth nearest, above), then */
+/* steps 2-7 of oracle_lbp_extract_src on the size x size image with a full ROI.  grey may  */
+/* be NULL for the depth source; depth may be NULL (no mask) for the grey source.           */
+int32_t oracle_lbp_extract_resized(const uint8_t* grey, const uint16_t* depth,
+                                   int32_t n_images, int32_t height, int32_t width,
+                                   int64_t grey_pitch, int64_t depth_pitch,
+                                   int64_t grey_img_stride, int64_t depth_img_stride,
+                                   const int32_t* rois, int32_t n_rois, int32_t size,
+                                   uint16_t dmin, uint16_t dmax, int32_t cells_x,
+                                   int32_t cells_y, int32_t bins, int32_t source,
+                                   uint16_t* desc, int32_t* roi_status)
+{
+    if (n_rois < 0 || size < 3) return ORC_E_ARG;
+    if (source != ORC_SRC_GREY && source != ORC_SRC_DEPTH && source != ORC_SRC_FUSED)
+        return ORC_E_ARG;
+    if (n_rois == 0) return ORC_OK;
+    if (!rois || !desc) return ORC_E_ARG;
+    if (source != ORC_SRC_DEPTH && !grey) return ORC_E_ARG;
+    if (source != ORC_SRC_GREY && !depth) return ORC_E_ARG;
+    if (bins != 59 && bins != 256) return ORC_E_ARG;
+    if (cells_x < 1 || cells_y < 1 || dmin > dmax) return ORC_E_ARG;
+    if (n_images < 1 || height < 1 || width < 1) return ORC_E_ARG;
+    if (grey && (grey_pitch < width || grey_img_stride < grey_pitch * (height - 1) + width))
+        return ORC_E_ARG;
+    if (depth && (depth_pitch < width || depth_img_stride < depth_pitch * (height - 1) + width))
+        return ORC_E_ARG;
+    int64_t dim = (int64_t)cells_x * cells_y * bins;
+    int64_t row = (source == ORC_SRC_FUSED) ? 2 * dim : dim;
+    if (row > 0x7FFFFFFF) return ORC_E_ARG;
+
+    int64_t px = (int64_t)size * size;
+    uint8_t* g = (uint8_t*)malloc((size_t)px);
+    uint16_t* d = (uint16_t*)malloc((size_t)px * 2);
+    if (!g || !d) { free(g); free(d); return ORC_E_ARG; }
+    int32_t full[5] = {0, 0, 0, size, size};
+    int32_t rc = ORC_OK;
+    for (int32_t n = 0; n < n_rois && rc == ORC_OK; ++n) {
+        uint16_t* h = desc + (int64_t)n * row;
+        const int32_t* roi = rois + (int64_t)n * 5;
+        int64_t img = roi[0];
+        int64_t x0 = roi[1], y0 = roi[2], x1 = x0 + roi[3], y1 = y0 + roi[4];
+        if (x0 < 0) x0 = 0;
+        if (y0 < 0) y0 = 0;
+        if (x1 > width) x1 = width;
+        if (y1 > height) y1 = height;
+        if (img < 0 || img >= n_images || x1 <= x0 || y1 <= y0) {
+            for (int64_t k = 0; k < row; ++k) h[k] = 0;
+            if (roi_status) roi_status[n] = ORC_E_ROI;
+            continue;
+        }
+        int32_t cw = (int32_t)(x1 - x0), ch = (int32_t)(y1 - y0);
+        if (grey)
+            oracle_resize_grey(grey + img * grey_img_stride + y0 * grey_pitch + x0, ch, cw,
+                               grey_pitch, size, size, g);
+        if (depth)
+            oracle_resize_depth(depth + img * depth_img_stride + y0 * depth_pitch + x0, ch, cw,
+                                depth_pitch, size, size, d);
+        int32_t st = ORC_OK;
+        rc = oracle_lbp_extract_src(grey ? g : NULL, depth ? d : NULL, 1, size, size, size, size,
+                                    px, px, full, 1, dmin, dmax, cells_x, cells_y, bins, source,
+                                    h, &st);
+        if (roi_status) roi_status[n] = st;
+    }
+    free(g);
+    free(d);
+    return rc;
 }
 
 /* ------------------------------------------------------------------------ */
