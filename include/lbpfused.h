@@ -112,6 +112,25 @@ int32_t lbp_extract_source(const uint8_t* grey, const uint16_t* depth, lbp_image
                            uint16_t* desc, int32_t* roi_status, lbp_stream_t stream);
 
 /*
+ * lbp_extract_resized -- descriptors of ROIs resized to size x size (P:154
+ * "The detected face ... is resized to 200x200 pixels"; R19):
+ *   crop = clamp(roi, image) (empty / bad image -> LBP_E_ROI and a zero row), then
+ *   grey: bilinear with half-pixel centres, rounded half up (exact integer arithmetic);
+ *   depth: nearest neighbour with half-pixel centres, ties toward the smaller index (holes
+ *   are never blended); then every step of lbp_extract_source on the size x size image
+ *   with a full ROI (border, mask, codes of `source`, floor cells, bins, statuses).  The
+ *   resized crops live only in shared memory (the resize is fused into the staging).
+ *   size       output side, 3..1024 (LBP_E_ARG otherwise)
+ *   desc       out: u16 [n_rois][dim] (or [n_rois][2*dim] for LBP_SRC_FUSED)
+ * Image width and height must be <= 2^20 (LBP_E_UNSUPPORTED otherwise).
+ */
+int32_t lbp_extract_resized(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                            const lbp_roi_t* rois, int32_t n_rois, int32_t size, uint16_t dmin,
+                            uint16_t dmax, int32_t cells_x, int32_t cells_y, int32_t bins,
+                            int32_t source, uint16_t* desc, int32_t* roi_status,
+                            lbp_stream_t stream);
+
+/*
  * svm_score -- SURVEY §8a step a7: linear one-vs-rest SVM decision ("a classifier
  * defined by a hyperplane"; A-vs-B training per identity):
  *   s[n][c] = fp32( b[c] + sum_d W[c][d] * desc[n][d] ), accumulated EXACTLY (each

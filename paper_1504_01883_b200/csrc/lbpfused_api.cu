@@ -7,6 +7,7 @@
 #include "lbp_hist_generic.cuh"
 #include "lbp_hist_fast.cuh"
 #include "lbp_hist_lane59.cuh"
+#include "lbp_resize.cuh"
 #include "svm_fp64.cuh"
 #include "svm_gemm.cuh"
 
@@ -157,6 +158,45 @@ int32_t lbp_extract_source(const uint8_t* grey, const uint16_t* depth, lbp_image
         st = extract_block(grey, depth, true, geom, rois, n_rois, win, cells_x, cells_y, bins,
                            desc + (source == LBP_SRC_FUSED ? dim : 0), stride, roi_status, stream);
     return st;
+}
+
+int32_t lbp_extract_resized(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                            const lbp_roi_t* rois, int32_t n_rois, int32_t size, uint16_t dmin,
+                            uint16_t dmax, int32_t cells_x, int32_t cells_y, int32_t bins,
+                            int32_t source, uint16_t* desc, int32_t* roi_status,
+                            lbp_stream_t stream_) {
+    if (n_rois < 0 || size < 3 || size > kResizeMaxSize) return LBP_E_ARG;
+    if (source != LBP_SRC_GREY && source != LBP_SRC_DEPTH && source != LBP_SRC_FUSED)
+        return LBP_E_ARG;
+    const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
+    if (dim < 0) return dim;
+    if (source == LBP_SRC_FUSED && dim > 0x3FFFFFFF) return LBP_E_ARG;
+    if (dmin > dmax) return LBP_E_ARG;
+    if (n_rois == 0) return LBP_OK;
+    const bool need_grey = source != LBP_SRC_DEPTH, need_depth = source != LBP_SRC_GREY;
+    if (!rois || !desc || (need_grey && !grey) || (need_depth && !depth)) return LBP_E_ARG;
+    int32_t st = check_geometry(geom, need_grey, depth != nullptr);
+    if (st != LBP_OK) return st;
+    if (geom.width > (1 << 20) || geom.height > (1 << 20)) return LBP_E_UNSUPPORTED;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const DepthWindow win = make_window(dmin, dmax);
+    const int64_t stride = source == LBP_SRC_FUSED ? 2 * (int64_t)dim : dim;
+    const int grid = (int)std::min<int64_t>((int64_t)n_rois * cells_y, (int64_t)num_sms() * 8);
+    const uint8_t* g = need_grey ? grey : nullptr;
+#define LBPF_RESIZE_LAUNCH(B, SRCV)                                                          \
+    lbp_hist_resize_kernel<B, SRCV><<<grid, kResizeThreads, 0, stream>>>(                  \
+        g, depth, geom, rois, n_rois, size, win, cells_x, cells_y, desc, stride, roi_status)
+    if (bins == 59) {
+        if (source == LBP_SRC_GREY) LBPF_RESIZE_LAUNCH(59, 0);
+        else if (source == LBP_SRC_DEPTH) LBPF_RESIZE_LAUNCH(59, 1);
+        else LBPF_RESIZE_LAUNCH(59, 2);
+    } else {
+        if (source == LBP_SRC_GREY) LBPF_RESIZE_LAUNCH(256, 0);
+        else if (source == LBP_SRC_DEPTH) LBPF_RESIZE_LAUNCH(256, 1);
+        else LBPF_RESIZE_LAUNCH(256, 2);
+    }
+#undef LBPF_RESIZE_LAUNCH
+    return launch_status(cudaGetLastError());
 }
 
 int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,

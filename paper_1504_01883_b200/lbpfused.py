@@ -55,6 +55,9 @@ def lib():
         L.lbp_extract_source.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, i32,
                                          P, P, P]
         L.lbp_extract_source.restype = i32
+        L.lbp_extract_resized.argtypes = [P, P, lbp_images_t, P, i32, i32, u16, u16, i32, i32,
+                                          i32, i32, P, P, P]
+        L.lbp_extract_resized.restype = i32
         L.svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, P, f32, P]
         L.svm_score.restype = i32
         L.svm_workspace_bytes.argtypes = [i32, i32]
@@ -170,6 +173,36 @@ def lbp_extract_source(grey: torch.Tensor | None, depth: torch.Tensor | None,
                                   _ptr(out), _ptr(roi_status), _stream(stream))
     if st != LBP_OK:
         raise LbpError(st, "lbp_extract_source")
+    return out
+
+
+def lbp_extract_resized(grey: torch.Tensor | None, depth: torch.Tensor | None,
+                        rois: torch.Tensor, size: int, dmin: int, dmax: int, cells_x: int,
+                        cells_y: int, bins: int, source: int = LBP_SRC_GREY,
+                        out: torch.Tensor | None = None,
+                        roi_status: torch.Tensor | None = None,
+                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Descriptors of the ROIs cropped (clamped) and resized to size x size on the GPU
+    (grey bilinear, depth nearest)."""
+    _check_cuda(grey, depth, rois, out, roi_status)
+    assert grey is None or grey.dtype == torch.uint8
+    assert depth is None or depth.dtype == torch.uint16
+    assert rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5
+    if grey is None and depth is None:
+        raise LbpError(LBP_E_ARG, "lbp_extract_resized: no image plane")
+    n = rois.shape[0]
+    dim = lbp_descriptor_dim(cells_x, cells_y, bins) * (2 if source == LBP_SRC_FUSED else 1)
+    dev = (grey if grey is not None else depth).device
+    if out is None:
+        out = torch.empty((n, dim), dtype=torch.uint16, device=dev)
+    assert out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim
+    if roi_status is not None:
+        assert roi_status.dtype == torch.int32 and roi_status.numel() >= n
+    st = lib().lbp_extract_resized(_ptr(grey), _ptr(depth), images_geometry(grey, depth),
+                                   _ptr(rois), n, size, dmin, dmax, cells_x, cells_y, bins,
+                                   source, _ptr(out), _ptr(roi_status), _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_extract_resized")
     return out
 
 

@@ -101,6 +101,25 @@ def test_extract_source_argument_errors(L):
     assert call(lb.LBP_SRC_DEPTH, grey=None, geom=bad) == lb.LBP_E_ARG
 
 
+def test_extract_resized_argument_errors(L):
+    from paper_1504_01883_b200 import lbpfused as lb
+    P = ctypes.c_void_p
+    dummy = P(0x1000)
+    g = _geom(lb)
+
+    def call(size=64, source=0, grey=dummy, depth=dummy, n=1, geom=g):
+        return L.lbp_extract_resized(grey, depth, geom, dummy, n, size, 0, 10, 2, 2, 59, source,
+                                     dummy, None, None)
+    assert call(size=2) == lb.LBP_E_ARG
+    assert call(size=1025) == lb.LBP_E_ARG
+    assert call(source=5) == lb.LBP_E_ARG
+    assert call(source=lb.LBP_SRC_DEPTH, depth=None) == lb.LBP_E_ARG
+    assert call(grey=None) == lb.LBP_E_ARG
+    assert call(n=0) == lb.LBP_OK
+    big = lb.lbp_images_t(1, 8, (1 << 20) + 1, 0, (1 << 20) + 1, (1 << 20) + 1, 8 << 21, 8 << 21)
+    assert call(geom=big) == lb.LBP_E_UNSUPPORTED
+
+
 def test_svm_argument_errors(L):
     from paper_1504_01883_b200 import lbpfused as lb
     P = ctypes.c_void_p
