@@ -83,6 +83,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 10)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     p.add_argument("--skip-cpu", action="store_true")
+    p.add_argument("--resize", type=int, default=0,
+                   help="configs 1/2: resize every ROI to S x S on the GPU before the "
+                        "descriptor (the paper's 200x200, P:154; lbp_extract_resized)")
     p.add_argument("--chunks", type=int, default=4,
                    help="config5: extraction/all-gather overlap chunks (1 = serial)")
     return p.parse_args()
@@ -440,7 +443,11 @@ def run_latency(args):
     def call(f):
         r = rois[f * n_per:(f + 1) * n_per]
         o = desc[f * n_per:(f + 1) * n_per]
-        lb.lbp_fused_extract(grey, depth, r, DMIN, DMAX, cx, cy, bins, out=o, stream=stream)
+        if args.resize:
+            lb.lbp_extract_resized(grey, depth, r, args.resize, DMIN, DMAX, cx, cy, bins,
+                                   out=o, stream=stream)
+        else:
+            lb.lbp_fused_extract(grey, depth, r, DMIN, DMAX, cx, cy, bins, out=o, stream=stream)
         lb.svm_score(o, W, b, prepared=prepared, want_scores=False,
                      labels=labels[f * n_per:(f + 1) * n_per],
                      top_score=top[f * n_per:(f + 1) * n_per], stream=stream)
@@ -481,7 +488,8 @@ def run_latency(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
         "config": {"workload": f"{args.workload}: {desc_txt}", "crops_per_call": n_per,
-                   "calls": n_calls, "classes": C, "l2": "inputs L2-resident (latency config)"},
+                   "calls": n_calls, "classes": C, "l2": "inputs L2-resident (latency config)",
+                   "resize": args.resize or None},
         "latency_us": {"eager_p50": float(np.percentile(lat, 50) * 1e3),
                        "eager_p99": float(np.percentile(lat, 99) * 1e3),
                        "graph_per_call": per_call_graph * 1e3},
@@ -502,7 +510,10 @@ def latency_cpu_leg(args, g, d, rois_np, n_per, W_np, b_np, cx, cy, bins):
     t0 = time.perf_counter()
     for f in range(calls):
         r = rois_np[f * n_per:(f + 1) * n_per]
-        dd = oracle.lbp_extract(g, d, r, DMIN, DMAX, cx, cy, bins)
+        if args.resize:
+            dd = oracle.lbp_extract_resized(g, d, r, args.resize, DMIN, DMAX, cx, cy, bins)
+        else:
+            dd = oracle.lbp_extract(g, d, r, DMIN, DMAX, cx, cy, bins)
         oracle.svm_score(dd, W_np, b_np)
     ms = (time.perf_counter() - t0) / calls * 1e3
     return {"value": n_per / (ms * 1e-3), "unit": UNIT, "cores": 1, "kind": "oracle",
