@@ -214,7 +214,7 @@ def run_reference(args):
     n_gpu_crops, H, Wd, cx, cy, bins, C, desc_txt = WORKLOADS[args.workload]
     bins = args.bins or bins
     threads = len(os.sched_getaffinity(0))
-    per_step = max(threads, 4 * threads)
+    per_step = 256 * threads  # ~0.1 s of oracle work per step: thread start-up stays negligible
     total = per_step * (args.steps + args.warmup)
     grey, depth = synthgen.face_crops(per_step, H, Wd, seed=args.seed, dist=args.dist)
     if args.no_depth:
