@@ -35,15 +35,17 @@ constexpr int kGroupThreads = 256;
 constexpr int kThreads = kGroups * kGroupThreads;
 constexpr int kTile = 128;
 constexpr int kBins = 59;
+constexpr int kBinsAlloc = 60;  // + a dummy bin row that counts the masked-out pixels
 constexpr int kStages = 3;
 constexpr int kGreyBytes = kTile * kTile;                      // 16,384
 constexpr int kStageBytes = kGreyBytes + 2 * kTile * kTile;    // + depth 32,768 = 49,152
-constexpr int kHistBytes = 2 * kBins * 32 * 4;                 // [g][bin][lane] = 15,104
+constexpr int kHistBytes = 2 * kBinsAlloc * 32 * 4;            // [g][bin][lane] = 15,360
 constexpr int kDescBytes = 64 * kBins * 2;                     // 7,552
 constexpr int kGroupOff = kStages * kStageBytes;               // 147,456
-constexpr int kGroupBytes = (kHistBytes + kDescBytes + 255) / 256 * 256;  // 22,784
-constexpr int kLutOff = kGroupOff + kGroups * kGroupBytes;     // 215,808 (256-aligned)
-constexpr int kLutBytes = 64 * 128;
+constexpr int kGroupBytes = (kHistBytes + kDescBytes + 255) / 256 * 256;  // 23,040
+constexpr int kLutOff = kGroupOff + kGroups * kGroupBytes;     // 216,576 (256-aligned)
+constexpr int kLutBytes = 65 * 128;  // 64 lane-banked rows + the dummy row (bin 59 everywhere)
+constexpr uint32_t kDummyOff2 = 0x84008400u;  // LUT offset of the dummy row, both halves
 constexpr int kPlainLutOff = kLutOff + kLutBytes;
 constexpr int kBarOff = kPlainLutOff + 256;
 constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;        // + 128-B alignment slack
@@ -146,6 +148,12 @@ __device__ __forceinline__ DepthRow depth_row(uint32_t addr) {
     return r;
 }
 
+__device__ __forceinline__ uint32_t hle2_mask(uint32_t a, uint32_t b) {
+    uint32_t r;  // 0xFFFF / 0 per half
+    asm("set.le.u32.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t hge2_one(uint32_t a, uint32_t b) {
     uint32_t r;  // 1.0 / 0.0 per half
     asm("set.ge.f16x2.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -169,7 +177,7 @@ __device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uin
     return f + a;
 }
 
-template <bool HAS_DEPTH, bool DEPTH_SRC>
+template <bool HAS_DEPTH, bool DEPTH_SRC, bool FP16WIN>
 __global__ void __launch_bounds__(l59::kThreads, 1)
 lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const __grid_constant__ CUtensorMap depth_map,
@@ -213,7 +221,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     // ---- one-time setup: LUTs, zero counters, barriers, first three positions
     for (int i = tid; i < kLutBytes; i += kThreads) {
         const int code = (i >> 7) * 4 + (i & 3);
-        smem[kLutOff + i] = kUniformLutDev.v[code];
+        smem[kLutOff + i] = code < 256 ? kUniformLutDev.v[code] : (uint8_t)kBins;  // row 64: dummy
     }
     if (tid < 256) smem[kPlainLutOff + tid] = kUniformLutDev.v[tid];
     for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
@@ -236,12 +244,13 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const bool inner = (x != 0) && (x != kTile - 1);  // the 1-px ROI border has no code
         const int cx = inner ? (8 * x - 1) / (kTile - 2) : (lane >> 2);
         const int col = (cx == (lane >> 2)) ? lane : 4 * cx;  // spill-over -> next cell's lane
-        colb[k] = opaque(hist0 + (uint32_t)(((warp >> 2) * kBins * 32 + col) * 4));
+        colb[k] = opaque(hist0 + (uint32_t)(((warp >> 2) * kBinsAlloc * 32 + col) * 4));
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
         mult_row[k] = mult[k];
     }
     const uint32_t lo16 = win.lo << 16;
     const uint32_t span16 = (win.span << 16) | 0xFFFFu;
+    const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // FP16WIN
     const uint32_t lut_lane = opaque(smem_u32(smem + kLutOff) + 4 * lane - 0x6400u);
     const int i0 = (warp * (kTile - 2)) / 8;                   // first interior row of cell row
     const int nrows = ((warp + 1) * (kTile - 2)) / 8 - i0;     // 15 or 16
@@ -302,7 +311,26 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                                  bot.mh, mid.mh);
             }
             uint32_t val[4];
-            if (HAS_DEPTH) {
+            if constexpr (HAS_DEPTH && FP16WIN) {
+                // depth window on both halves at once (dmax <= 0x7BFE): a clamped u16 read as
+                // fp16 bits compares exactly (see depth_row); masked-out pixels are redirected
+                // to the dummy LUT row (-> dummy bin) instead of adding 0
+                uint32_t c0, c1;
+                if constexpr (DEPTH_SRC) {
+                    c0 = mid.h0;
+                    c1 = mid.h1;
+                } else {
+                    const uint2 d = ld_shared_u32x2(d0 + j * (kTile * 2));
+                    c0 = vmin_u16x2(d.x, 0x7BFF7BFFu);
+                    c1 = vmin_u16x2(d.y, 0x7BFF7BFFu);
+                }
+                const uint32_t m0 = hge2_mask(c0, lo2) & hle2_mask(c0, hi2);
+                const uint32_t m1 = hge2_mask(c1, lo2) & hle2_mask(c1, hi2);
+                t0 = (t0 & m0) | (kDummyOff2 & ~m0);
+                t1 = (t1 & m1) | (kDummyOff2 & ~m1);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
+            } else if (HAS_DEPTH) {
                 uint2 d;
                 if constexpr (DEPTH_SRC) d = make_uint2(mid.raw0, mid.raw1);  // centre row
                 else d = ld_shared_u32x2(d0 + j * (kTile * 2));
@@ -349,8 +377,14 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         // ---- epilogue: quad q = (g, bin, cx) holds the 4 lane columns of cells (4g + j, cx),
         // j = byte.  Byte-transpose the 4 words and sum each byte column with IDP4A.
-        for (int q = gtid; q < 2 * kBins * 8; q += kGroupThreads) {
+        for (int q = gtid; q < 2 * kBinsAlloc * 8; q += kGroupThreads) {
             const uint32_t qa = hist0 + q * 16;
+            const int g = q / (kBinsAlloc * 8), rem = q - g * (kBinsAlloc * 8);
+            const int bin = rem >> 3, cx = rem & 7;
+            if (bin == kBins) {  // dummy bin (masked-out pixels): only re-zeroed
+                st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+                continue;
+            }
             const uint4 w = ld_shared_u32x4(qa);
             st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
             const uint32_t lo01 = prmt(w.x, w.y, 0x5140), hi01 = prmt(w.x, w.y, 0x7362);
@@ -359,8 +393,6 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             const uint32_t c1 = __dp4a(prmt(lo01, lo23, 0x7632), 0x01010101u, 0u);
             const uint32_t c2 = __dp4a(prmt(hi01, hi23, 0x5410), 0x01010101u, 0u);
             const uint32_t c3 = __dp4a(prmt(hi01, hi23, 0x7632), 0x01010101u, 0u);
-            const int g = q / (kBins * 8), rem = q - g * (kBins * 8);
-            const int bin = rem >> 3, cx = rem & 7;
             const uint32_t o = staging + (((4 * g) * 8 + cx) * kBins + bin) * 2;  // cell (4g, cx)
             constexpr uint32_t kRow = 8 * kBins * 2;                             // next cell row
             asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "h"((uint16_t)c0) : "memory");
@@ -394,9 +426,12 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
         dm = gm;
     }
     if (depth_source) gm = dm;  // grey is not read
-    auto kern = depth_source ? lbp_hist_lane59_kernel<true, true>
-                : depth      ? lbp_hist_lane59_kernel<true, false>
-                             : lbp_hist_lane59_kernel<false, false>;
+    // depth window as fp16 compares whenever dmax <= 0x7BFE (always for the depth source)
+    const bool fp16win = depth && !win.none_valid && win.lo + win.span <= 0x7BFEu;
+    auto kern = depth_source ? lbp_hist_lane59_kernel<true, true, true>
+                : depth      ? (fp16win ? lbp_hist_lane59_kernel<true, false, true>
+                                        : lbp_hist_lane59_kernel<true, false, false>)
+                             : lbp_hist_lane59_kernel<false, false, false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l59::kSmemBytes);
     if (e != cudaSuccess) return e;
