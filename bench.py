@@ -86,6 +86,9 @@ def parse():
     p.add_argument("--resize", type=int, default=0,
                    help="configs 1/2: resize every ROI to S x S on the GPU before the "
                         "descriptor (the paper's 200x200, P:154; lbp_extract_resized)")
+    p.add_argument("--api", default="fused", choices=["fused", "split"],
+                   help="configs 1/2: lbp_recognize (one fused cluster launch) or "
+                        "lbp_fused_extract + svm_score (two launches)")
     p.add_argument("--chunks", type=int, default=4,
                    help="config5: extraction/all-gather overlap chunks (1 = serial)")
     return p.parse_args()
@@ -440,9 +443,16 @@ def run_latency(args):
     top = torch.empty(n_calls * n_per, dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(dev)
 
+    fused = args.api == "fused" and not args.resize
+
     def call(f):
         r = rois[f * n_per:(f + 1) * n_per]
         o = desc[f * n_per:(f + 1) * n_per]
+        if fused:  # one launch: cluster of cells_y CTAs per ROI, extraction + SVM via DSMEM
+            lb.lbp_recognize(grey, depth, r, DMIN, DMAX, cx, cy, bins, W, b, prepared=prepared,
+                             desc=o, labels=labels[f * n_per:(f + 1) * n_per],
+                             top_score=top[f * n_per:(f + 1) * n_per], stream=stream)
+            return
         if args.resize:
             lb.lbp_extract_resized(grey, depth, r, args.resize, DMIN, DMAX, cx, cy, bins,
                                    out=o, stream=stream)
@@ -493,7 +503,9 @@ def run_latency(args):
         "latency_us": {"eager_p50": float(np.percentile(lat, 50) * 1e3),
                        "eager_p99": float(np.percentile(lat, 99) * 1e3),
                        "graph_per_call": per_call_graph * 1e3},
-        "frame_h2d_bytes": frame_bytes, "gpu_launches": 2 * n_calls * reps, "clocks": clk.summary(),
+        "frame_h2d_bytes": frame_bytes, "gpu_launches": (1 if fused else 2) * n_calls * reps,
+        "api": "lbp_recognize (fused)" if fused else "lbp_fused_extract/lbp_extract_resized + "
+               "svm_score", "clocks": clk.summary(),
         "roofline": None, "cpu_baseline": latency_cpu_leg(args, g, d, rois_np, n_per, W_np, b_np,
                                                           cx, cy, bins), "e2e": None,
     }

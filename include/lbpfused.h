@@ -150,6 +150,25 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W,
                   int32_t* labels, float* top_score, float reject_threshold,
                   lbp_stream_t stream);
 
+/*
+ * lbp_recognize -- the whole device path in one call (lbp_fused_extract + svm_score, grey
+ * source): descriptors, statuses, scores, labels and top scores exactly as the two calls
+ * would produce them (same oracle definitions).  For batches smaller than the SM count with
+ * cells_y <= 8 and n_classes <= 2048 it is ONE launch: a thread-block cluster of cells_y CTAs
+ * per ROI computes one cell row each, scores its descriptor segment, and rank 0 combines the
+ * per-class partials over distributed shared memory; otherwise
+ * it runs the two kernels of lbp_fused_extract and svm_score.
+ *   desc       out, REQUIRED: u16 [n_rois][dim] (also the scorer's input)
+ *   prepared   nullable svm_prepare() workspace (tensor-core scorer for large batches)
+ *   scores / roi_status / labels / top_score  nullable outputs as in svm_score / extract
+ */
+int32_t lbp_recognize(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                      const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                      int32_t cells_x, int32_t cells_y, int32_t bins, const float* W,
+                      const float* bias, int32_t n_classes, const void* prepared,
+                      float reject_threshold, uint16_t* desc, int32_t* roi_status, float* scores,
+                      int32_t* labels, float* top_score, lbp_stream_t stream);
+
 /* Bytes of device workspace svm_prepare() needs for a [n_classes][dim] model
  * (0 if the tensor-core path does not apply to this shape). */
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim);

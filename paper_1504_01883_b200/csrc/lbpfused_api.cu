@@ -8,6 +8,7 @@
 #include "lbp_hist_fast.cuh"
 #include "lbp_hist_lane59.cuh"
 #include "lbp_resize.cuh"
+#include "lbp_recognize.cuh"
 #include "svm_fp64.cuh"
 #include "svm_gemm.cuh"
 
@@ -197,6 +198,36 @@ int32_t lbp_extract_resized(const uint8_t* grey, const uint16_t* depth, lbp_imag
     }
 #undef LBPF_RESIZE_LAUNCH
     return launch_status(cudaGetLastError());
+}
+
+int32_t lbp_recognize(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                      const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                      int32_t cells_x, int32_t cells_y, int32_t bins, const float* W,
+                      const float* bias, int32_t n_classes, const void* prepared,
+                      float reject_threshold, uint16_t* desc, int32_t* roi_status, float* scores,
+                      int32_t* labels, float* top_score, lbp_stream_t stream_) {
+    if (n_rois < 0 || n_classes < 1) return LBP_E_ARG;
+    const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
+    if (dim < 0) return dim;
+    if (dmin > dmax) return LBP_E_ARG;
+    if (n_rois == 0) return LBP_OK;
+    if (!grey || !rois || !desc || !W || !bias) return LBP_E_ARG;
+    int32_t st = check_geometry(geom, true, depth != nullptr);
+    if (st != LBP_OK) return st;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    // small batches: one launch, a cluster of cells_y CTAs per ROI (extract + score via DSMEM)
+    if (n_rois < num_sms() && cells_y <= kRecMaxCluster && n_classes <= kRecMaxClasses &&
+        (int64_t)n_rois * cells_y <= 0x7FFFFFFF) {
+        const DepthWindow win = make_window(dmin, dmax);
+        return launch_status(launch_lbp_recognize_cluster(
+            grey, depth, geom, rois, n_rois, win, cells_x, cells_y, bins, desc, roi_status, W,
+            bias, n_classes, scores, labels, top_score, reject_threshold, stream));
+    }
+    st = lbp_extract_source(grey, depth, geom, rois, n_rois, dmin, dmax, cells_x, cells_y, bins,
+                            LBP_SRC_GREY, desc, roi_status, stream_);
+    if (st != LBP_OK) return st;
+    return svm_score(desc, n_rois, dim, W, bias, n_classes, prepared, scores, labels, top_score,
+                     reject_threshold, stream_);
 }
 
 int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,

@@ -58,6 +58,9 @@ def lib():
         L.lbp_extract_resized.argtypes = [P, P, lbp_images_t, P, i32, i32, u16, u16, i32, i32,
                                           i32, i32, P, P, P]
         L.lbp_extract_resized.restype = i32
+        L.lbp_recognize.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, P, P,
+                                    i32, P, f32, P, P, P, P, P, P]
+        L.lbp_recognize.restype = i32
         L.svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, P, f32, P]
         L.svm_score.restype = i32
         L.svm_workspace_bytes.argtypes = [i32, i32]
@@ -204,6 +207,41 @@ def lbp_extract_resized(grey: torch.Tensor | None, depth: torch.Tensor | None,
     if st != LBP_OK:
         raise LbpError(st, "lbp_extract_resized")
     return out
+
+
+def lbp_recognize(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.Tensor,
+                  dmin: int, dmax: int, cells_x: int, cells_y: int, bins: int, W: torch.Tensor,
+                  bias: torch.Tensor, prepared=None, reject_threshold: float = -math.inf,
+                  want_scores: bool = False, desc: torch.Tensor | None = None,
+                  labels: torch.Tensor | None = None, top_score: torch.Tensor | None = None,
+                  roi_status: torch.Tensor | None = None,
+                  stream: torch.cuda.Stream | None = None):
+    """Descriptors + SVM in one call (one fused launch for small batches):
+    returns (desc u16 [n][dim], scores fp32 [n][C] or None, labels int32 [n], top fp32 [n])."""
+    _check_cuda(grey, depth, rois, W, bias, prepared, desc, labels, top_score, roi_status)
+    assert grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)
+    assert rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5
+    assert W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32
+    n = rois.shape[0]
+    dim = lbp_descriptor_dim(cells_x, cells_y, bins)
+    C = W.shape[0]
+    if W.shape[1] != dim or bias.numel() != C:
+        raise LbpError(LBP_E_ARG, "lbp_recognize: weight shape mismatch")
+    dev = grey.device
+    if desc is None:
+        desc = torch.empty((n, dim), dtype=torch.uint16, device=dev)
+    if labels is None:
+        labels = torch.empty(n, dtype=torch.int32, device=dev)
+    if top_score is None:
+        top_score = torch.empty(n, dtype=torch.float32, device=dev)
+    scores = torch.empty((n, C), dtype=torch.float32, device=dev) if want_scores else None
+    st = lib().lbp_recognize(_ptr(grey), _ptr(depth), images_geometry(grey, depth), _ptr(rois),
+                             n, dmin, dmax, cells_x, cells_y, bins, _ptr(W), _ptr(bias), C,
+                             _ptr(prepared), reject_threshold, _ptr(desc), _ptr(roi_status),
+                             _ptr(scores), _ptr(labels), _ptr(top_score), _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_recognize")
+    return desc, scores, labels, top_score
 
 
 def svm_workspace_bytes(n_classes: int, dim: int) -> int:
