@@ -62,6 +62,8 @@ def lib():
         L.oracle_lbp_extract_resized.argtypes = [P, P, i32, i32, i32, i64, i64, i64, i64, P, i32,
                                                  i32, u16, u16, i32, i32, i32, i32, P, P]
         L.oracle_lbp_extract_resized.restype = i32
+        L.oracle_svm_score_l1.argtypes = [P, i32, i32, i32, P, P, i32, P, P, P, f32]
+        L.oracle_svm_score_l1.restype = i32
         L.oracle_svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, f32]
         L.oracle_svm_score.restype = i32
         _lib = L
@@ -197,4 +199,22 @@ def svm_score(desc: np.ndarray, W: np.ndarray, bias: np.ndarray,
                                 _ptr(labels), _ptr(top), reject_threshold)
     if st != ORC_OK:
         raise ValueError(f"oracle_svm_score status {st}")
+    return scores, labels, top
+
+
+def svm_score_l1(desc: np.ndarray, W: np.ndarray, bias: np.ndarray, block: int,
+                 reject_threshold: float = float("-inf")):
+    """SVM on per-block L1-normalised descriptors: (scores, labels, top)."""
+    desc = np.ascontiguousarray(desc, dtype=np.uint16)
+    W = np.ascontiguousarray(W, dtype=np.float32)
+    bias = np.ascontiguousarray(bias, dtype=np.float32)
+    n, dim = desc.shape
+    C = W.shape[0]
+    scores = np.zeros((n, C), dtype=np.float32)
+    labels = np.zeros(n, dtype=np.int32)
+    top = np.zeros(n, dtype=np.float32)
+    st = lib().oracle_svm_score_l1(_ptr(desc), n, dim, block, _ptr(W), _ptr(bias), C,
+                                   _ptr(scores), _ptr(labels), _ptr(top), reject_threshold)
+    if st != ORC_OK:
+        raise ValueError(f"oracle_svm_score_l1 status {st}")
     return scores, labels, top

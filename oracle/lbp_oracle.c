@@ -262,6 +262,52 @@ int32_t oracle_lbp_extract(const uint8_t* grey, const uint16_t* depth,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Linear OvR SVM on L1-normalised blocks (SURVEY §8f-3 variant; S:379-387 normalize:    */
+/* "each block divided by its own count sum; empty block maps to all zeros"):           */
+/*   f[n][d] = h[n][d] / N_k for d in block k (N_k = sum of the block's counts;          */
+/*   f = 0 when N_k = 0), blocks of `block` consecutive entries (one cell = `bins`);     */
+/*   s[n][c] = (float)( (double)b[c] + sum_{d ascending} (double)W[c][d] * f[n][d] )     */
+/* with f computed in fp64 (one division per entry), labels as in oracle_svm_score.     */
+/* ------------------------------------------------------------------------ */
+int32_t oracle_svm_score_l1(const uint16_t* desc, int32_t n, int32_t dim, int32_t block,
+                            const float* W, const float* bias, int32_t n_classes,
+                            float* scores, int32_t* labels, float* top_score,
+                            float reject_threshold)
+{
+    if (n < 0 || dim < 1 || n_classes < 1 || block < 1 || dim % block != 0) return ORC_E_ARG;
+    if (n == 0) return ORC_OK;
+    if (!desc || !W || !bias) return ORC_E_ARG;
+    double* f = (double*)malloc((size_t)dim * sizeof(double));
+    if (!f) return ORC_E_ARG;
+    for (int32_t i = 0; i < n; ++i) {
+        const uint16_t* h = desc + (int64_t)i * dim;
+        for (int32_t k0 = 0; k0 < dim; k0 += block) {
+            uint64_t sum = 0;
+            for (int32_t d = k0; d < k0 + block; ++d) sum += h[d];
+            for (int32_t d = k0; d < k0 + block; ++d)
+                f[d] = sum ? (double)h[d] / (double)sum : 0.0;
+        }
+        float best = 0.0f;
+        int32_t best_c = 0;
+        for (int32_t c = 0; c < n_classes; ++c) {
+            const float* w = W + (int64_t)c * dim;
+            double acc = (double)bias[c];
+            for (int32_t d = 0; d < dim; ++d) acc += (double)w[d] * f[d];
+            float sc = (float)acc;
+            if (scores) scores[(int64_t)i * n_classes + c] = sc;
+            if (c == 0 || sc > best) {
+                best = sc;
+                best_c = c;
+            }
+        }
+        if (top_score) top_score[i] = best;
+        if (labels) labels[i] = (best < reject_threshold) ? -1 : best_c;
+    }
+    free(f);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* ROI resize ("The detected face ... is resized to 200x200 pixels";  */
 /* SURVEY §8f-2; S:91-99 resize):                                           */
 /*  grey : bilinear with half-pixel centres, rounded half up.  Output pixel */
