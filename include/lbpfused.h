@@ -169,6 +169,18 @@ int32_t lbp_recognize(const uint8_t* grey, const uint16_t* depth, lbp_images_t g
                       float reject_threshold, uint16_t* desc, int32_t* roi_status, float* scores,
                       int32_t* labels, float* top_score, lbp_stream_t stream);
 
+/*
+ * svm_score_l1 -- the linear OvR SVM on per-block L1-normalised descriptors (SURVEY §8f-3
+ * variant; S:379-387 normalize: each block divided by its own count sum, an empty block maps
+ * to zeros): s[n][c] = fp32(b[c] + sum_k (sum_{d in block k} W[c][d] h[n][d]) / N_k), blocks
+ * of `block` consecutive entries (one cell: block = bins); labels / top / reject as
+ * svm_score.  CUDA cores, fp64 accumulation of exact products.  dim % block != 0 -> LBP_E_ARG;
+ * LBP_E_UNSUPPORTED if one staged descriptor row (4 B per entry) exceeds 200 KB.
+ */
+int32_t svm_score_l1(const uint16_t* desc, int32_t n, int32_t dim, int32_t block, const float* W,
+                     const float* bias, int32_t n_classes, float* scores, int32_t* labels,
+                     float* top_score, float reject_threshold, lbp_stream_t stream);
+
 /* Bytes of device workspace svm_prepare() needs for a [n_classes][dim] model
  * (0 if the tensor-core path does not apply to this shape). */
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim);

@@ -276,6 +276,38 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, 
     return launch_status(cudaGetLastError());
 }
 
+int32_t svm_score_l1(const uint16_t* desc, int32_t n, int32_t dim, int32_t block, const float* W,
+                     const float* bias, int32_t n_classes, float* scores, int32_t* labels,
+                     float* top_score, float reject_threshold, lbp_stream_t stream_) {
+    if (n < 0 || dim < 1 || n_classes < 1 || block < 1 || dim % block != 0) return LBP_E_ARG;
+    if (n == 0) return LBP_OK;
+    if (!desc || !W || !bias) return LBP_E_ARG;
+    const int nblk = dim / block;
+    auto smem_for = [&](int rows) {
+        return (size_t)rows * dim * sizeof(float) + 8 + (size_t)rows * nblk * sizeof(double);
+    };
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (smem_for(kSvmRowsMax) <= 200 * 1024) {  // 8 crops per CTA
+        const size_t smem = smem_for(kSvmRowsMax);
+        cudaError_t e = cudaFuncSetAttribute(svm_score_l1_kernel<kSvmRowsMax>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return launch_status(e);
+        const int grid = (int)((n + kSvmRowsMax - 1) / kSvmRowsMax);
+        svm_score_l1_kernel<kSvmRowsMax><<<grid, kSvmThreads, smem, stream>>>(
+            desc, n, dim, block, W, bias, n_classes, scores, labels, top_score, reject_threshold);
+        return launch_status(cudaGetLastError());
+    }
+    if (smem_for(1) > 200 * 1024) return LBP_E_UNSUPPORTED;
+    cudaError_t e = cudaFuncSetAttribute(svm_score_l1_kernel<1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_for(1));
+    if (e != cudaSuccess) return launch_status(e);
+    svm_score_l1_kernel<1><<<n, kSvmThreads, smem_for(1), stream>>>(
+        desc, n, dim, block, W, bias, n_classes, scores, labels, top_score, reject_threshold);
+    return launch_status(cudaGetLastError());
+}
+
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim) {
     SvmPrepHeader h;
     if (!svm_layout(n_classes, dim, &h)) return 0;

@@ -152,3 +152,107 @@ svm_score_fp64_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
 }
 
 }  // namespace lbpf
+
+namespace lbpf {
+
+// ---------------------------------------------------------------------------- L1 variant
+// s[n][c] = fp32(b[c] + sum_k (sum_{d in block k} W[c][d] h[n][d]) / N_k), N_k = the block's
+// count sum (blocks with N_k = 0 contribute 0): the SVM on per-block L1-normalised
+// descriptors, with the division applied to each block's exact-product fp64
+// partial sum (the same real number as the oracle's sum of W * (h / N_k)).  CTA = R (8, or 1
+// for long descriptors) crops staged in smem as fp32 (exact counts); a warp per class; lane l owns blocks
+// l, l+32, ... and sums them in order, then one shuffle reduction per class.
+template <int R>
+__global__ void __launch_bounds__(kSvmThreads)
+svm_score_l1_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim, int32_t block,
+                    const float* __restrict__ W, const float* __restrict__ bias,
+                    int32_t n_classes, float* __restrict__ scores, int32_t* __restrict__ labels,
+                    float* __restrict__ top_score, float reject_threshold) {
+    extern __shared__ float l1s[];  // [rows][dim] fp32 counts, then [rows][nblk] fp64 N_k
+    constexpr int kWarps = kSvmThreads / 32;
+    __shared__ float wbest[kWarps][R];
+    __shared__ int wbest_c[kWarps][R];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nblk = dim / block;
+    const int64_t row0 = (int64_t)blockIdx.x * R;
+    const int rows = (int)((n - row0) < R ? (n - row0) : R);
+    float* xs = l1s;
+    double* nk = reinterpret_cast<double*>(l1s + ((R * dim + 1) & ~1));
+    for (int i = threadIdx.x; i < R * dim; i += blockDim.x)
+        xs[i] = i < rows * dim ? (float)__ldg(desc + row0 * dim + i) : 0.0f;
+    __syncthreads();
+    for (int i = threadIdx.x; i < R * nblk; i += blockDim.x) {
+        const int r = i / nblk, k = i - r * nblk;
+        double sum = 0.0;  // exact: integer counts
+        for (int d = k * block; d < (k + 1) * block; ++d) sum += (double)xs[r * dim + d];
+        nk[i] = sum;
+    }
+    __syncthreads();
+    float best[R];
+    int best_c[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        best[r] = -INFINITY;
+        best_c[r] = 0x7FFFFFFF;
+    }
+    for (int c = warp; c < n_classes; c += kWarps) {
+        const float* w = W + (int64_t)c * dim;
+        double acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = 0.0;
+        for (int k = lane; k < nblk; k += 32) {
+            double p[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) p[r] = 0.0;
+            for (int d = k * block; d < (k + 1) * block; ++d) {
+                const double wd = (double)__ldg(w + d);
+#pragma unroll
+                for (int r = 0; r < R; ++r) p[r] = fma(wd, (double)xs[r * dim + d], p[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double N = nk[r * nblk + k];
+                if (N > 0.0) acc[r] += p[r] / N;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xFFFFFFFFu, acc[r], off);
+        }
+        const double b = (double)__ldg(bias + c);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const float sc = (float)(acc[r] + b);
+            if (lane == 0 && r < rows && scores) scores[(row0 + r) * n_classes + c] = sc;
+            if (better(sc, c, best[r], best_c[r]) || best_c[r] == 0x7FFFFFFF) {
+                best[r] = sc;
+                best_c[r] = c;
+            }
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            wbest[warp][r] = best[r];
+            wbest_c[warp][r] = best_c[r];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < rows) {
+        const int r = threadIdx.x;
+        float b = wbest[0][r];
+        int bc = wbest_c[0][r];
+        for (int w2 = 1; w2 < kWarps; ++w2) {
+            if (wbest_c[w2][r] == 0x7FFFFFFF) continue;
+            if (bc == 0x7FFFFFFF || better(wbest[w2][r], wbest_c[w2][r], b, bc)) {
+                b = wbest[w2][r];
+                bc = wbest_c[w2][r];
+            }
+        }
+        if (top_score) top_score[row0 + r] = b;
+        if (labels) labels[row0 + r] = (b < reject_threshold) ? -1 : bc;
+    }
+}
+
+}  // namespace lbpf

@@ -63,6 +63,8 @@ def lib():
         L.lbp_recognize.restype = i32
         L.svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, P, f32, P]
         L.svm_score.restype = i32
+        L.svm_score_l1.argtypes = [P, i32, i32, i32, P, P, i32, P, P, P, f32, P]
+        L.svm_score_l1.restype = i32
         L.svm_workspace_bytes.argtypes = [i32, i32]
         L.svm_workspace_bytes.restype = sz
         L.svm_prepare.argtypes = [P, i32, i32, P, sz, P]
@@ -314,3 +316,25 @@ def lbp_recognize_host(grey_h: torch.Tensor, depth_h: torch.Tensor | None, rois_
                                   workspace.numel(), _ptr(labels_h), _ptr(top_h), _stream(stream))
     if st != LBP_OK:
         raise LbpError(st, "lbp_recognize_host")
+
+
+def svm_score_l1(desc: torch.Tensor, W: torch.Tensor, bias: torch.Tensor, block: int,
+                 reject_threshold: float = -math.inf, want_scores: bool = True,
+                 stream=None):
+    """(scores or None, labels, top) of the SVM on per-block L1-normalised descriptors."""
+    _check_cuda(desc, W, bias)
+    assert desc.dtype == torch.uint16 and desc.is_contiguous()
+    assert W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32
+    n, dim = desc.shape
+    C = W.shape[0]
+    if W.shape[1] != dim or bias.numel() != C:
+        raise LbpError(LBP_E_ARG, "svm_score_l1: dimension mismatch")
+    dev = desc.device
+    scores = torch.empty((n, C), dtype=torch.float32, device=dev) if want_scores else None
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    top = torch.empty(n, dtype=torch.float32, device=dev)
+    st = lib().svm_score_l1(_ptr(desc), n, dim, block, _ptr(W), _ptr(bias), C, _ptr(scores),
+                            _ptr(labels), _ptr(top), reject_threshold, _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "svm_score_l1")
+    return scores, labels, top
