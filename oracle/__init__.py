@@ -64,6 +64,8 @@ def lib():
         L.oracle_lbp_extract_resized.restype = i32
         L.oracle_svm_score_l1.argtypes = [P, i32, i32, i32, P, P, i32, P, P, P, f32]
         L.oracle_svm_score_l1.restype = i32
+        L.oracle_svm_train_ovr.argtypes = [P, i32, i32, P, i32, P, i64, i32, P, P, P]
+        L.oracle_svm_train_ovr.restype = i32
         L.oracle_svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, f32]
         L.oracle_svm_score.restype = i32
         _lib = L
@@ -218,3 +220,21 @@ def svm_score_l1(desc: np.ndarray, W: np.ndarray, bias: np.ndarray, block: int,
     if st != ORC_OK:
         raise ValueError(f"oracle_svm_score_l1 status {st}")
     return scores, labels, top
+
+
+def svm_train_ovr(desc: np.ndarray, labels: np.ndarray, n_classes: int, order: np.ndarray,
+                  inv_lambda: int, return_z: bool = False):
+    """One-vs-rest linear SVM training (exact integer Pegasos form, R20):
+    (W fp32 [C][dim], bias fp32 [C]) (and the integer state z [C][dim+1])."""
+    desc = np.ascontiguousarray(desc, dtype=np.uint16)
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    n, dim = desc.shape
+    W = np.zeros((n_classes, dim), np.float32)
+    b = np.zeros(n_classes, np.float32)
+    z = np.zeros((n_classes, dim + 1), np.int64)
+    st = lib().oracle_svm_train_ovr(_ptr(desc), n, dim, _ptr(labels), n_classes, _ptr(order),
+                                    order.size, inv_lambda, _ptr(W), _ptr(b), _ptr(z))
+    if st != ORC_OK:
+        raise ValueError(f"oracle_svm_train_ovr status {st}")
+    return (W, b, z) if return_z else (W, b)

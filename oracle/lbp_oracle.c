@@ -262,6 +262,64 @@ int32_t oracle_lbp_extract(const uint8_t* grey, const uint16_t* depth,
 }
 
 /* ------------------------------------------------------------------------ */
+/* One-vs-rest linear SVM training ("finding a hyperplane ...",  */
+/* P:144 A-vs-B per identity; S:449-466 train_binary / train_ovr: minimise               */
+/* lambda/2 |w|^2 + mean hinge loss by epoch-based subgradient steps 1/(lambda t) over a */
+/* seeded visit order).  DESIGN.md reading R20: the bias is folded in as a constant      */
+/* feature 1 (regularised with w), lambda = 1 / inv_lambda, and the step is Pegasos':     */
+/*   t = 1..T, i = order[t-1], y = +1 if label[i] == c else -1, x~ = (x_i, 1):            */
+/*   violated iff t == 1 or y (w_{t-1} . x~) < 1;                                          */
+/*   w_t = (1 - 1/t) w_{t-1} + [violated] y x~ / (lambda t).                               */
+/* Written exactly: with z_t = lambda t w_t, z_t = z_{t-1} + [violated] y x~ -- an integer */
+/* vector -- and (t > 1) the test y (w_{t-1} . x~) < 1 is y (z_{t-1} . x~) < lambda (t-1), */
+/* i.e. the integer y (z . x~) < ceil((t - 1) / inv_lambda).  The model is the last       */
+/* iterate w_T = inv_lambda z_T / T, rounded once fp64 -> fp32 per entry.                 */
+/* Requires |y (z . x~)| < 2^63 (e.g. T <= 2^24 and sum_d x_d <= 2^16).                   */
+/* ------------------------------------------------------------------------ */
+static int64_t ceil_div_pos(int64_t a, int64_t b) { /* a >= 0, b > 0 */
+    return (a + b - 1) / b;
+}
+
+int32_t oracle_svm_train_ovr(const uint16_t* desc, int32_t n, int32_t dim,
+                             const int32_t* labels, int32_t n_classes,
+                             const int32_t* order, int64_t T, int32_t inv_lambda,
+                             float* W /* [C][dim] */, float* bias /* [C] */,
+                             int64_t* z_out /* nullable [C][dim + 1] */)
+{
+    if (n < 1 || dim < 1 || n_classes < 1 || T < 1 || inv_lambda < 1) return ORC_E_ARG;
+    if (!desc || !labels || !order || !W || !bias) return ORC_E_ARG;
+    for (int64_t t = 0; t < T; ++t)
+        if (order[t] < 0 || order[t] >= n) return ORC_E_ARG;
+    int64_t* z = (int64_t*)malloc((size_t)(dim + 1) * sizeof(int64_t));
+    if (!z) return ORC_E_ARG;
+    for (int32_t c = 0; c < n_classes; ++c) {
+        for (int32_t d = 0; d <= dim; ++d) z[d] = 0;
+        for (int64_t t = 1; t <= T; ++t) {
+            int32_t i = order[t - 1];
+            const uint16_t* x = desc + (int64_t)i * dim;
+            int64_t y = (labels[i] == c) ? 1 : -1;
+            int violated = 1;
+            if (t > 1) {
+                int64_t dot = z[dim]; /* the constant feature 1 */
+                for (int32_t d = 0; d < dim; ++d) dot += z[d] * (int64_t)x[d];
+                violated = y * dot < ceil_div_pos(t - 1, inv_lambda);
+            }
+            if (violated) {
+                for (int32_t d = 0; d < dim; ++d) z[d] += y * (int64_t)x[d];
+                z[dim] += y;
+            }
+        }
+        for (int32_t d = 0; d < dim; ++d)
+            W[(int64_t)c * dim + d] = (float)((double)((int64_t)inv_lambda * z[d]) / (double)T);
+        bias[c] = (float)((double)((int64_t)inv_lambda * z[dim]) / (double)T);
+        if (z_out)
+            for (int32_t d = 0; d <= dim; ++d) z_out[(int64_t)c * (dim + 1) + d] = z[d];
+    }
+    free(z);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Linear OvR SVM on L1-normalised blocks (SURVEY §8f-3 variant; S:379-387 normalize:    */
 /* "each block divided by its own count sum; empty block maps to all zeros"):           */
 /*   f[n][d] = h[n][d] / N_k for d in block k (N_k = sum of the block's counts;          */

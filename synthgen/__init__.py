@@ -241,3 +241,16 @@ def kinect_frames(n_frames: int, n_faces: int = 4, H: int = 480, W: int = 640, r
             d = np.where(e <= a2 * b2, fd[k] - relief, d)
         depth[f] = d.astype(np.uint16)
     return grey, depth, rois
+
+
+# --------------------------------------------------------------------------- training inputs
+
+def train_order(n: int, epochs: int, seed: int = 42) -> np.ndarray:
+    """The seeded visit order of SVM training ("samples visited in seeded-shuffle
+    order"): epoch e is a permutation of 0..n-1 drawn from SeedSequence([seed, e]); the
+    epochs are concatenated (int32 [epochs * n])."""
+    out = np.empty(epochs * n, np.int32)
+    for e in range(epochs):
+        rng = np.random.default_rng(np.random.SeedSequence([seed, e, 0x5EED]))
+        out[e * n:(e + 1) * n] = rng.permutation(n)
+    return out
