@@ -51,6 +51,10 @@ WORKLOADS = {
     "config5": (262144, 128, 128, 8, 8, 59, 0,
                 "BASELINE configs[4]: online database build, 256k 128x128 crops sharded over the "
                 "GPUs, descriptors + int32 labels all-gathered (NCCL) into the training matrix"),
+    # training after the database build: crops = database size, 1 epoch
+    "train": (16384, 128, 128, 8, 8, 59, 100,
+              "SURVEY 8f-4: one-vs-rest linear SVM training (exact integer Pegasos) on a "
+              "16384-crop database, 100 identities, 1 epoch"),
 }
 N_IDS = 100  # identities of the database build (label = crop index mod N_IDS)
 DMIN, DMAX = 600, 1400
@@ -279,6 +283,8 @@ def main():
         return run_reference(args)
     if args.workload == "config5":
         return run_dbbuild(args)
+    if args.workload == "train":
+        return run_train(args)
     if args.workload in ("config1", "config2"):
         return run_latency(args)
 
@@ -644,6 +650,63 @@ def run_dbbuild(args):
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+    return 0
+
+
+def run_train(args):
+    """SVM training on the GPU: descriptors of a synthetic database, then
+    svm_train_ovr over one seeded epoch; rate = training steps (sample x class) per second.
+    The oracle trains the same classes on the same inputs for a bounded sample of classes
+    (equivalence gate: the integer state must match bit for bit)."""
+    import torch
+
+    import paper_1504_01883_b200 as lb
+    import synthgen
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n, H, Wd, cx, cy, bins, C, desc_txt = WORKLOADS["train"]
+    n = args.crops or n
+    grey, depth = synthgen.gpu_face_crops(n, H, Wd, seed=args.seed, device=dev)
+    rois = torch.from_numpy(synthgen.full_rois(n, H, Wd)).to(dev)
+    desc = lb.lbp_fused_extract(grey, depth, rois, DMIN, DMAX, cx, cy, bins)
+    labels = (torch.arange(n, device=dev) % C).to(torch.int32)
+    order = torch.from_numpy(synthgen.train_order(n, 1, seed=args.seed)).to(dev)
+    inv_lambda = 10000
+    lb.svm_train_ovr(desc, labels, C, order[:min(n, 256)], inv_lambda)  # warm-up
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        a.record(stream)
+        W, b, zst = lb.svm_train_ovr(desc, labels, C, order, inv_lambda, return_z=True)
+        z.record(stream)
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(z)
+    steps = n * C
+    cpu = None
+    if not args.skip_cpu:
+        import oracle
+        k = 2  # classes timed on the host (one thread), same inputs
+        dn = desc.cpu().view(torch.int16).numpy().view(np.uint16)
+        t0 = time.perf_counter()
+        _, _, zr = oracle.svm_train_ovr(dn, labels.cpu().numpy(), k, order.cpu().numpy(),
+                                        inv_lambda, return_z=True)
+        secs = time.perf_counter() - t0
+        gate = bool(np.array_equal(zst[:k].cpu().numpy(), zr))
+        cpu = {"value": n * k / secs, "unit": "training steps/s", "cores": 1, "kind": "oracle",
+               "sample": f"{k} of {C} classes, one epoch of {n} samples, one thread, {secs:.1f} s",
+               "equivalence_gate": "pass" if gate else "FAIL"}
+        if not gate:
+            print(json.dumps({"error": "equivalence gate failed: GPU training != oracle"}))
+            return 3
+    line = {"metric": "SVM training steps (sample x class) per second", "value": steps / (ms * 1e-3),
+            "unit": "training steps/s", "n_gpus": 1, "steps": 1, "warmup": 1, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic",
+            "config": {"workload": f"train: {desc_txt}", "samples": n, "classes": C,
+                       "epochs": 1, "dim": cx * cy * bins, "inv_lambda": inv_lambda},
+            "cpu_baseline": cpu, "e2e": None, "gpu_launches": 1, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
     return 0
 
 

@@ -181,6 +181,28 @@ int32_t svm_score_l1(const uint16_t* desc, int32_t n, int32_t dim, int32_t block
                      const float* bias, int32_t n_classes, float* scores, int32_t* labels,
                      float* top_score, float reject_threshold, lbp_stream_t stream);
 
+/*
+ * svm_train_ovr -- one-vs-rest linear SVM training on the descriptors (P:140-144
+ * "finding a hyperplane"; P:144 one identity against the others; R20):
+ * for every class c, Pegasos steps over the visit order with lambda = 1 / inv_lambda and the
+ * bias folded in as a constant feature 1 (regularised with w):
+ *   t = 1..T, i = order[t-1], y = +1 if labels[i] == c else -1 (labels outside [0, C) are
+ *   negatives for every class), x~ = (desc[i], 1);
+ *   violated iff t == 1 or y (w_{t-1} . x~) < 1;  w_t = (1 - 1/t) w_{t-1} + [violated] y x~/(lambda t)
+ * computed EXACTLY in integers (z_t = lambda t w_t), so the result is bit-reproducible and
+ * identical to the oracle's; the model is the last iterate, W[c][d] = fp32(fp64(inv_lambda
+ * z_T[d]) / T), bias[c] likewise from the constant feature.
+ *   desc     u16 [n][dim] (device), dim <= 16,384 (LBP_E_UNSUPPORTED above)
+ *   labels   int32 [n];  order int32 [T], every entry in [0, n) (NOT checked: an index out of
+ *            range is undefined behaviour); e.g. one seeded permutation of 0..n-1 per epoch
+ *   W, bias  out fp32 [n_classes][dim], [n_classes];  z_out  nullable int64 [n_classes][dim+1]
+ * Preconditions for exact int64 arithmetic: T <= 2^31 and |z . x~| < 2^63 (e.g. T <= 2^24 with
+ * sum_d desc[i][d] <= 2^16).  One CTA per class; the T steps of a class are sequential.
+ */
+int32_t svm_train_ovr(const uint16_t* desc, int32_t n, int32_t dim, const int32_t* labels,
+                      int32_t n_classes, const int32_t* order, int64_t T, int32_t inv_lambda,
+                      float* W, float* bias, int64_t* z_out, lbp_stream_t stream);
+
 /* Bytes of device workspace svm_prepare() needs for a [n_classes][dim] model
  * (0 if the tensor-core path does not apply to this shape). */
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim);

@@ -10,7 +10,7 @@ from .lbpfused import (LBP_E_ARG, LBP_E_CUDA, LBP_E_GRID, LBP_E_OVERFLOW, LBP_E_
                        lbp_fused_extract, lbp_recognize, lbp_recognize_host,
                        lbp_recognize_workspace_bytes,
                        status_string, svm_prepare, svm_score, svm_score_l1,
-                       svm_workspace_bytes)
+                       svm_train_ovr, svm_workspace_bytes)
 
 __all__ = ["LBP_OK", "LBP_E_ARG", "LBP_E_ROI", "LBP_E_GRID", "LBP_E_OVERFLOW",
            "LBP_SRC_GREY", "LBP_SRC_DEPTH", "LBP_SRC_FUSED", "lbp_extract_source",
@@ -18,4 +18,4 @@ __all__ = ["LBP_OK", "LBP_E_ARG", "LBP_E_ROI", "LBP_E_GRID", "LBP_E_OVERFLOW",
            "LBP_E_UNSUPPORTED", "LBP_E_CUDA", "LbpError", "images_geometry",
            "lbp_descriptor_dim", "lbp_fused_extract", "lbp_recognize_host",
            "lbp_recognize_workspace_bytes", "status_string", "svm_prepare", "svm_score",
-           "svm_score_l1", "svm_workspace_bytes"]
+           "svm_score_l1", "svm_train_ovr", "svm_workspace_bytes"]

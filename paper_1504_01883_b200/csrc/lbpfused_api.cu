@@ -11,6 +11,7 @@
 #include "lbp_recognize.cuh"
 #include "svm_fp64.cuh"
 #include "svm_gemm.cuh"
+#include "svm_train.cuh"
 
 using namespace lbpf;
 
@@ -305,6 +306,23 @@ int32_t svm_score_l1(const uint16_t* desc, int32_t n, int32_t dim, int32_t block
     if (e != cudaSuccess) return launch_status(e);
     svm_score_l1_kernel<1><<<n, kSvmThreads, smem_for(1), stream>>>(
         desc, n, dim, block, W, bias, n_classes, scores, labels, top_score, reject_threshold);
+    return launch_status(cudaGetLastError());
+}
+
+int32_t svm_train_ovr(const uint16_t* desc, int32_t n, int32_t dim, const int32_t* labels,
+                      int32_t n_classes, const int32_t* order, int64_t T, int32_t inv_lambda,
+                      float* W, float* bias, int64_t* z_out, lbp_stream_t stream_) {
+    if (n < 1 || dim < 1 || n_classes < 1 || T < 1 || inv_lambda < 1) return LBP_E_ARG;
+    if (T > (int64_t(1) << 31)) return LBP_E_ARG;
+    if (!desc || !labels || !order || !W || !bias) return LBP_E_ARG;
+    if (dim > kTrainMaxDim) return LBP_E_UNSUPPORTED;
+    const size_t smem = (size_t)(dim + 1) * sizeof(int64_t);
+    cudaError_t e = cudaFuncSetAttribute(svm_train_ovr_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return launch_status(e);
+    const int grid = std::min(n_classes, 2 * num_sms());
+    svm_train_ovr_kernel<<<grid, kTrainThreads, smem, (cudaStream_t)stream_>>>(
+        desc, n, dim, labels, n_classes, order, T, inv_lambda, W, bias, z_out);
     return launch_status(cudaGetLastError());
 }
 

@@ -65,6 +65,8 @@ def lib():
         L.svm_score.restype = i32
         L.svm_score_l1.argtypes = [P, i32, i32, i32, P, P, i32, P, P, P, f32, P]
         L.svm_score_l1.restype = i32
+        L.svm_train_ovr.argtypes = [P, i32, i32, P, i32, P, ctypes.c_int64, i32, P, P, P, P]
+        L.svm_train_ovr.restype = i32
         L.svm_workspace_bytes.argtypes = [i32, i32]
         L.svm_workspace_bytes.restype = sz
         L.svm_prepare.argtypes = [P, i32, i32, P, sz, P]
@@ -338,3 +340,23 @@ def svm_score_l1(desc: torch.Tensor, W: torch.Tensor, bias: torch.Tensor, block:
     if st != LBP_OK:
         raise LbpError(st, "svm_score_l1")
     return scores, labels, top
+
+
+def svm_train_ovr(desc: torch.Tensor, labels: torch.Tensor, n_classes: int, order: torch.Tensor,
+                  inv_lambda: int, return_z: bool = False, stream=None):
+    """One-vs-rest linear SVM training on the GPU (exact integer Pegasos form): returns
+    (W fp32 [C][dim], bias fp32 [C]) (and z int64 [C][dim+1] when return_z)."""
+    _check_cuda(desc, labels, order)
+    assert desc.dtype == torch.uint16 and desc.is_contiguous()
+    assert labels.dtype == torch.int32 and order.dtype == torch.int32 and order.is_contiguous()
+    n, dim = desc.shape
+    dev = desc.device
+    W = torch.empty((n_classes, dim), dtype=torch.float32, device=dev)
+    b = torch.empty(n_classes, dtype=torch.float32, device=dev)
+    z = torch.empty((n_classes, dim + 1), dtype=torch.int64, device=dev) if return_z else None
+    st = lib().svm_train_ovr(_ptr(desc), n, dim, _ptr(labels), n_classes, _ptr(order),
+                             order.numel(), inv_lambda, _ptr(W), _ptr(b), _ptr(z),
+                             _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "svm_train_ovr")
+    return (W, b, z) if return_z else (W, b)

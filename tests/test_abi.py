@@ -120,6 +120,22 @@ def test_extract_resized_argument_errors(L):
     assert call(geom=big) == lb.LBP_E_UNSUPPORTED
 
 
+def test_svm_train_argument_errors(L):
+    from paper_1504_01883_b200 import lbpfused as lb
+    P = ctypes.c_void_p
+    d = P(0x1000)
+
+    def call(n=4, dim=8, C=2, T=10, inv=100, desc=d):
+        return L.svm_train_ovr(desc, n, dim, d, C, d, T, inv, d, d, None, None)
+    assert call(T=0) == lb.LBP_E_ARG
+    assert call(inv=0) == lb.LBP_E_ARG
+    assert call(n=0) == lb.LBP_E_ARG
+    assert call(C=0) == lb.LBP_E_ARG
+    assert call(desc=None) == lb.LBP_E_ARG
+    assert call(T=(1 << 31) + 1) == lb.LBP_E_ARG
+    assert call(dim=16385) == lb.LBP_E_UNSUPPORTED
+
+
 def test_svm_argument_errors(L):
     from paper_1504_01883_b200 import lbpfused as lb
     P = ctypes.c_void_p
