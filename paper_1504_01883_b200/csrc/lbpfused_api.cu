@@ -317,11 +317,20 @@ int32_t svm_train_ovr(const uint16_t* desc, int32_t n, int32_t dim, const int32_
     if (!desc || !labels || !order || !W || !bias) return LBP_E_ARG;
     if (dim > kTrainMaxDim) return LBP_E_UNSUPPORTED;
     const size_t smem = (size_t)(dim + 1) * sizeof(int64_t);
-    cudaError_t e = cudaFuncSetAttribute(svm_train_ovr_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (dim <= 256 * 16) {  // 59-bin descriptors: 256 threads x 16 entries (cheaper barriers)
+        auto k = svm_train_ovr_kernel<256, 16>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return launch_status(e);
+        k<<<std::min(n_classes, 4 * num_sms()), 256, smem, stream>>>(
+            desc, n, dim, labels, n_classes, order, T, inv_lambda, W, bias, z_out);
+        return launch_status(cudaGetLastError());
+    }
+    auto k = svm_train_ovr_kernel<1024, 16>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return launch_status(e);
-    const int grid = std::min(n_classes, 2 * num_sms());
-    svm_train_ovr_kernel<<<grid, kTrainThreads, smem, (cudaStream_t)stream_>>>(
+    k<<<std::min(n_classes, 2 * num_sms()), 1024, smem, stream>>>(
         desc, n, dim, labels, n_classes, order, T, inv_lambda, W, bias, z_out);
     return launch_status(cudaGetLastError());
 }

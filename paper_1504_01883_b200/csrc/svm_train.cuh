@@ -6,8 +6,8 @@
 //   z_t = z_{t-1} + [violated] y x~;   model w = inv_lambda z_T / T (fp64, then fp32).
 // (z_t = lambda t w_t of Pegasos' w_t = (1 - 1/t) w_{t-1} + [viol] y x~ / (lambda t).)
 //
-// One CTA (1,024 threads) per class; z (int64, dim + 1) lives in shared memory; each thread
-// owns the descriptor entries d = tid + k * 1024 and keeps the current and the next sample's
+// One CTA (NT threads) per class; z (int64, dim + 1) lives in shared memory; each thread
+// owns the descriptor entries d = tid + k * NT and keeps the current and the next sample's
 // counts in registers (the next sample is prefetched while the current step reduces).  A
 // step is an int64 dot product (warp shuffles + one smem pass), one uniform decision and, when
 // violated, an integer update of the thread's z entries.  The step chain of a class is
@@ -17,10 +17,10 @@
 
 namespace lbpf {
 
-constexpr int kTrainThreads = 1024;
-constexpr int kTrainPerThread = 16;  // dim <= 16,384 (8x8 cells x 256 bins)
-constexpr int kTrainMaxDim = kTrainThreads * kTrainPerThread;
+constexpr int kTrainMaxDim = 16384;  // 8x8 cells x 256 bins
 
+// NT threads, PER descriptor entries per thread (dim <= NT * PER)
+template <int kTrainThreads, int kTrainPerThread>
 __global__ void __launch_bounds__(kTrainThreads)
 svm_train_ovr_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
                      const int32_t* __restrict__ labels, int32_t n_classes,
