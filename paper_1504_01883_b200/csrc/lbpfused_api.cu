@@ -11,6 +11,7 @@
 #include "lbp_recognize.cuh"
 #include "svm_fp64.cuh"
 #include "svm_gemm.cuh"
+#include "svm_gemm_i8.cuh"
 #include "svm_train.cuh"
 
 using namespace lbpf;
@@ -33,6 +34,17 @@ int32_t check_geometry(const lbp_images_t& g, bool has_grey, bool has_depth) {
                       g.depth_img_stride < g.depth_pitch * (g.height - 1) + g.width))
         return LBP_E_ARG;
     return LBP_OK;
+}
+
+// Workspace format of svm_prepare for a [C][dim] model: the INT8 digit planes for many classes
+// (more than one fp16 TMEM pass), else the fp16 digit planes.
+bool svm_choose_layout(int32_t C, int32_t dim, lbpf::SvmPrepHeader* h) {
+    if (C > lbpf::kPassClasses && lbpf::svm_layout_i8(C, dim, h)) return true;
+    return lbpf::svm_layout(C, dim, h);
+}
+size_t svm_layout_total(const lbpf::SvmPrepHeader& h) {
+    const size_t elem = h.magic == lbpf::kPrep8Magic ? 1 : 2;
+    return (size_t)h.q_off + (size_t)h.total_rows * h.dim_pad * elem;
 }
 
 int num_sms() {
@@ -249,10 +261,15 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, 
     // Tensor-core path: exact integer digit-plane GEMM (needs svm_prepare()'s workspace);
     // below one 128-crop tile the CUDA-core kernel has the lower latency.
     SvmPrepHeader h;
-    if (prepared && n >= kGemmM && svm_layout(n_classes, dim, &h) &&
+    if (prepared && n >= kGemmM && svm_choose_layout(n_classes, dim, &h) &&
         (reinterpret_cast<uintptr_t>(desc) & 15) == 0) {
-        cudaError_t e = launch_svm_gemm(desc, n, dim, W, bias, h, (const uint8_t*)prepared, scores,
-                                        labels, top_score, reject_threshold, num_sms(), stream);
+        cudaError_t e = h.magic == kPrep8Magic
+                            ? launch_svm_gemm_i8(desc, n, dim, W, bias, h, (const uint8_t*)prepared,
+                                                 scores, labels, top_score, reject_threshold,
+                                                 num_sms(), stream)
+                            : launch_svm_gemm(desc, n, dim, W, bias, h, (const uint8_t*)prepared,
+                                              scores, labels, top_score, reject_threshold,
+                                              num_sms(), stream);
         if (e != cudaErrorNotSupported) return launch_status(e);
     }
     // CUDA-core path: exact fp64 accumulation; 8 crops per CTA, 1 for tiny batches
@@ -337,17 +354,22 @@ int32_t svm_train_ovr(const uint16_t* desc, int32_t n, int32_t dim, const int32_
 
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim) {
     SvmPrepHeader h;
-    if (!svm_layout(n_classes, dim, &h)) return 0;
-    return svm_layout_bytes(h);
+    if (!svm_choose_layout(n_classes, dim, &h)) return 0;
+    return svm_layout_total(h);
 }
 
 int32_t svm_prepare(const float* W, int32_t n_classes, int32_t dim, void* workspace,
                     size_t workspace_bytes, lbp_stream_t stream) {
     if (!W || !workspace || n_classes < 1 || dim < 1) return LBP_E_ARG;
     SvmPrepHeader h;
-    if (!svm_layout(n_classes, dim, &h)) return LBP_E_UNSUPPORTED;
-    if (workspace_bytes < svm_layout_bytes(h)) return LBP_E_ARG;
-    svm_prepare_kernel<<<h.total_rows, 256, 0, (cudaStream_t)stream>>>(W, h, (uint8_t*)workspace);
+    if (!svm_choose_layout(n_classes, dim, &h)) return LBP_E_UNSUPPORTED;
+    if (workspace_bytes < svm_layout_total(h)) return LBP_E_ARG;
+    if (h.magic == kPrep8Magic)
+        svm_prepare_i8_kernel<<<h.total_rows, 256, 0, (cudaStream_t)stream>>>(W, h,
+                                                                             (uint8_t*)workspace);
+    else
+        svm_prepare_kernel<<<h.total_rows, 256, 0, (cudaStream_t)stream>>>(W, h,
+                                                                          (uint8_t*)workspace);
     return launch_status(cudaGetLastError());
 }
 

@@ -307,3 +307,50 @@ def test_svm_single_crop_config1(lb):
         s_ref, lab_ref, _ = oracle.svm_score(desc, W, b)
         assert svm_tolerance_ok(desc, W, b, s, s_ref)[0]
         assert labels_agree_away_from_ties(s_ref, lab, lab_ref, desc, W, b)
+
+
+@pytest.mark.parametrize("kind", ["few_big", "many_big", "plain"])
+def test_svm_gemm_i8_counts_above_255(lb, kind):
+    """C > 124 takes the INT8 digit-plane kernel: counts above 255 enter the GEMM as their low
+    byte and their high part is added exactly (rows with > 8 such entries: fp64)."""
+    rng = np.random.default_rng(11)
+    n, D, C = 300, 3776, 150
+    desc = rng.integers(0, 9, (n, D)).astype(np.uint16)
+    if kind == "few_big":
+        for r in range(0, n, 7):
+            cols = rng.choice(D, 3, replace=False)
+            desc[r, cols] = rng.integers(256, 3000, 3)
+        desc[5, 0], desc[6, D - 1] = 256, 65535
+    elif kind == "many_big":
+        desc[[3, 150, 299], :40] = 300
+    W, b = synthgen.svm_weights(C, D, seed=12)
+    s, lab, top = _gpu_svm(lb, desc, W, b, prepared=True)
+    s_ref, lab_ref, _ = oracle.svm_score(desc, W, b)
+    ok, worst = svm_tolerance_ok(desc, W, b, s, s_ref)
+    assert ok, worst
+    assert labels_agree_away_from_ties(s_ref, lab, lab_ref, desc, W, b)
+
+
+def test_svm_prepare_i8_digit_roundtrip(lb):
+    """INT8 workspace (C > 124): W = m (2 u - 1), u = sum_k d_k 2^-(8(k+1)), |error| <= 2^-40 m."""
+    C, D = 130, 640
+    W, _ = synthgen.svm_weights(C, D, seed=6)
+    W[3] = 0.0
+    W[4, 10] = 2.0
+    ws = lb.svm_prepare(torch.from_numpy(W).to(DEV))
+    torch.cuda.synchronize()
+    raw = ws.cpu().numpy()
+    scale_off, q_off = 1024, (1024 + 4 * C + 1023) // 1024 * 1024
+    m = raw[scale_off:scale_off + 4 * C].view(np.float32).astype(np.float64)
+    npass, dpad = -(-C // 96), 640
+    q = raw[q_off:q_off + npass * 512 * dpad].reshape(npass, 512, dpad).astype(np.float64)
+    nat = np.empty_like(q)
+    for sr in range(512):  # pair-major storage -> natural rows (TMEM columns)
+        cr, within = divmod(sr, 256)
+        nat[:, (within // 128) * 256 + cr * 128 + within % 128] = q[:, sr]
+    for c in range(C):
+        p, j = divmod(c, 96)
+        u = sum(nat[p, k * 96 + j, :D] * 2.0 ** (-8 * (k + 1)) for k in range(5))
+        assert m[c] > np.abs(W[c]).max() and np.log2(m[c]) == np.round(np.log2(m[c]))
+        assert np.abs(m[c] * (2 * u - 1) - W[c].astype(np.float64)).max() <= 2.0 ** -40 * m[c]
+    assert (nat[:, 480, :D] == 1).all() and (nat[:, 480, D:] == 0).all()

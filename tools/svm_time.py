@@ -1,6 +1,7 @@
 """Times the tensor-core SVM scorer alone (svm_score with a prepared workspace, labels + top
 only, as bench.py calls it) with CUDA events on its stream, for the bench workloads.
-Usage: python tools/svm_time.py [n C] ..."""
+Usage: python tools/svm_time.py [n C] ...   (SVM_REAL=1: descriptors of the bench's synthetic
+crops instead of random counts 0..8; SVM_CLAMP=1 additionally clamps counts to 255)"""
 import os
 import sys
 
@@ -15,9 +16,17 @@ dev = torch.device("cuda", 0)
 args = [int(a) for a in sys.argv[1:]] or [16384, 100, 131072, 1000]
 D = 3776
 for n, C in zip(args[0::2], args[1::2]):
-    # counts 0..8: row sums ~15k, like the 126 x 126 interior pixels of a 128 x 128 crop
-    g = torch.Generator(device=dev).manual_seed(0)
-    desc = torch.randint(0, 9, (n, D), dtype=torch.int16, device=dev, generator=g).view(torch.uint16)
+    if os.environ.get("SVM_REAL"):  # real descriptors of the bench's synthetic crops
+        gr, dp = synthgen.gpu_face_crops(n, 128, 128, seed=42, device=dev)
+        desc = lb.lbp_fused_extract(gr, dp, torch.from_numpy(synthgen.full_rois(n, 128, 128)).to(dev),
+                                    600, 1400, 8, 8, 59)
+        del gr, dp
+        if os.environ.get("SVM_CLAMP"):  # counts above 255 clamped (no high-part corrections)
+            desc = desc.view(torch.int16).clamp_(max=255).view(torch.uint16)
+    else:
+        # counts 0..8: row sums ~15k, like the 126 x 126 interior pixels of a 128 x 128 crop
+        g = torch.Generator(device=dev).manual_seed(0)
+        desc = torch.randint(0, 9, (n, D), dtype=torch.int16, device=dev, generator=g).view(torch.uint16)
     W, b = synthgen.svm_weights(C, D, seed=1)
     Wt, bt = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
     ws = lb.svm_prepare(Wt)
