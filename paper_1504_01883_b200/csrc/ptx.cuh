@@ -55,10 +55,6 @@ __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
 }
 
 // fire-and-forget shared-memory increment (SASS: ATOMS.POPC.INC / ATOMS.ADD without return)
-__device__ __forceinline__ void red_shared_inc(uint32_t addr) {
-    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
-}
-
 __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
@@ -70,13 +66,6 @@ __device__ __forceinline__ uint32_t opaque(uint32_t v) {
 }
 
 // predicated variant: no branch, the predicate guards the ATOMS itself
-__device__ __forceinline__ void red_shared_inc_if(uint32_t addr, bool pred) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], 1;\n\t}" ::"r"(addr),
-        "r"((uint32_t)pred)
-        : "memory");
-}
-
 __device__ __forceinline__ void named_barrier_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -179,15 +168,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(bar))
         : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
 }
 // 32 consecutive fp32 columns of this warp's 32 TMEM lanes (asynchronous until
 // tmem_ld_wait_regs names the same registers)
@@ -311,17 +291,6 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
     d |= (uint64_t)2 << 61;             // SWIZZLE_128B
     return d;
 }
-// K-major operand tile with 64-B swizzle (rows of 32 fp16): 8-row atoms of 512 B
-__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t smem_addr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
-    d |= (uint64_t)(16 >> 4) << 16;     // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(512 >> 4) << 32;    // SBO: 8 rows x 64 B
-    d |= (uint64_t)1 << 46;             // version (Blackwell)
-    d |= (uint64_t)4 << 61;             // SWIZZLE_64B
-    return d;
-}
-
 // instruction descriptor, kind::f16: A,B fp16 K-major, D fp32, shape M x N
 __host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
     return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);

@@ -34,13 +34,11 @@
 
 namespace lbpf {
 
-constexpr int kSvmDigits = 4;
 constexpr int kPassClasses = 124;
 constexpr int kGemmM = 128;
 constexpr int kGemmK = 64;                  // K per pipeline stage (fp16 elements)
 constexpr int kRowBytes = kGemmK * 2;       // one swizzled smem row: 128 B (SWIZZLE_128B)
 constexpr int kDimAlign = 64;               // workspace dim padding
-constexpr int kBoxRows = 32;
 constexpr int kGemmThreads = 224;
 constexpr uint32_t kPrepMagic = 0x53564D31u;  // "SVM1"
 
@@ -70,10 +68,6 @@ inline bool svm_layout(int32_t C, int32_t D, SvmPrepHeader* h) {
     h->scale_off = 1024;
     h->q_off = (1024 + 4 * C + 1023) / 1024 * 1024;
     return true;
-}
-
-inline size_t svm_layout_bytes(const SvmPrepHeader& h) {
-    return (size_t)h.q_off + (size_t)h.total_rows * h.dim_pad * 2;
 }
 
 // ---------------------------------------------------------------------------- prepare
@@ -236,7 +230,7 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
             uint32_t ph = 0, acc_ph = 0;
             // 128-B swizzle descriptors differ only in the 14-bit start-address field of the
             // low word: desc(base + off) = desc(base) + off / 16 while the address stays < 256 KB
-            const uint64_t d0 = kGemmK == 64 ? umma_desc_sw128(smem_u32(smem)) : umma_desc_sw64(smem_u32(smem));
+            const uint64_t d0 = umma_desc_sw128(smem_u32(smem));
             const uint32_t d_hi = (uint32_t)(d0 >> 32), d_lo0 = (uint32_t)d0;
             for (int t = pair; t < n_tiles; t += n_pairs_grid) {
                 for (int p = 0; p < h.n_pass; ++p) {
@@ -432,7 +426,7 @@ inline bool encode_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt
     cuuint32_t estr[2] = {1, 1};
     (void)esize;
     return fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, kGemmK == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
