@@ -1,0 +1,38 @@
+"""Small invocations of every kernel of the library in one process (a fault smoke test; also
+the input for compute-sanitizer where it is available -- it is not on this GPU pool)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1504_01883_b200 as lb
+import synthgen
+
+dev = torch.device("cuda", 0)
+g, d = synthgen.gpu_face_crops(150, 128, 128, seed=1, device=dev)
+r = torch.from_numpy(synthgen.full_rois(150, 128, 128)).to(dev)
+desc = lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 59)            # lane59 (TMA)
+lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 256)                   # fast v3 (256 bins)
+lb.lbp_fused_extract(g, None, r, 0, 0, 8, 8, 59)                      # lane59, no depth
+lb.lbp_extract_source(g, d, r, 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)  # + depth source
+lb.lbp_fused_extract(g, d, r[:8].contiguous(), 600, 1400, 8, 8, 59)   # band kernel
+gf, df, rf = synthgen.kinect_frames(2, seed=2)
+gf, dft = torch.from_numpy(gf).to(dev), torch.from_numpy(df.view(np.int16)).to(dev).view(torch.uint16)
+rf = torch.from_numpy(rf).to(dev)
+lb.lbp_extract_resized(gf, dft, rf, 200, 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)
+for C in (10, 130):
+    W, b = synthgen.svm_weights(C, 3776, seed=C)
+    Wt, bt = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+    ws = lb.svm_prepare(Wt)
+    lb.svm_score(desc, Wt, bt, prepared=ws)                             # tcgen05 fp16 / INT8
+    lb.svm_score(desc[:5].contiguous(), Wt, bt)                         # fp64, tiny batch
+    lb.svm_score(desc[:40].contiguous(), Wt, bt)                        # fp64, staged
+    lb.lbp_recognize(gf, dft, rf, 600, 1400, 8, 8, 59, Wt, bt)          # fused cluster kernel
+    lb.svm_score_l1(desc, Wt, bt, 59)
+    labels = (torch.arange(150, device=dev) % C).to(torch.int32)
+    order = torch.from_numpy(synthgen.train_order(150, 1, seed=3)).to(dev)
+    lb.svm_train_ovr(desc, labels, C, order[:60].contiguous(), 100)
+torch.cuda.synchronize()
+print("sanitize_small: done")
