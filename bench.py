@@ -527,6 +527,22 @@ def run_latency(args):
         z.record(stream)
         torch.cuda.synchronize()
     per_call_graph = a.elapsed_time(z) / reps / n_calls
+    # batched: every call's ROIs in one extraction + one scoring launch (a frame buffer
+    # processed as a batch; >= 148 ROIs take the persistent TMA kernel)
+    def batched():
+        lb.lbp_fused_extract(grey, depth, rois, DMIN, DMAX, cx, cy, bins, out=desc, stream=stream)
+        lb.svm_score(desc, W, b, prepared=prepared, want_scores=False, labels=labels,
+                     top_score=top, stream=stream)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            batched()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            batched()
+        z.record(stream)
+        torch.cuda.synchronize()
+    per_batch = a.elapsed_time(z) / reps
     line = {
         "metric": METRIC, "value": n_per / (per_call_graph * 1e-3), "unit": UNIT, "n_gpus": 1,
         "steps": reps * n_calls, "warmup": 8, "ms_per_step": per_call_graph,
@@ -538,6 +554,8 @@ def run_latency(args):
         "latency_us": {"eager_p50": float(np.percentile(lat, 50) * 1e3),
                        "eager_p99": float(np.percentile(lat, 99) * 1e3),
                        "graph_per_call": per_call_graph * 1e3},
+        "batched": {"calls": n_calls, "crops": n_calls * n_per, "us_per_batch": per_batch * 1e3,
+                    "crops_per_s": n_calls * n_per / (per_batch * 1e-3)},
         "frame_h2d_bytes": frame_bytes, "gpu_launches": (1 if fused else 2) * n_calls * reps,
         "api": "lbp_recognize (fused)" if fused else "lbp_fused_extract/lbp_extract_resized + "
                "svm_score", "clocks": clk.summary(),

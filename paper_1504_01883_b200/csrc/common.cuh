@@ -105,5 +105,11 @@ __device__ __forceinline__ bool roi_is_fast(const lbp_roi_t& r, const lbp_images
            (r.x & 15) == 0 &&
            r.y >= 0 && (int64_t)r.x + kFastTile <= g.width && (int64_t)r.y + kFastTile <= g.height;
 }
+// Same for the frame variant of the lane-private kernel, which stages a wider box at the
+// aligned-down column and takes any x.
+__device__ __forceinline__ bool roi_is_fast_frame(const lbp_roi_t& r, const lbp_images_t& g) {
+    return r.w == kFastTile && r.h == kFastTile && r.img >= 0 && r.img < g.n_images && r.x >= 0 &&
+           r.y >= 0 && (int64_t)r.x + kFastTile <= g.width && (int64_t)r.y + kFastTile <= g.height;
+}
 
 }  // namespace lbpf

@@ -324,12 +324,13 @@ inline PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 inline bool encode_stack_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int elem,
-                             const lbp_images_t& g, int64_t pitch, int64_t img_stride) {
+                             const lbp_images_t& g, int64_t pitch, int64_t img_stride,
+                             int box_w = kFastTile) {
     auto fn = get_encode_fn();
     if (!fn) return false;
     cuuint64_t dims[3] = {(cuuint64_t)g.width, (cuuint64_t)g.height, (cuuint64_t)g.n_images};
     cuuint64_t strides[2] = {(cuuint64_t)(pitch * elem), (cuuint64_t)(img_stride * elem)};
-    cuuint32_t box[3] = {kFastTile, kFastTile, 1};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, kFastTile, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

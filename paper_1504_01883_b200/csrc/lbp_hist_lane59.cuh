@@ -37,22 +37,50 @@ constexpr int kTile = 128;
 constexpr int kBins = 59;
 constexpr int kBinsAlloc = 60;  // + a dummy bin row that counts the masked-out pixels
 constexpr int kStages = 3;
-constexpr int kGreyBytes = kTile * kTile;                      // 16,384
-constexpr int kStageBytes = kGreyBytes + 2 * kTile * kTile;    // + depth 32,768 = 49,152
 constexpr int kHistBytes = 2 * kBinsAlloc * 32 * 4;            // [g][bin][lane] = 15,360
 constexpr int kDescBytes = 64 * kBins * 2;                     // 7,552
-constexpr int kGroupOff = kStages * kStageBytes;               // 147,456
-constexpr int kGroupBytes = (kHistBytes + kDescBytes + 255) / 256 * 256;  // 23,040
-constexpr int kLutOff = kGroupOff + kGroups * kGroupBytes;     // 216,576 (256-aligned)
+constexpr int kGroupBytes = (kHistBytes + kDescBytes + 255) / 256 * 256;  // 23,040 (+ staging)
 constexpr int kLutBytes = 65 * 128;  // 64 lane-banked rows + the dummy row (bin 59 everywhere)
 constexpr uint32_t kDummyOff2 = 0x84008400u;  // LUT offset of the dummy row, both halves
-constexpr int kPlainLutOff = kLutOff + kLutBytes;
-constexpr int kBarOff = kPlainLutOff + 256;
-constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;        // + 128-B alignment slack
-static_assert(kGroupBytes % 128 == 0 && kLutOff % 256 == 0, "alignment");
-static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 static_assert(kStages >= kGroups, "every group needs a stage");
+
+// Stage layout of the two variants.  FRAME (ROIs at any column of wider frames): the grey
+// box is 144 px wide at x & ~15 and the depth box 136 px at x & ~7 (TMA needs 16-B aligned
+// box starts), so each lane's 4 columns start og = x & 15 bytes (grey) / od = x & 7 pixels
+// (depth) into the staged row; the 7,552-B descriptor staging then lives inside the group's
+// own stage (stage == group since kStages == kGroups) to stay within shared memory.
+template <bool FRAME>
+struct Layout {
+    static constexpr int kGreyW = FRAME ? 144 : kTile;   // grey row bytes in a stage
+    static constexpr int kDepthW = FRAME ? 136 : kTile;  // depth row pixels in a stage
+    static constexpr int kGreyBytes = kGreyW * kTile;
+    static constexpr int kStageBytes = kGreyBytes + 2 * kDepthW * kTile;
+    static constexpr int kGroupOff = kStages * kStageBytes;
+    static constexpr int kGroupBytes = FRAME ? kHistBytes : l59::kGroupBytes;
+    static constexpr int kLutOff = kGroupOff + kGroups * kGroupBytes;
+    static constexpr int kPlainLutOff = kLutOff + kLutBytes;
+    static constexpr int kBarOff = kPlainLutOff + 256;
+    static constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;  // + 128-B alignment slack
+    // headline: stages 3 x 49,152, groups 3 x 23,040 (counters + staging), LUT at 216,576;
+    // FRAME: stages 3 x 53,248, groups 3 x 15,360, LUT at 205,824
+    static_assert(kStageBytes % 128 == 0 && kGreyBytes % 128 == 0 && kLutOff % 256 == 0,
+                  "alignment");
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory");
+    static_assert(!FRAME || kStages == kGroups, "frame staging lives in the group's stage");
+    static_assert(kDescBytes <= kGreyBytes, "staging fits a stage region");
+};
 }  // namespace l59
+
+// 4 bytes starting s = sel-encoded bytes into the word pair at addr (funnel shift by PRMT)
+__device__ __forceinline__ uint32_t ld_shared_funnel1(uint32_t addr, uint32_t sel) {
+    return prmt(ld_shared_u32(addr), ld_shared_u32(addr + 4), sel);
+}
+// 8 bytes starting 0 or 2 bytes into the three words at addr (sel 0x3210 / 0x5432)
+__device__ __forceinline__ uint2 ld_shared_funnel2(uint32_t addr, uint32_t sel) {
+    const uint32_t w0 = ld_shared_u32(addr), w1 = ld_shared_u32(addr + 4),
+                   w2 = ld_shared_u32(addr + 8);
+    return make_uint2(prmt(w0, w1, sel), prmt(w1, w2, sel));
+}
 
 __device__ __forceinline__ void bulk_store_s2g(void* gdst, uint32_t ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
@@ -82,8 +110,7 @@ struct LaneRow {
     uint32_t lh0, mh, rh1;  // (4l-1, 4l), (4l+1, 4l+2), (4l+3, 4l+4)
 };
 
-__device__ __forceinline__ LaneRow lane_row(uint32_t word_addr) {
-    const uint32_t w = ld_shared_u32(word_addr);
+__device__ __forceinline__ LaneRow lane_row_w(uint32_t w) {
     LaneRow r;
     r.h0 = prmt(w, 0x64646464u, 0x5140);
     r.h1 = prmt(w, 0x64646464u, 0x7362);
@@ -93,6 +120,9 @@ __device__ __forceinline__ LaneRow lane_row(uint32_t word_addr) {
     r.mh = prmt(r.h0, r.h1, 0x5432);
     r.rh1 = prmt(r.h1, right, 0x5432);
     return r;
+}
+__device__ __forceinline__ LaneRow lane_row(uint32_t word_addr) {
+    return lane_row_w(ld_shared_u32(word_addr));
 }
 
 // Eq. 2 for the centre pair c as the lane-banked LUT offset, per 16-bit half:
@@ -133,8 +163,7 @@ __device__ __forceinline__ uint32_t vmin_u16x2(uint32_t a, uint32_t b) {
     return __vminu2(a, b);  // VIMNMX.U16x2
 }
 
-__device__ __forceinline__ DepthRow depth_row(uint32_t addr) {
-    const uint2 w = ld_shared_u32x2(addr);
+__device__ __forceinline__ DepthRow depth_row_w(uint2 w) {
     DepthRow r;
     r.raw0 = w.x;
     r.raw1 = w.y;
@@ -146,6 +175,9 @@ __device__ __forceinline__ DepthRow depth_row(uint32_t addr) {
     r.mh = prmt(r.h0, r.h1, 0x5432);
     r.rh1 = prmt(r.h1, right, 0x5432);
     return r;
+}
+__device__ __forceinline__ DepthRow depth_row(uint32_t addr) {
+    return depth_row_w(ld_shared_u32x2(addr));
 }
 
 __device__ __forceinline__ uint32_t hle2_mask(uint32_t a, uint32_t b) {
@@ -177,7 +209,7 @@ __device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uin
     return f + a;
 }
 
-template <bool HAS_DEPTH, bool DEPTH_SRC, bool FP16WIN>
+template <bool HAS_DEPTH, bool DEPTH_SRC, bool FP16WIN, bool FRAME>
 __global__ void __launch_bounds__(l59::kThreads, 1)
 lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const __grid_constant__ CUtensorMap depth_map,
@@ -186,6 +218,16 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        DepthWindow win, uint16_t* __restrict__ desc, int64_t desc_stride,
                        int32_t* __restrict__ roi_status) {
     using namespace l59;
+    using L = Layout<FRAME>;
+    constexpr int kGreyBytes = L::kGreyBytes, kStageBytes = L::kStageBytes;
+    constexpr int kGroupOff = L::kGroupOff, kGroupBytes = L::kGroupBytes;
+    constexpr int kLutOff = L::kLutOff, kPlainLutOff = L::kPlainLutOff, kBarOff = L::kBarOff;
+    // FRAME with grey codes and a depth mask: the staging overwrites the stage's grey rows, so
+    // the next grey box is loaded only once the descriptor store has read the staging (the
+    // depth box goes first); without depth it uses the unused depth region, for the depth
+    // source the unused grey region.
+    constexpr bool kLateGrey = FRAME && HAS_DEPTH && !DEPTH_SRC;
+    constexpr uint32_t kStagingOff = (FRAME && !HAS_DEPTH) ? kGreyBytes : 0;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
                                                ~uintptr_t(127));
@@ -194,7 +236,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const int warp = gtid >> 5, lane = gtid & 31;
     const uint32_t stages0 = smem_u32(smem);
     const uint32_t hist0 = stages0 + kGroupOff + group * kGroupBytes;
-    const uint32_t staging = hist0 + kHistBytes;
+    const uint32_t staging = FRAME ? stages0 + group * kStageBytes + kStagingOff
+                                   : hist0 + kHistBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     const uint32_t bar_id = 1 + group;
 
@@ -203,17 +246,26 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     auto crop_of = [&](int i) -> int32_t { return (int32_t)blockIdx.x + i * (int32_t)gridDim.x; };
     // fill position i into stage i % 3: TMA for fast crops, a plain arrive otherwise (keeps the
     // stage barrier's phase count in step with the positions)
-    auto issue = [&](int i) {
+    auto is_fast = [&](const lbp_roi_t& r) {
+        return FRAME ? roi_is_fast_frame(r, geom) : roi_is_fast(r, geom);
+    };
+    // part bit 1: arrive (+ expect the stage's bytes) and load all but a late grey box;
+    // part bit 2: the late grey box (kLateGrey)
+    auto issue = [&](int i, int part) {
         if (i >= n_pos) return;
         const int s = i % kStages;
         const lbp_roi_t r = rois[crop_of(i)];
-        if (roi_is_fast(r, geom)) {
-            mbar_arrive_expect_tx(&bars[s], DEPTH_SRC ? kStageBytes - kGreyBytes
-                                                      : HAS_DEPTH ? kStageBytes : kGreyBytes);
+        if (is_fast(r)) {
             uint8_t* st = smem + s * kStageBytes;
-            if (!DEPTH_SRC) tma_load_3d(st, &grey_map, &bars[s], r.x, r.y, r.img);
-            if (HAS_DEPTH) tma_load_3d(st + kGreyBytes, &depth_map, &bars[s], r.x, r.y, r.img);
-        } else {
+            const int gx = FRAME ? (r.x & ~15) : r.x, dx = FRAME ? (r.x & ~7) : r.x;
+            if (part & 1) {
+                mbar_arrive_expect_tx(&bars[s], DEPTH_SRC ? kStageBytes - kGreyBytes
+                                                          : HAS_DEPTH ? kStageBytes : kGreyBytes);
+                if (HAS_DEPTH) tma_load_3d(st + kGreyBytes, &depth_map, &bars[s], dx, r.y, r.img);
+            }
+            if (!DEPTH_SRC && (part & (kLateGrey ? 2 : 1)))
+                tma_load_3d(st, &grey_map, &bars[s], gx, r.y, r.img);
+        } else if (part & 1) {
             mbar_arrive(&bars[s]);
         }
     };
@@ -231,7 +283,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         fence_mbar_init();
         prefetch_tensormap(&grey_map);
         if (HAS_DEPTH) prefetch_tensormap(&depth_map);
-        for (int i = 0; i < kStages; ++i) issue(i);
+        for (int i = 0; i < kStages; ++i) issue(i, 3);
     }
     __syncthreads();
 
@@ -268,8 +320,11 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const lbp_roi_t roi = rois[n];
         const int s = i % kStages;
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
-        if (!roi_is_fast(roi, geom)) {
-            if (gtid == 0) issue(i + kStages);  // stage s was never filled: release it at once
+        if (!is_fast(roi)) {
+            if (gtid == 0) {  // stage s was never filled: release it at once
+                if (FRAME) bulk_wait_read_all();  // (the staging may live in the stage)
+                issue(i + kStages, 3);
+            }
             if (DEPTH_SRC)
                 extract_roi_generic<kBins, kGroupThreads>(
                     CodePlane<uint16_t>{depth, geom.depth_pitch, geom.depth_img_stride}, depth, geom,
@@ -286,13 +341,24 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             continue;
         }
         const uint32_t st = stages0 + s * kStageBytes;
-        // code plane rows: grey u8 (128 B per row) or depth u16 (256 B per row, DEPTH_SRC)
-        constexpr uint32_t kRowStep = DEPTH_SRC ? kTile * 2 : kTile;
-        const uint32_t g0 = DEPTH_SRC ? opaque(st + kGreyBytes + i0 * (kTile * 2) + 8 * lane)
-                                      : opaque(st + i0 * kTile + 4 * lane);
-        const uint32_t d0 = opaque(st + kGreyBytes + (i0 + 1) * (kTile * 2) + 8 * lane);
+        // code plane rows: grey u8 (kGreyW B per row) or depth u16 (2 kDepthW B, DEPTH_SRC).
+        // FRAME: the lane's bytes start og (grey) / 2 od (depth) bytes past its aligned words.
+        constexpr uint32_t kDRow = 2 * L::kDepthW;
+        constexpr uint32_t kRowStep = DEPTH_SRC ? kDRow : L::kGreyW;
+        const uint32_t og = FRAME ? (uint32_t)roi.x & 15u : 0u;
+        const uint32_t od2 = FRAME ? 2u * ((uint32_t)roi.x & 7u) : 0u;
+        const uint32_t gsel = 0x3210u + (og & 3u) * 0x1111u;    // funnel by og & 3 bytes
+        const uint32_t dsel = (od2 & 2u) ? 0x5432u : 0x3210u;  // funnel by 0 / 2 bytes
+        const uint32_t g0 = DEPTH_SRC ? opaque(st + kGreyBytes + i0 * kDRow + 8 * lane + (od2 & ~3u))
+                                      : opaque(st + i0 * L::kGreyW + 4 * lane + (og & ~3u));
+        const uint32_t d0 = opaque(st + kGreyBytes + (i0 + 1) * kDRow + 8 * lane + (od2 & ~3u));
+        auto load_depth = [&](uint32_t addr) {
+            if constexpr (FRAME) return ld_shared_funnel2(addr, dsel);
+            else return ld_shared_u32x2(addr);
+        };
         auto load_row = [&](uint32_t addr) {
-            if constexpr (DEPTH_SRC) return depth_row(addr);
+            if constexpr (DEPTH_SRC) return depth_row_w(load_depth(addr));
+            else if constexpr (FRAME) return lane_row_w(ld_shared_funnel1(addr, gsel));
             else return lane_row(addr);
         };
         using Row = decltype(load_row(0u));
@@ -320,7 +386,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                     c0 = mid.h0;
                     c1 = mid.h1;
                 } else {
-                    const uint2 d = ld_shared_u32x2(d0 + j * (kTile * 2));
+                    const uint2 d = load_depth(d0 + j * kDRow);
                     c0 = vmin_u16x2(d.x, 0x7BFF7BFFu);
                     c1 = vmin_u16x2(d.y, 0x7BFF7BFFu);
                 }
@@ -333,7 +399,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             } else if (HAS_DEPTH) {
                 uint2 d;
                 if constexpr (DEPTH_SRC) d = make_uint2(mid.raw0, mid.raw1);  // centre row
-                else d = ld_shared_u32x2(d0 + j * (kTile * 2));
+                else d = load_depth(d0 + j * kDRow);
                 // depth window on a u16 in either half of a word
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
@@ -372,7 +438,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (gtid == 0) bulk_wait_read_all();        // previous descriptor left the staging
         named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
         if (gtid == 0) {
-            issue(i + kStages);
+            issue(i + kStages, 1);
             if (roi_status) roi_status[n] = LBP_OK;
         }
         // ---- epilogue: quad q = (g, bin, cx) holds the 4 lane columns of cells (4g + j, cx),
@@ -402,7 +468,15 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         fence_proxy_async_smem();                   // staging writes -> async proxy
         named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-        if (gtid == 0) bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
+        if (gtid == 0) {
+            bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
+            if (kLateGrey) {  // the grey box overwrites the staging: wait for the store's read
+                bulk_wait_read_all();
+                issue(i + kStages, 2);
+            } else if (FRAME) {
+                issue(i + kStages, 2);  // (no-op: nothing is late)
+            }
+        }
         pending = n;
     }
     if (gtid == 0 && pending >= 0) bulk_wait_all();
@@ -412,15 +486,17 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
                                           const lbp_images_t& geom, const lbp_roi_t* rois,
                                           int32_t n_rois, const DepthWindow& win, uint16_t* desc,
                                           int64_t desc_stride, int32_t* roi_status, int sms,
-                                          cudaStream_t stream, bool depth_source = false) {
+                                          cudaStream_t stream, bool depth_source = false,
+                                          bool frame = false) {
     CUtensorMap gm, dm;
     if (!depth_source &&
         !encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
-                          geom.grey_img_stride))
+                          geom.grey_img_stride, frame ? l59::Layout<true>::kGreyW : kFastTile))
         return cudaErrorNotSupported;
     if (depth) {
         if (!encode_stack_map(&dm, depth, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, geom,
-                              geom.depth_pitch, geom.depth_img_stride))
+                              geom.depth_pitch, geom.depth_img_stride,
+                              frame ? l59::Layout<true>::kDepthW : kFastTile))
             return cudaErrorNotSupported;
     } else {
         dm = gm;
@@ -428,16 +504,20 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     if (depth_source) gm = dm;  // grey is not read
     // depth window as fp16 compares whenever dmax <= 0x7BFE (always for the depth source)
     const bool fp16win = depth && !win.none_valid && win.lo + win.span <= 0x7BFEu;
-    auto kern = depth_source ? lbp_hist_lane59_kernel<true, true, true>
-                : depth      ? (fp16win ? lbp_hist_lane59_kernel<true, false, true>
-                                        : lbp_hist_lane59_kernel<true, false, false>)
-                             : lbp_hist_lane59_kernel<false, false, false>;
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l59::kSmemBytes);
+    auto pick = [&](auto frame_tag) {
+        constexpr bool F = decltype(frame_tag)::value;
+        return depth_source ? lbp_hist_lane59_kernel<true, true, true, F>
+               : depth      ? (fp16win ? lbp_hist_lane59_kernel<true, false, true, F>
+                                       : lbp_hist_lane59_kernel<true, false, false, F>)
+                            : lbp_hist_lane59_kernel<false, false, false, F>;
+    };
+    auto kern = frame ? pick(std::true_type{}) : pick(std::false_type{});
+    const int smem = frame ? l59::Layout<true>::kSmemBytes : l59::Layout<false>::kSmemBytes;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(sms, n_rois));
-    kern<<<grid, l59::kThreads, l59::kSmemBytes, stream>>>(gm, dm, grey, depth, geom, rois, n_rois,
-                                                          win, desc, desc_stride, roi_status);
+    kern<<<grid, l59::kThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win,
+                                                 desc, desc_stride, roi_status);
     return cudaGetLastError();
 }
 

@@ -91,6 +91,10 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
     // Small batches (the frame-stream and single-crop configs): the band kernel spreads every
     // ROI over cells_y CTAs; the persistent TMA kernel would give each ROI one 8-warp group.
     const bool small_batch = n_rois < num_sms();
+    // Frames wider than a crop: the FRAME variant of the lane-private kernel stages a wider
+    // box so that 128x128 ROIs at any column take the TMA path (crop stacks keep the
+    // 128-wide boxes).
+    const bool frame = geom.width >= l59::Layout<true>::kGreyW;
     if (!depth_source && !small_batch) {
         // Fast path (8x8 cells, 16-B aligned rows): one TMA-staged persistent kernel; ROIs
         // that are not fully-inside 128x128 boxes take the generic code path inside it.
@@ -99,7 +103,7 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
             if (bins == 59)  // conflict-free lane-private kernel (the headline configuration)
                 return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win,
                                                             desc, desc_stride, roi_status,
-                                                            num_sms(), stream));
+                                                            num_sms(), stream, false, frame));
             return launch_status(launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins,
                                                       desc, desc_stride, roi_status, num_sms(),
                                                       stream));
@@ -113,7 +117,7 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
         ((desc_stride * 2) & 15) == 0)
         return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win, desc,
                                                     desc_stride, roi_status, num_sms(), stream,
-                                                    true));
+                                                    true, frame));
     // one CTA per (ROI, cell row) unit, grid-strided
     const int grid = (int)std::min<int64_t>((int64_t)n_rois * cells_y, (int64_t)num_sms() * 8);
     if (depth_source) {
