@@ -55,6 +55,10 @@ def lib():
         L.oracle_lbp_extract_src.argtypes = [P, P, i32, i32, i32, i64, i64, i64, i64, P, i32,
                                              u16, u16, i32, i32, i32, i32, P, P]
         L.oracle_lbp_extract_src.restype = i32
+        L.oracle_desc_pack_u8.argtypes = [P, i64, i32, i64, P, P, P, P, i32, P]
+        L.oracle_desc_pack_u8.restype = i32
+        L.oracle_desc_unpack_u8.argtypes = [P, i64, i32, i64, P, P, P, i32, P]
+        L.oracle_desc_unpack_u8.restype = i32
         L.oracle_resize_grey.argtypes = [P, i32, i32, i64, i32, i32, P]
         L.oracle_resize_grey.restype = i32
         L.oracle_resize_depth.argtypes = [P, i32, i32, i64, i32, i32, P]
@@ -238,3 +242,40 @@ def svm_train_ovr(desc: np.ndarray, labels: np.ndarray, n_classes: int, order: n
     if st != ORC_OK:
         raise ValueError(f"oracle_svm_train_ovr status {st}")
     return (W, b, z) if return_z else (W, b)
+
+
+def desc_pack_u8(desc: np.ndarray, row_base: int = 0, cap: int | None = None):
+    """Descriptor compaction (R21): (packed u8 [n][dim], exceptions int64 [k][3] of
+    (row, index, value) in row-major order, total exception count)."""
+    desc = np.ascontiguousarray(desc, dtype=np.uint16)
+    n, dim = desc.shape
+    if cap is None:
+        cap = int(np.count_nonzero(desc > 255))
+    packed = np.zeros((n, dim), np.uint8)
+    rows = np.zeros(max(cap, 1), np.int64)
+    idx = np.zeros(max(cap, 1), np.int32)
+    val = np.zeros(max(cap, 1), np.int32)
+    cnt = np.zeros(1, np.int32)
+    st = lib().oracle_desc_pack_u8(_ptr(desc), n, dim, row_base, _ptr(packed), _ptr(rows),
+                                   _ptr(idx), _ptr(val), cap, _ptr(cnt))
+    if st != ORC_OK:
+        raise ValueError(f"oracle_desc_pack_u8 status {st}")
+    k = min(int(cnt[0]), cap)
+    exc = np.stack([rows[:k], idx[:k].astype(np.int64), val[:k].astype(np.int64)], 1)
+    return packed, exc, int(cnt[0])
+
+
+def desc_unpack_u8(packed: np.ndarray, exc: np.ndarray, row_base: int = 0) -> np.ndarray:
+    """Inverse of desc_pack_u8: u16 [n][dim] from the packed rows and (row, index, value)."""
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    n, dim = packed.shape
+    exc = np.asarray(exc, np.int64).reshape(-1, 3)
+    rows = np.ascontiguousarray(exc[:, 0])
+    idx = np.ascontiguousarray(exc[:, 1], dtype=np.int32)
+    val = np.ascontiguousarray(exc[:, 2], dtype=np.int32)
+    out = np.zeros((n, dim), np.uint16)
+    st = lib().oracle_desc_unpack_u8(_ptr(packed), n, dim, row_base, _ptr(rows), _ptr(idx),
+                                     _ptr(val), len(exc), _ptr(out))
+    if st != ORC_OK:
+        raise ValueError(f"oracle_desc_unpack_u8 status {st}")
+    return out

@@ -539,3 +539,51 @@ int32_t oracle_svm_score(const uint16_t* desc, int32_t n, int32_t dim,
     }
     return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Descriptor compaction for the database all-gather ("pack   */
+/* counts (u8 + overflow flag) to halve all-gather bytes"; R21).  */
+/* An encoding, written as its definition:                                  */
+/*   packed[i][d] = min(h[i][d], 255)                                       */
+/*   exceptions   = { (row_base + i, d, h[i][d]) : h[i][d] > 255 }, listed   */
+/*                  in row-major order; *count = their number (entries past */
+/*                  cap are counted but not stored).                        */
+/* Decoding: h[r][d] = packed[r][d], then h[row][index] = value for every   */
+/* listed exception.  Pins: decode(encode(h)) == h on random and edge data  */
+/* (tests/test_oracle_compact.py), packed == the saturated counts.          */
+/* ------------------------------------------------------------------------ */
+int32_t oracle_desc_pack_u8(const uint16_t* desc, int64_t n, int32_t dim, int64_t row_base,
+                            uint8_t* packed, int64_t* exc_row, int32_t* exc_index,
+                            int32_t* exc_value, int32_t cap, int32_t* count) {
+    if (n < 0 || dim < 1 || cap < 0 || !count) return ORC_E_ARG;
+    int32_t c = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int32_t d = 0; d < dim; ++d) {
+            uint16_t h = desc[i * dim + d];
+            packed[i * dim + d] = (uint8_t)(h > 255 ? 255 : h);
+            if (h > 255) {
+                if (c < cap) {
+                    exc_row[c] = row_base + i;
+                    exc_index[c] = d;
+                    exc_value[c] = h;
+                }
+                ++c;
+            }
+        }
+    }
+    *count = c;
+    return ORC_OK;
+}
+
+int32_t oracle_desc_unpack_u8(const uint8_t* packed, int64_t n, int32_t dim, int64_t row_base,
+                              const int64_t* exc_row, const int32_t* exc_index,
+                              const int32_t* exc_value, int32_t n_exc, uint16_t* desc) {
+    if (n < 0 || dim < 1 || n_exc < 0) return ORC_E_ARG;
+    for (int64_t i = 0; i < n * (int64_t)dim; ++i) desc[i] = packed[i];
+    for (int32_t k = 0; k < n_exc; ++k) {
+        int64_t r = exc_row[k] - row_base;
+        if (r < 0 || r >= n || exc_index[k] < 0 || exc_index[k] >= dim) continue;
+        desc[r * dim + exc_index[k]] = (uint16_t)exc_value[k];
+    }
+    return ORC_OK;
+}
