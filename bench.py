@@ -100,6 +100,9 @@ def parse():
                         "lbp_fused_extract + svm_score (two launches)")
     p.add_argument("--chunks", type=int, default=4,
                    help="config5: extraction/all-gather overlap chunks (1 = serial)")
+    p.add_argument("--compact", action="store_true",
+                   help="config5: all-gather u8 descriptors + exception lists (serial; "
+                        "lbp_desc_pack_u8 / lbp_desc_unpack_u8), and time pack/unpack")
     return p.parse_args()
 
 
@@ -595,6 +598,7 @@ def run_dbbuild(args):
     import paper_1504_01883_b200 as lb
     import synthgen
     from paper_1504_01883_b200.parallel import (gather_database, gather_database_chunked,
+                                                gather_database_compact,
                                                 shard_range)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -621,6 +625,8 @@ def run_dbbuild(args):
     stream = torch.cuda.current_stream(dev)
 
     comm = torch.cuda.Stream(dev)
+    if args.compact:
+        args.chunks = 1  # the compact exchange is serial: extract, pack, all-gather, unpack
 
     def extract_chunk(lo, hi):
         lb.lbp_fused_extract(grey, depth, rois[lo:hi], DMIN, DMAX, cx, cy, bins,
@@ -635,7 +641,10 @@ def run_dbbuild(args):
                                  stream=stream)
             if ev is not None:
                 ev[1].record(stream)
-            full, lab = gather_database(desc, labels, n_total)
+            if args.compact:
+                full, lab = gather_database_compact(desc, labels, n_total)
+            else:
+                full, lab = gather_database(desc, labels, n_total)
         else:  # chunked: chunk k's all-gather overlaps chunk k+1's extraction
             if ev is not None:
                 ev[1].record(stream)
@@ -663,7 +672,31 @@ def run_dbbuild(args):
     t = torch.tensor([tot, ext, gat], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot, ext, gat = (float(v) for v in t)
-    gathered = n_total * dim * 2 + n_total * 4
+    gathered = n_total * dim * (1 if args.compact else 2) + n_total * 4
+    compact = None
+    if args.compact:  # the pack / unpack kernels alone on this rank's shard (HBM-bound)
+        packed, exc, cnt = lb.desc_pack_u8(desc, row_base=first, cap=4096)
+        out16 = torch.empty_like(desc)
+        reps = 10
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        torch.cuda.synchronize()
+        e[0].record(stream)
+        for _ in range(reps):
+            lb.desc_pack_u8(desc, row_base=first, cap=4096, packed=packed, exc=exc, count=cnt)
+        e[1].record(stream)
+        for _ in range(reps):
+            lb.desc_unpack_u8(packed, exc, cnt, 4096, row_base=first, out=out16)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        pk, up = e[0].elapsed_time(e[1]) / reps, e[1].elapsed_time(e[2]) / reps
+        entries = count * dim
+        compact = {"pack_ms": pk, "unpack_ms": up, "exceptions": int(cnt.item()),
+                   "pack_GBps": 3 * entries / (pk * 1e-3) / 1e9,
+                   "unpack_GBps": 3 * entries / (up * 1e-3) / 1e9,
+                   "roundtrip_exact": bool(torch.equal(out16.view(torch.int16),
+                                                       desc.view(torch.int16))),
+                   "note": "bytes per entry: pack 2 read + 1 written, unpack 1 + 2; the "
+                           "all-gather moves 1 B per entry + 16 B per exception"}
     if args.chunks > 1:  # phases overlap: no separate phase times; bound both by the step
         ext = gat = tot
     peak, peak_src = load_peaks()
@@ -682,6 +715,7 @@ def run_dbbuild(args):
             "allgather_ms": gat if args.chunks <= 1 else None,
             "overlap": {"chunks": args.chunks, "note": "chunk k's all-gather on a second stream "
                         "overlaps chunk k+1's extraction" if args.chunks > 1 else "serial"},
+            "compact": compact,
             "allgather": {"bytes_out_per_rank": gathered,
                           "algbw_GBps": gathered / (gat * 1e-3) / 1e9 if gat > 0 else None,
                           "busbw_GBps": gathered * (world - 1) / world / (gat * 1e-3) / 1e9
@@ -691,7 +725,9 @@ def run_dbbuild(args):
                          "unit": "GB/s", "frac": bpc * count / (ext * 1e-3) / 1e9 / peak,
                          "peak_source": peak_src, "traffic": None},
             "cpu_baseline": None, "e2e": None,
-            "gpu_launches": args.steps * max(1, args.chunks), "clocks": clk.summary(),
+            "gpu_launches": args.steps * (max(1, args.chunks) +
+                                            (3 if args.compact and world > 1 else 0)),
+            "clocks": clk.summary(),
             "check": {"rows": int(full.shape[0]), "label_ok": bool(
                 (lab.cpu() == (torch.arange(n_total) % N_IDS).to(torch.int32)).all())},
         }

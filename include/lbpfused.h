@@ -203,6 +203,46 @@ int32_t svm_train_ovr(const uint16_t* desc, int32_t n, int32_t dim, const int32_
                       int32_t n_classes, const int32_t* order, int64_t T, int32_t inv_lambda,
                       float* W, float* bias, int64_t* z_out, lbp_stream_t stream);
 
+/*
+ * Descriptor compaction for the database all-gather ("pack counts (u8 +
+ * overflow flag) to halve all-gather bytes"; R21).  Cell counts of 128x128 crops
+ * are <= 256 and almost always <= 255, so a descriptor travels as one byte per entry plus a
+ * short list of the entries that do not fit:
+ *   packed[i][d] = min(desc[i][d], 255)
+ *   exceptions   = { (row_base + i, d, desc[i][d]) : desc[i][d] > 255 }
+ * The list order is unspecified (entries are unique, so decoding does not depend on it).
+ */
+typedef struct {
+    int64_t row;    /* global descriptor row */
+    int32_t index;  /* entry within the row, [0, dim) */
+    int32_t value;  /* the u16 count, > 255 */
+} lbp_desc_exc_t;
+
+/*
+ * lbp_desc_pack_u8 -- desc u16 [n][dim] (device, contiguous rows) -> packed u8 [n][dim] and
+ * exceptions (device arrays, caller-owned).  *exc_count (device int32) is set to the number
+ * of exceptions found -- entries past exc_cap are counted but not stored, so a count >
+ * exc_cap after the stream synchronises means "re-run with a larger cap".  Two launches (a
+ * memset of the count and one streaming kernel: 2 B read + 1 B written per entry).
+ * n == 0 -> LBP_OK (only the count is zeroed); null pointers, n < 0, dim < 1, exc_cap < 0
+ * -> LBP_E_ARG before anything is enqueued.
+ */
+int32_t lbp_desc_pack_u8(const uint16_t* desc, int64_t n, int32_t dim, int64_t row_base,
+                         uint8_t* packed, lbp_desc_exc_t* exc, int32_t exc_cap,
+                         int32_t* exc_count, lbp_stream_t stream);
+
+/*
+ * lbp_desc_unpack_u8 -- the inverse, for rows [row_base, row_base + n): desc[i][d] =
+ * packed[i][d], then every listed exception whose row falls in the range overwrites its
+ * entry (others are ignored).  The exceptions come as n_lists lists of exc_cap records each
+ * (list l at exc + l * exc_cap, e.g. one per rank after an all-gather) with counts
+ * exc_counts[l] (device int32; min(count, exc_cap) records of a list are read).  Two
+ * launches (widen: 1 B read + 2 B written per entry; scatter of the exceptions).
+ */
+int32_t lbp_desc_unpack_u8(const uint8_t* packed, int64_t n, int32_t dim, int64_t row_base,
+                           const lbp_desc_exc_t* exc, const int32_t* exc_counts, int32_t n_lists,
+                           int32_t exc_cap, uint16_t* desc, lbp_stream_t stream);
+
 /* Bytes of device workspace svm_prepare() needs for a [n_classes][dim] model
  * (0 if the tensor-core path does not apply to this shape). */
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim);

@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "desc_pack.cuh"
 #include "lbp_hist_generic.cuh"
 #include "lbp_hist_fast.cuh"
 #include "lbp_hist_lane59.cuh"
@@ -353,6 +354,59 @@ int32_t svm_train_ovr(const uint16_t* desc, int32_t n, int32_t dim, const int32_
     if (e != cudaSuccess) return launch_status(e);
     k<<<std::min(n_classes, 2 * num_sms()), 1024, smem, stream>>>(
         desc, n, dim, labels, n_classes, order, T, inv_lambda, W, bias, z_out);
+    return launch_status(cudaGetLastError());
+}
+
+int32_t lbp_desc_pack_u8(const uint16_t* desc, int64_t n, int32_t dim, int64_t row_base,
+                         uint8_t* packed, lbp_desc_exc_t* exc, int32_t exc_cap,
+                         int32_t* exc_count, lbp_stream_t stream_) {
+    if (n < 0 || dim < 1 || exc_cap < 0 || !exc_count) return LBP_E_ARG;
+    if (n > 0 && (!desc || !packed || (exc_cap > 0 && !exc))) return LBP_E_ARG;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    cudaError_t e = cudaMemsetAsync(exc_count, 0, sizeof(int32_t), stream);
+    if (e != cudaSuccess) return launch_status(e);
+    if (n == 0) return LBP_OK;
+    const int64_t total = n * (int64_t)dim;
+    const bool vec = ((reinterpret_cast<uintptr_t>(desc) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(packed) & 7) == 0);
+    const int64_t work = vec ? (total >> 3) + 8 : total;
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((work + kPackThreads - 1) / kPackThreads, (int64_t)num_sms() * 8));
+    if (vec)
+        desc_pack_u8_kernel<true><<<grid, kPackThreads, 0, stream>>>(
+            desc, total, dim, row_base, packed, exc, exc_cap, exc_count);
+    else
+        desc_pack_u8_kernel<false><<<grid, kPackThreads, 0, stream>>>(
+            desc, total, dim, row_base, packed, exc, exc_cap, exc_count);
+    return launch_status(cudaGetLastError());
+}
+
+int32_t lbp_desc_unpack_u8(const uint8_t* packed, int64_t n, int32_t dim, int64_t row_base,
+                           const lbp_desc_exc_t* exc, const int32_t* exc_counts, int32_t n_lists,
+                           int32_t exc_cap, uint16_t* desc, lbp_stream_t stream_) {
+    if (n < 0 || dim < 1 || n_lists < 0 || exc_cap < 0) return LBP_E_ARG;
+    if (n == 0) return LBP_OK;
+    if (!packed || !desc || (n_lists > 0 && exc_cap > 0 && (!exc || !exc_counts)))
+        return LBP_E_ARG;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int64_t total = n * (int64_t)dim;
+    const bool vec = ((reinterpret_cast<uintptr_t>(desc) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(packed) & 7) == 0);
+    const int64_t work = vec ? (total >> 3) + 8 : total;
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((work + kPackThreads - 1) / kPackThreads, (int64_t)num_sms() * 8));
+    if (vec)
+        desc_unpack_u8_kernel<true><<<grid, kPackThreads, 0, stream>>>(packed, total, desc);
+    else
+        desc_unpack_u8_kernel<false><<<grid, kPackThreads, 0, stream>>>(packed, total, desc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return launch_status(e);
+    const int64_t recs = (int64_t)n_lists * exc_cap;
+    if (recs == 0) return LBP_OK;
+    const int sgrid = (int)std::min<int64_t>((recs + kPackThreads - 1) / kPackThreads,
+                                             (int64_t)num_sms() * 4);
+    desc_exc_scatter_kernel<<<sgrid, kPackThreads, 0, stream>>>(exc, exc_counts, n_lists, exc_cap,
+                                                                row_base, n, dim, desc);
     return launch_status(cudaGetLastError());
 }
 

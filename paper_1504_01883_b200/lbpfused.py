@@ -67,6 +67,11 @@ def lib():
         L.svm_score_l1.restype = i32
         L.svm_train_ovr.argtypes = [P, i32, i32, P, i32, P, ctypes.c_int64, i32, P, P, P, P]
         L.svm_train_ovr.restype = i32
+        i64 = ctypes.c_int64
+        L.lbp_desc_pack_u8.argtypes = [P, i64, i32, i64, P, P, i32, P, P]
+        L.lbp_desc_pack_u8.restype = i32
+        L.lbp_desc_unpack_u8.argtypes = [P, i64, i32, i64, P, P, i32, i32, P, P]
+        L.lbp_desc_unpack_u8.restype = i32
         L.svm_workspace_bytes.argtypes = [i32, i32]
         L.svm_workspace_bytes.restype = sz
         L.svm_prepare.argtypes = [P, i32, i32, P, sz, P]
@@ -360,3 +365,49 @@ def svm_train_ovr(desc: torch.Tensor, labels: torch.Tensor, n_classes: int, orde
     if st != LBP_OK:
         raise LbpError(st, "svm_train_ovr")
     return (W, b, z) if return_z else (W, b)
+
+
+def desc_pack_u8(desc: torch.Tensor, row_base: int = 0, cap: int = 4096,
+                 packed: torch.Tensor | None = None, exc: torch.Tensor | None = None,
+                 count: torch.Tensor | None = None, stream=None):
+    """Descriptor compaction (lbp_desc_pack_u8): returns (packed u8 [n][dim], exceptions int32
+    [cap][4] = lbp_desc_exc_t records (row lo, row hi, index, value), count int32 [1]).
+    count > cap after the stream synchronises means the list was truncated."""
+    _check_cuda(desc, packed, exc, count)
+    assert desc.dtype == torch.uint16 and desc.is_contiguous() and desc.dim() == 2
+    n, dim = desc.shape
+    dev = desc.device
+    if packed is None:
+        packed = torch.empty((n, dim), dtype=torch.uint8, device=dev)
+    if exc is None:
+        exc = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=dev)
+    if count is None:
+        count = torch.empty(1, dtype=torch.int32, device=dev)
+    assert packed.dtype == torch.uint8 and packed.is_contiguous() and packed.numel() >= n * dim
+    assert exc.dtype == torch.int32 and exc.is_contiguous() and exc.numel() >= 4 * cap
+    st = lib().lbp_desc_pack_u8(_ptr(desc), n, dim, row_base, _ptr(packed), _ptr(exc), cap,
+                                _ptr(count), _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_desc_pack_u8")
+    return packed, exc, count
+
+
+def desc_unpack_u8(packed: torch.Tensor, exc: torch.Tensor, counts: torch.Tensor, cap: int,
+                   row_base: int = 0, out: torch.Tensor | None = None, stream=None):
+    """Inverse of desc_pack_u8 (lbp_desc_unpack_u8): u16 [n][dim] from packed u8 [n][dim] and
+    len(counts) exception lists of `cap` records each (exc int32 [len(counts) * cap][4])."""
+    _check_cuda(packed, exc, counts, out)
+    assert packed.dtype == torch.uint8 and packed.is_contiguous() and packed.dim() == 2
+    assert exc.dtype == torch.int32 and exc.is_contiguous()
+    assert counts.dtype == torch.int32 and counts.is_contiguous()
+    n, dim = packed.shape
+    n_lists = counts.numel()
+    assert exc.numel() >= 4 * n_lists * cap
+    if out is None:
+        out = torch.empty((n, dim), dtype=torch.uint16, device=packed.device)
+    assert out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim
+    st = lib().lbp_desc_unpack_u8(_ptr(packed), n, dim, row_base, _ptr(exc), _ptr(counts),
+                                  n_lists, cap, _ptr(out), _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_desc_unpack_u8")
+    return out

@@ -61,6 +61,71 @@ def gather_database(local_desc: torch.Tensor, local_labels: torch.Tensor, n_tota
     return recv.index_select(0, keep).view(torch.uint16), recv_lab.index_select(0, keep)
 
 
+def _gpu_pack(desc, row_base, cap, packed_out):
+    from . import lbpfused
+    _, exc, count = lbpfused.desc_pack_u8(desc, row_base=row_base, cap=cap,
+                                          packed=packed_out[:desc.shape[0]])
+    return exc, count
+
+
+def _gpu_unpack(packed, exc, counts, cap):
+    from . import lbpfused
+    return lbpfused.desc_unpack_u8(packed, exc, counts, cap)
+
+
+def gather_database_compact(local_desc: torch.Tensor, local_labels: torch.Tensor, n_total: int,
+                            group=None, cap: int = 4096, pack=None, unpack=None
+                            ) -> tuple[torch.Tensor, torch.Tensor]:
+    """gather_database with compacted descriptors (R21): every rank
+    sends its rows as u8 counts (min(count, 255), lbp_desc_pack_u8) plus a list of the
+    entries > 255, so the all-gather moves half the bytes; the receiver rebuilds the exact
+    u16 matrix (lbp_desc_unpack_u8).  Same result as gather_database.
+
+    The exception lists have a fixed capacity per rank for the collective: each rank packs
+    with `cap` records, the counts are all-gathered (one host sync per build), and if any
+    rank overflowed every rank re-packs with the largest count.  pack / unpack default to the
+    CUDA library; CPU (gloo) tests pass stand-ins with the same contract:
+      pack(desc u16 [n][dim], row_base, cap, packed_out u8 [>= n][dim]) -> (exc int32 [cap][4],
+           count int32 [1]);  unpack(packed u8 [N][dim], exc int32 [L * cap][4],
+           counts int32 [L], cap) -> u16 [N][dim]."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    first, count = shard_range(n_total, rank, world)
+    if local_desc.shape[0] != count or local_labels.shape[0] != count:
+        raise ValueError(f"rank {rank}: shard has {local_desc.shape[0]} rows, expected {count}")
+    if world == 1:
+        return local_desc, local_labels
+    pack = pack or _gpu_pack
+    unpack = unpack or _gpu_unpack
+    cap = max(1, int(cap))
+    dim = local_desc.shape[1]
+    rows_cap = -(-n_total // world)
+    dev = local_desc.device
+    send = torch.zeros((rows_cap, dim), dtype=torch.uint8, device=dev)
+    desc = local_desc.contiguous()
+    exc, cnt = pack(desc, first, cap, send)
+    counts = torch.empty(world, dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(counts, cnt.reshape(1), group=group)
+    most = int(counts.max())
+    if most > cap:  # some rank's list overflowed: everyone re-packs with the largest count
+        cap = most
+        exc, cnt = pack(desc, first, cap, send)
+    recv = torch.empty((world * rows_cap, dim), dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    exc_all = torch.empty((world * cap, 4), dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(exc_all, exc[:cap].contiguous(), group=group)
+    lab_send = torch.full((rows_cap,), -1, dtype=torch.int32, device=dev)
+    lab_send[:count] = local_labels
+    lab_recv = torch.empty((world * rows_cap,), dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(lab_recv, lab_send, group=group)
+    if n_total % world != 0:  # drop the padding rows (exceptions carry global row numbers)
+        keep = torch.cat([torch.arange(r * rows_cap, r * rows_cap + shard_range(n_total, r, world)[1])
+                          for r in range(world)]).to(dev)
+        recv = recv.index_select(0, keep)
+        lab_recv = lab_recv.index_select(0, keep)
+    return unpack(recv, exc_all, counts, cap), lab_recv
+
+
 def gather_database_chunked(extract_chunk, local_labels: torch.Tensor, n_total: int, dim: int,
                             chunks: int, group=None, device=None,
                             comm_stream: torch.cuda.Stream | None = None

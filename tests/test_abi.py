@@ -166,3 +166,19 @@ def test_binding_refuses_cpu_tensors():
     r = torch.zeros(1, 5, dtype=torch.int32)
     with pytest.raises(ValueError):
         lb.lbp_fused_extract(g, None, r, 0, 10, 2, 2, 59)
+
+
+def test_desc_pack_host_errors(L):
+    from paper_1504_01883_b200 import lbpfused as lb
+    fake = ctypes.c_void_p(16)  # never dereferenced: every call below fails validation first
+    assert L.lbp_desc_pack_u8(fake, 4, 0, 0, fake, fake, 8, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_pack_u8(fake, -1, 8, 0, fake, fake, 8, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_pack_u8(fake, 4, 8, 0, fake, fake, -1, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_pack_u8(fake, 4, 8, 0, fake, fake, 8, None, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_pack_u8(None, 4, 8, 0, fake, fake, 8, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_pack_u8(fake, 4, 8, 0, fake, None, 8, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_unpack_u8(fake, 4, 0, 0, fake, fake, 1, 8, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_unpack_u8(None, 4, 8, 0, fake, fake, 1, 8, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_unpack_u8(fake, 4, 8, 0, None, fake, 1, 8, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_unpack_u8(fake, 4, 8, 0, fake, fake, -1, 8, fake, None) == lb.LBP_E_ARG
+    assert L.lbp_desc_unpack_u8(fake, 0, 8, 0, fake, fake, 1, 8, fake, None) == lb.LBP_OK

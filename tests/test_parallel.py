@@ -108,3 +108,70 @@ def test_gather_database_chunked_gloo(tmp_path, world, n_total, chunks):
     for r in range(world):
         assert np.array_equal(np.load(tmp_path / f"desc{r}.npy").view(np.uint16), ref)
         assert np.array_equal(np.load(tmp_path / f"lab{r}.npy"), np.arange(n_total) % 5)
+
+
+# ---- compacted database all-gather (R21) with CPU stand-ins for the
+# CUDA pack/unpack that follow the same contract (the oracle's encoding)
+def _cpu_pack(desc, row_base, cap, packed_out):
+    packed, exc, cnt = oracle.desc_pack_u8(desc.view(torch.int16).numpy().view(np.uint16),
+                                           row_base=row_base, cap=cap)
+    packed_out[:desc.shape[0]] = torch.from_numpy(packed)
+    rec = np.zeros((cap, 4), np.int32)
+    if len(exc):
+        rec[:len(exc), 0:2] = exc[:, 0].astype(np.int64).view(np.int32).reshape(-1, 2)
+        rec[:len(exc), 2] = exc[:, 1]
+        rec[:len(exc), 3] = exc[:, 2]
+    return torch.from_numpy(rec), torch.tensor([cnt], dtype=torch.int32)
+
+
+def _cpu_unpack(packed, exc, counts, cap):
+    rec = exc.numpy().reshape(-1, cap, 4)
+    lists = []
+    for l, c in enumerate(counts.tolist()):
+        r = rec[l, :min(c, cap)]
+        rows = np.ascontiguousarray(r[:, 0:2]).view(np.int64).reshape(-1)
+        lists.append(np.stack([rows, r[:, 2].astype(np.int64), r[:, 3].astype(np.int64)], 1))
+    out = oracle.desc_unpack_u8(packed.numpy(), np.concatenate(lists) if lists else
+                                np.zeros((0, 3), np.int64))
+    return torch.from_numpy(out.view(np.int16)).view(torch.uint16)
+
+
+def _compact_crops(first, count):
+    """128x128 crops without depth; every third crop constant (its 36 16x16 cells count 256)"""
+    grey, _ = synthgen.face_crops(count, 128, 128, seed=11, first_index=first)
+    for k in range(count):
+        if (first + k) % 3 == 0:
+            grey[k] = 90
+    return grey
+
+
+def _worker_compact(rank, world, port, n_total, cap, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1504_01883_b200.parallel import gather_database_compact
+        first, count = shard_range(n_total, rank, world)
+        desc = oracle.lbp_extract(_compact_crops(first, count), None,
+                                  synthgen.full_rois(count, 128, 128), 0, 0, 8, 8, 59)
+        labels = torch.from_numpy((np.arange(first, first + count) % 4).astype(np.int32))
+        full, lab = gather_database_compact(torch.from_numpy(desc.view(np.int16)).view(torch.uint16),
+                                            labels, n_total, cap=cap, pack=_cpu_pack,
+                                            unpack=_cpu_unpack)
+        np.save(os.path.join(out_dir, f"desc{rank}.npy"), full.view(torch.int16).numpy())
+        np.save(os.path.join(out_dir, f"lab{rank}.npy"), lab.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_total,cap", [(2, 6, 4096), (3, 7, 8), (2, 5, 1)])
+def test_gather_database_compact_gloo(tmp_path, world, n_total, cap):
+    """u8 + exceptions all-gather == the oracle's u16 matrix; small caps take the re-pack."""
+    mp.spawn(_worker_compact, args=(world, _free_port(), n_total, cap, str(tmp_path)),
+             nprocs=world, join=True)
+    ref = oracle.lbp_extract(_compact_crops(0, n_total), None,
+                             synthgen.full_rois(n_total, 128, 128), 0, 0, 8, 8, 59)
+    assert (ref > 255).sum() == 36 * len(range(0, n_total, 3))
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"desc{r}.npy").view(np.uint16), ref)
+        assert np.array_equal(np.load(tmp_path / f"lab{r}.npy"), np.arange(n_total) % 4)
