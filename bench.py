@@ -100,6 +100,8 @@ def parse():
                         "lbp_fused_extract + svm_score (two launches)")
     p.add_argument("--chunks", type=int, default=4,
                    help="config5: extraction/all-gather overlap chunks (1 = serial)")
+    p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                   help="process-group backend for N > 1 (gloo: functional check only)")
     p.add_argument("--compact", action="store_true",
                    help="config5: all-gather u8 descriptors + exception lists (serial; "
                         "lbp_desc_pack_u8 / lbp_desc_unpack_u8), and time pack/unpack")
@@ -307,10 +309,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = rank_device(torch, local, world, args)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dist, args, dev)
 
     n, H, Wd, cx, cy, bins, C, desc_txt = WORKLOADS[args.workload]
     n = args.crops or n
@@ -431,6 +432,15 @@ def main():
         if not gate_ok:
             print(json.dumps({"error": "equivalence gate failed: GPU != oracle on the sample"}),
                   flush=True)
+            return 3
+    elif world > 1:  # every rank checks its own shard's first crops; any failure stops all
+        ok = rank_gate(torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins,
+                       source, 512)
+        flag = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag[0]) == 0:
+            if rank == 0:
+                print(json.dumps({"error": "equivalence gate failed on some rank"}), flush=True)
             return 3
 
     if rank == 0:
@@ -604,10 +614,9 @@ def run_dbbuild(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = rank_device(torch, local, world, args)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dist, args, dev)
     else:  # the gather is a no-op copy; keep one code path with a 1-rank gloo group
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", str(29500 + (os.getpid() % 1000)))
@@ -729,8 +738,14 @@ def run_dbbuild(args):
                                             (3 if args.compact and world > 1 else 0)),
             "clocks": clk.summary(),
             "check": {"rows": int(full.shape[0]), "label_ok": bool(
-                (lab.cpu() == (torch.arange(n_total) % N_IDS).to(torch.int32)).all())},
+                (lab.cpu() == (torch.arange(n_total) % N_IDS).to(torch.int32)).all()),
+                "desc_sample_ok": db_sample_ok(full, n_total, H, Wd, cx, cy, bins, args)},
         }
+        if not (line["check"]["label_ok"] and line["check"]["desc_sample_ok"]):
+            print(json.dumps({"error": "database check failed", "check": line["check"]}),
+                  flush=True)
+            dist.destroy_process_group()
+            return 3
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
@@ -847,19 +862,71 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
                                                         SOURCES[args.source])
     gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
     glab = labels[:m].cpu().numpy()
-    ok = bool(np.array_equal(gdesc, odesc))
-    if ok:
-        import oracle
-        s_ref, _, _ = oracle.svm_score(odesc, W_np, b_np)
-        srt = np.sort(s_ref, axis=1)
-        clear = (srt[:, -1] - srt[:, -2]) > 1e-4 * np.maximum(np.abs(srt[:, -1]), 1e-3)
-        ok = bool(np.array_equal(glab[clear], olab[clear]))
+    ok = gate_compare(gdesc, glab, odesc, olab, W_np, b_np)
     cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
            "sample": f"first {m} crops of this workload x {passes} passes = {done} crops "
                      f"(extraction + SVM), {threads} threads x unmodified single-threaded C "
                      f"oracle on disjoint shards, {secs:.1f} s",
            "cpu": cpu_model(), "equivalence_gate": "pass" if ok else "FAIL"}
     return cpu, ok
+
+
+def db_sample_ok(full, n_total, H, Wd, cx, cy, bins, args, k=8):
+    """The gathered database against the oracle on k rows spread over every rank's shard
+    (crop i is a pure function of its global index, so rank 0 regenerates it)."""
+    import oracle
+    import synthgen
+    import torch
+    idx = np.unique(np.linspace(0, n_total - 1, k).astype(np.int64))
+    for i in idx:
+        g, d = synthgen.face_crops(1, H, Wd, seed=args.seed, first_index=int(i), dist=args.dist)
+        ref = oracle.lbp_extract(g, d, synthgen.full_rois(1, H, Wd), DMIN, DMAX, cx, cy, bins)
+        got = full[int(i)].cpu().view(torch.int16).numpy().view(np.uint16)
+        if not np.array_equal(got, ref[0]):
+            return False
+    return True
+
+
+def gate_compare(gdesc, glab, odesc, olab, W_np, b_np):
+    """Equivalence gate: descriptors bit-exact, labels equal wherever the oracle's top-2 gap
+    is clear of the score tolerance."""
+    if not np.array_equal(gdesc, odesc):
+        return False
+    import oracle
+    s_ref, _, _ = oracle.svm_score(odesc, W_np, b_np)
+    srt = np.sort(s_ref, axis=1)
+    clear = (srt[:, -1] - srt[:, -2]) > 1e-4 * np.maximum(np.abs(srt[:, -1]), 1e-3)
+    return bool(np.array_equal(glab[clear], olab[clear]))
+
+
+def rank_gate(torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins, source, m):
+    """The equivalence gate on every rank at N > 1 (no CPU timing): the oracle on this
+    rank's first m crops."""
+    import oracle
+    m = min(m, grey.shape[0])
+    g = grey[:m].cpu().numpy()
+    d = depth[:m].cpu().view(torch.int16).numpy().view(np.uint16) if depth is not None else None
+    r = rois[:m].cpu().numpy()
+    odesc = oracle.lbp_extract(g, d, r, DMIN, DMAX, cx, cy, bins, source=source)
+    _, olab, _ = oracle.svm_score(odesc, W_np, b_np)
+    gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
+    return gate_compare(gdesc, labels[:m].cpu().numpy(), odesc, olab, W_np, b_np)
+
+
+def rank_device(torch, local, world, args):
+    """cuda:LOCAL_RANK (one process per GPU).  --dist-backend gloo lets several ranks share
+    a device (a functional check of the multi-rank code path on a one-GPU box: nothing in the
+    timed path waits on another rank's kernels; such a run is never a measurement)."""
+    idx = local if args.dist_backend == "nccl" else local % torch.cuda.device_count()
+    torch.cuda.set_device(idx)
+    return torch.device("cuda", idx)
+
+
+def init_dist(dist, args, dev):
+    if args.dist_backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
 
 
 def load_peaks():
