@@ -338,8 +338,24 @@ int32_t svm_train_ovr(const uint16_t* desc, int32_t n, int32_t dim, const int32_
     if (T > (int64_t(1) << 31)) return LBP_E_ARG;
     if (!desc || !labels || !order || !W || !bias) return LBP_E_ARG;
     if (dim > kTrainMaxDim) return LBP_E_UNSUPPORTED;
-    const size_t smem = (size_t)(dim + 1) * sizeof(int64_t);
     cudaStream_t stream = (cudaStream_t)stream_;
+    // even dim, 4-B aligned rows: z in registers, one barrier per step (svm_train.cuh)
+    if ((dim & 1) == 0 && (reinterpret_cast<uintptr_t>(desc) & 3) == 0) {
+        const bool z32 = T * 65535 < (int64_t(1) << 31);  // |z_T[d]| <= T * 65535
+        if (dim <= 2 * 256 * 8) {
+            auto k = z32 ? svm_train_ovr_reg_kernel<256, 8, true>
+                         : svm_train_ovr_reg_kernel<256, 8, false>;
+            k<<<std::min(n_classes, 4 * num_sms()), 256, 0, stream>>>(
+                desc, n, dim, labels, n_classes, order, T, inv_lambda, W, bias, z_out);
+        } else {
+            auto k = z32 ? svm_train_ovr_reg_kernel<1024, 8, true>
+                         : svm_train_ovr_reg_kernel<1024, 8, false>;
+            k<<<std::min(n_classes, 2 * num_sms()), 1024, 0, stream>>>(
+                desc, n, dim, labels, n_classes, order, T, inv_lambda, W, bias, z_out);
+        }
+        return launch_status(cudaGetLastError());
+    }
+    const size_t smem = (size_t)(dim + 1) * sizeof(int64_t);
     if (dim <= 256 * 16) {  // 59-bin descriptors: 256 threads x 16 entries (cheaper barriers)
         auto k = svm_train_ovr_kernel<256, 16>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -13,6 +13,8 @@
 // violated, an integer update of the thread's z entries.  The step chain of a class is
 // sequential by definition; classes run in parallel.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace lbpf {
@@ -100,6 +102,119 @@ svm_train_ovr_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
         if (z_out)
             for (int d = t0; d <= dim; d += kTrainThreads) z_out[(int64_t)c * (dim + 1) + d] = z[d];
         __syncthreads();  // z is reset for the next class
+    }
+}
+
+// Register-resident variant (even dim): each thread owns the descriptor entry PAIRS
+// (2p, 2p+1), p = tid + k * NT, and keeps its z entries in registers (they are private to the
+// thread: the update of entry d only needs z[d] and x[d]).  The dot product's warp partials go
+// to a double-buffered smem array; after ONE barrier every thread sums the partials itself
+// and takes the (identical, integer) decision, so no second barrier and no smem z.  The bias
+// entry z[dim] is kept by every thread redundantly.  Z32: int32 z, exact while T * 65535 <
+// 2^31 (|z_T[d]| <= T max x); the products accumulate in int64 (IMAD.WIDE).
+template <int NT, int PAIRS, bool Z32>
+__global__ void __launch_bounds__(NT)
+svm_train_ovr_reg_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t dim,
+                         const int32_t* __restrict__ labels, int32_t n_classes,
+                         const int32_t* __restrict__ order, int64_t T, int32_t inv_lambda,
+                         float* __restrict__ W, float* __restrict__ bias,
+                         int64_t* __restrict__ z_out) {
+    using ZT = typename std::conditional<Z32, int32_t, int64_t>::type;
+    constexpr int kWarps = NT / 32;
+    __shared__ long long red[2][kWarps];
+    const int t0 = threadIdx.x, warp = t0 >> 5, lane = t0 & 31;
+    const int half = dim >> 1;
+    const uint32_t* __restrict__ d32 = reinterpret_cast<const uint32_t*>(desc);
+
+    for (int32_t c = blockIdx.x; c < n_classes; c += gridDim.x) {
+        ZT z[2 * PAIRS];
+#pragma unroll
+        for (int k = 0; k < 2 * PAIRS; ++k) z[k] = 0;
+        ZT zb = 0;
+        // software pipeline over a 3-slot register ring, the step loop unrolled by 3 so that
+        // every slot is a fixed register set (a register copy of a just-requested load would
+        // wait for it): step t (slot r = (t-1) % 3) uses the counts in buf[r] requested two
+        // steps ago, requests the counts of step t+2 into buf[(r+2)%3] from the index ids[..]
+        // loaded one step ago, and loads the index of step t+3 into ids[r].
+        auto idx = [&](int64_t j) { return __ldg(order + (j < T ? j : T - 1)); };
+        uint32_t buf[3][PAIRS];
+        int32_t ids[3] = {idx(0), idx(1), idx(2)};
+        int32_t labs[3];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+            for (int k = 0; k < PAIRS; ++k) {
+                const int p = t0 + k * NT;
+                buf[r][k] = p < half ? __ldg(d32 + (int64_t)ids[r] * half + p) : 0u;
+            }
+            labs[r] = __ldg(labels + ids[r]);
+        }
+        for (int64_t t0s = 1; t0s <= T; t0s += 3) {
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const int64_t t = t0s + r;
+                if (t > T) break;  // uniform
+                const int rn = (r + 2) % 3;
+#pragma unroll
+                for (int k = 0; k < PAIRS; ++k) {
+                    const int p = t0 + k * NT;
+                    buf[rn][k] = p < half ? __ldg(d32 + (int64_t)ids[rn] * half + p) : 0u;
+                }
+                labs[rn] = __ldg(labels + ids[rn]);
+                ids[r] = idx(t + 2);
+                const ZT y = (labs[r] == c) ? 1 : -1;
+                bool viol = true;
+                if (t > 1) {
+                    long long part = 0;
+#pragma unroll
+                    for (int k = 0; k < PAIRS; ++k) {
+                        part += (long long)z[2 * k] * (long long)(buf[r][k] & 0xFFFFu);
+                        part += (long long)z[2 * k + 1] * (long long)(buf[r][k] >> 16);
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1)
+                        part += __shfl_xor_sync(0xFFFFFFFFu, part, off);
+                    const int rb = (int)(t & 1);
+                    if (lane == 0) red[rb][warp] = part;
+                    __syncthreads();
+                    long long dot = (long long)zb;
+#pragma unroll
+                    for (int w = 0; w < kWarps; ++w) dot += red[rb][w];
+                    // (an incremental loop-carried threshold and a 32-bit division both
+                    // measured slower: this form depends only on t and overlaps the reduction)
+                    const long long thr = (long long)((t - 1 + inv_lambda - 1) / inv_lambda);
+                    viol = (long long)y * dot < thr;
+                }
+                if (viol) {
+#pragma unroll
+                    for (int k = 0; k < PAIRS; ++k) {
+                        z[2 * k] += y * (ZT)(buf[r][k] & 0xFFFFu);
+                        z[2 * k + 1] += y * (ZT)(buf[r][k] >> 16);
+                    }
+                    zb += y;
+                }
+            }
+        }
+        // model: w = inv_lambda z_T / T, one fp64 division (correctly rounded) then fp32
+        const double Td = (double)T;
+#pragma unroll
+        for (int k = 0; k < PAIRS; ++k) {
+            const int p = t0 + k * NT;
+            if (p < half) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int d = 2 * p + e;
+                    const int64_t zd = (int64_t)z[2 * k + e];
+                    W[(int64_t)c * dim + d] = (float)((double)((int64_t)inv_lambda * zd) / Td);
+                    if (z_out) z_out[(int64_t)c * (dim + 1) + d] = zd;
+                }
+            }
+        }
+        if (t0 == 0) {
+            bias[c] = (float)((double)((int64_t)inv_lambda * (int64_t)zb) / Td);
+            if (z_out) z_out[(int64_t)c * (dim + 1) + dim] = (int64_t)zb;
+        }
+        __syncthreads();  // the partial buffers are reused by the next class
     }
 }
 

@@ -67,3 +67,13 @@ def test_trained_model_recognises_separable_clusters(lb):
     W, b = _check(lb, X, labels, C, synthgen.train_order(len(X), 20, seed=4), 100)
     _, pred, _ = lb.svm_score(torch.from_numpy(X.view(np.int16)).to(DEV).view(torch.uint16), W, b)
     assert np.array_equal(pred.cpu().numpy(), labels)
+
+
+@pytest.mark.parametrize("dim,n,epochs", [(59, 30, 3),        # odd dim: smem-z kernel
+                                          (120, 40, 820),     # T = 32,800: int64 register z
+                                          (16384, 6, 2)])     # 1,024-thread register kernel
+def test_kernel_variants(lb, dim, n, epochs):
+    rng = np.random.default_rng(dim + n)
+    desc = rng.integers(0, 300, (n, dim)).astype(np.uint16)
+    labels = rng.integers(0, 4, n).astype(np.int32)
+    _check(lb, desc, labels, 3, synthgen.train_order(n, epochs, seed=dim), 97)
