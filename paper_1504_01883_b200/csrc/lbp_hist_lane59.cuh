@@ -186,6 +186,14 @@ __device__ __forceinline__ uint32_t hle2_mask(uint32_t a, uint32_t b) {
     return r;
 }
 
+// |a - b| per half (exact where used: see the WINM == 2 window below)
+__device__ __forceinline__ uint32_t habsdiff2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    asm("abs.f16x2 %0, %0;" : "+r"(d));
+    return d;
+}
+
 __device__ __forceinline__ uint32_t hge2_one(uint32_t a, uint32_t b) {
     uint32_t r;  // 1.0 / 0.0 per half
     asm("set.ge.f16x2.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -209,7 +217,16 @@ __device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uin
     return f + a;
 }
 
-template <bool HAS_DEPTH, bool DEPTH_SRC, bool FP16WIN, bool FRAME>
+// WINM: how the depth window is tested.  0: integer compare per pixel; 1: both halves of a
+// depth word at once as fp16 compares, dmax <= 0x7BFE (a u16 d read as fp16 bits is, for
+// d <= 0x7BFF, a non-negative finite half whose bit order is its value order; larger bit
+// patterns are +inf, NaN or negative and fail d >= dmin or d <= dmax, so the raw words are
+// compared); 2: |d - mid| <= half with mid = (dmin + dmax) / 2 and half = (dmax - dmin) / 2,
+// when dmax < 2048 and dmin + dmax is even -- below 2048 the halves are exact multiples of
+// 2^-24 (value = bits * 2^-24), so the subtraction is exact there; for larger d either
+// mid/2 <= d <= 2 mid (exact by Sterbenz) or d > 2 mid, where the rounded difference is still
+// >= mid > half; NaN / inf / negative patterns fail the compare.
+template <bool HAS_DEPTH, bool DEPTH_SRC, int WINM, bool FRAME>
 __global__ void __launch_bounds__(l59::kThreads, 1)
 lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const __grid_constant__ CUtensorMap depth_map,
@@ -219,6 +236,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        int32_t* __restrict__ roi_status) {
     using namespace l59;
     using L = Layout<FRAME>;
+    constexpr bool FP16WIN = WINM != 0;
     constexpr int kGreyBytes = L::kGreyBytes, kStageBytes = L::kStageBytes;
     constexpr int kGroupOff = L::kGroupOff, kGroupBytes = L::kGroupBytes;
     constexpr int kLutOff = L::kLutOff, kPlainLutOff = L::kPlainLutOff, kBarOff = L::kBarOff;
@@ -302,7 +320,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     }
     const uint32_t lo16 = win.lo << 16;
     const uint32_t span16 = (win.span << 16) | 0xFFFFu;
-    const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // FP16WIN
+    const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // WINM 1
+    const uint32_t mid2 = ((2 * win.lo + win.span) / 2) * 0x10001u;                 // WINM 2
+    const uint32_t half2 = (win.span / 2) * 0x10001u;
     const uint32_t lut_lane = opaque(smem_u32(smem + kLutOff) + 4 * lane - 0x6400u);
     const int i0 = (warp * (kTile - 2)) / 8;                   // first interior row of cell row
     const int nrows = ((warp + 1) * (kTile - 2)) / 8 - i0;     // 15 or 16
@@ -378,20 +398,26 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             }
             uint32_t val[4];
             if constexpr (HAS_DEPTH && FP16WIN) {
-                // depth window on both halves at once (dmax <= 0x7BFE): a clamped u16 read as
-                // fp16 bits compares exactly (see depth_row); masked-out pixels are redirected
-                // to the dummy LUT row (-> dummy bin) instead of adding 0
+                // depth window on both halves at once, on the raw words (see WINM above);
+                // masked-out pixels are redirected to the dummy LUT row (-> dummy bin)
+                // instead of adding 0
                 uint32_t c0, c1;
                 if constexpr (DEPTH_SRC) {
-                    c0 = mid.h0;
-                    c1 = mid.h1;
+                    c0 = mid.raw0;
+                    c1 = mid.raw1;
                 } else {
                     const uint2 d = load_depth(d0 + j * kDRow);
-                    c0 = vmin_u16x2(d.x, 0x7BFF7BFFu);
-                    c1 = vmin_u16x2(d.y, 0x7BFF7BFFu);
+                    c0 = d.x;
+                    c1 = d.y;
                 }
-                const uint32_t m0 = hge2_mask(c0, lo2) & hle2_mask(c0, hi2);
-                const uint32_t m1 = hge2_mask(c1, lo2) & hle2_mask(c1, hi2);
+                uint32_t m0, m1;
+                if constexpr (WINM == 2) {
+                    m0 = hle2_mask(habsdiff2(c0, mid2), half2);
+                    m1 = hle2_mask(habsdiff2(c1, mid2), half2);
+                } else {
+                    m0 = hge2_mask(c0, lo2) & hle2_mask(c0, hi2);
+                    m1 = hge2_mask(c1, lo2) & hle2_mask(c1, hi2);
+                }
                 t0 = (t0 & m0) | (kDummyOff2 & ~m0);
                 t1 = (t1 & m1) | (kDummyOff2 & ~m1);
 #pragma unroll
@@ -504,12 +530,18 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     if (depth_source) gm = dm;  // grey is not read
     // depth window as fp16 compares whenever dmax <= 0x7BFE (always for the depth source)
     const bool fp16win = depth && !win.none_valid && win.lo + win.span <= 0x7BFEu;
+    const uint32_t whi = win.lo + win.span;
+    const bool centred = fp16win && whi < 2048u && ((win.lo + whi) & 1u) == 0;  // WINM 2
     auto pick = [&](auto frame_tag) {
         constexpr bool F = decltype(frame_tag)::value;
-        return depth_source ? lbp_hist_lane59_kernel<true, true, true, F>
-               : depth      ? (fp16win ? lbp_hist_lane59_kernel<true, false, true, F>
-                                       : lbp_hist_lane59_kernel<true, false, false, F>)
-                            : lbp_hist_lane59_kernel<false, false, false, F>;
+        if (depth_source)
+            return centred ? lbp_hist_lane59_kernel<true, true, 2, F>
+                           : lbp_hist_lane59_kernel<true, true, 1, F>;
+        if (depth)
+            return centred   ? lbp_hist_lane59_kernel<true, false, 2, F>
+                   : fp16win ? lbp_hist_lane59_kernel<true, false, 1, F>
+                             : lbp_hist_lane59_kernel<true, false, 0, F>;
+        return lbp_hist_lane59_kernel<false, false, 0, F>;
     };
     auto kern = frame ? pick(std::true_type{}) : pick(std::false_type{});
     const int smem = frame ? l59::Layout<true>::kSmemBytes : l59::Layout<false>::kSmemBytes;
