@@ -57,15 +57,17 @@ struct Layout {
     static constexpr int kStageBytes = kGreyBytes + 2 * kDepthW * kTile;
     static constexpr int kGroupOff = kStages * kStageBytes;
     static constexpr int kGroupBytes = FRAME ? kHistBytes : l59::kGroupBytes;
-    static constexpr int kLutOff = kGroupOff + kGroups * kGroupBytes;
-    static constexpr int kPlainLutOff = kLutOff + kLutBytes;
-    static constexpr int kBarOff = kPlainLutOff + 256;
-    static constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;  // + 128-B alignment slack
-    // headline: stages 3 x 49,152, groups 3 x 23,040 (counters + staging), LUT at 216,576;
-    // FRAME: stages 3 x 53,248, groups 3 x 15,360, LUT at 205,824
-    static_assert(kStageBytes % 128 == 0 && kGreyBytes % 128 == 0 && kLutOff % 256 == 0,
+    // the lane-banked LUT goes at the first offset >= kLutMin whose shared-window address is
+    // 0x6400 mod 2^16 (lut_placement): then the LUT address of a code offset t (a 16-bit half
+    // 0x6400 + ...) is (address - 0x6400) | t, one LOP3 / LEA.HI per half.  The plain LUT and
+    // the stage barriers follow it.
+    static constexpr int kLutMin = kGroupOff + kGroups * kGroupBytes;
+    static constexpr int kTailBytes = kLutBytes + 256 + kStages * 8 + 128;  // + align slack
+    // headline: stages 3 x 49,152, groups 3 x 23,040 (counters + staging), LUT >= 216,576;
+    // FRAME: stages 3 x 53,248, groups 3 x 15,360, LUT >= 205,824
+    static_assert(kStageBytes % 128 == 0 && kGreyBytes % 128 == 0 && kLutMin % 256 == 0,
                   "alignment");
-    static_assert(kSmemBytes <= 227 * 1024, "shared memory");
+    static_assert(kLutMin + kTailBytes <= 227 * 1024, "shared memory");
     static_assert(!FRAME || kStages == kGroups, "frame staging lives in the group's stage");
     static_assert(kDescBytes <= kGreyBytes, "staging fits a stage region");
 };
@@ -126,17 +128,17 @@ __device__ __forceinline__ LaneRow lane_row(uint32_t word_addr) {
 }
 
 // Eq. 2 for the centre pair c as the lane-banked LUT offset, per 16-bit half:
-// 0x6400 + (code & 3) + 128 * (code >> 2) with the Fig. 7 bits (TL 1, T 2, TR 4, R 8,
-// BR 16, B 32, BL 64, L 128).  TL, T, TR, R, BR: FMA pipe, sat(g_p - g_c + 1) in {0,1}
-// scaled by 1, 2, 128, 256, 512 onto 1024.0 (exact fp16 integers, sum <= 1923); B, BL, L:
-// ALU pipe, HSET2 masks at offsets 1024..4096.  The bias 0x6400 is an arithmetic constant
-// removed by the LUT base.
+// 0x6400 + 4 lane + (code & 3) + 128 * (code >> 2) with the Fig. 7 bits (TL 1, T 2, TR 4,
+// R 8, BR 16, B 32, BL 64, L 128).  TL, T, TR, R, BR: FMA pipe, sat(g_p - g_c + 1) in {0,1}
+// scaled by 1, 2, 128, 256, 512 onto base2 = 1024 + 4 lane (exact fp16 integers, sum <=
+// 1024 + 124 + 899 = 2047, so the bits are 0x6400 + the integer); B, BL, L: ALU pipe, HSET2
+// masks at offsets 1024..4096 (each half <= 0x6400 + 8191: no carry between halves).
 __device__ __forceinline__ uint32_t lbp_offset2(uint32_t c, uint32_t tl, uint32_t t, uint32_t tr,
                                                 uint32_t r, uint32_t br, uint32_t b, uint32_t bl,
-                                                uint32_t l) {
-    constexpr uint32_t kOne = 0x3C003C00u, kMinusOne = 0xBC00BC00u, k1024 = 0x64006400u;
+                                                uint32_t l, uint32_t base2) {
+    constexpr uint32_t kOne = 0x3C003C00u, kMinusOne = 0xBC00BC00u;
     const uint32_t negc1 = f16_fma(c, kMinusOne, kOne);                 // 1 - g_c
-    uint32_t f = f16_fma(f16_fma_sat(tl, kOne, negc1), kOne, k1024);   // TL +1
+    uint32_t f = f16_fma(f16_fma_sat(tl, kOne, negc1), kOne, base2);   // TL +1
     f = f16_fma(f16_fma_sat(t, kOne, negc1), 0x40004000u, f);          // T  +2
     f = f16_fma(f16_fma_sat(tr, kOne, negc1), 0x58005800u, f);         // TR +128
     f = f16_fma(f16_fma_sat(r, kOne, negc1), 0x5C005C00u, f);          // R  +256
@@ -144,7 +146,7 @@ __device__ __forceinline__ uint32_t lbp_offset2(uint32_t c, uint32_t tl, uint32_
     uint32_t a = hge2_mask(b, c) & 0x04000400u;                        // B  +1024
     a |= hge2_mask(bl, c) & 0x08000800u;                               // BL +2048
     a |= hge2_mask(l, c) & 0x10001000u;                                // L  +4096
-    return f + a;  // no carry between halves (each half <= 0x6400 + 8067)
+    return f + a;
 }
 
 // ---- depth source: codes on the u16 depth plane.  A u16 d <= 0x7BFF read as
@@ -205,8 +207,9 @@ __device__ __forceinline__ uint32_t hge2_one(uint32_t a, uint32_t b) {
 // fp16 integers <= 1923), B, BL, L as HSET2 masks at 1024..4096.
 __device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uint32_t t,
                                                     uint32_t tr, uint32_t r, uint32_t br,
-                                                    uint32_t b, uint32_t bl, uint32_t l) {
-    uint32_t f = f16_fma(hge2_one(tl, c), 0x3C003C00u, 0x64006400u);  // TL +1
+                                                    uint32_t b, uint32_t bl, uint32_t l,
+                                                    uint32_t base2) {
+    uint32_t f = f16_fma(hge2_one(tl, c), 0x3C003C00u, base2);        // TL +1
     f = f16_fma(hge2_one(t, c), 0x40004000u, f);                       // T  +2
     f = f16_fma(hge2_one(tr, c), 0x58005800u, f);                      // TR +128
     f = f16_fma(hge2_one(r, c), 0x5C005C00u, f);                       // R  +256
@@ -233,13 +236,14 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
                        lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
                        DepthWindow win, uint16_t* __restrict__ desc, int64_t desc_stride,
-                       int32_t* __restrict__ roi_status) {
+                       int32_t* __restrict__ roi_status, int32_t lut_off) {
     using namespace l59;
     using L = Layout<FRAME>;
     constexpr bool FP16WIN = WINM != 0;
     constexpr int kGreyBytes = L::kGreyBytes, kStageBytes = L::kStageBytes;
     constexpr int kGroupOff = L::kGroupOff, kGroupBytes = L::kGroupBytes;
-    constexpr int kLutOff = L::kLutOff, kPlainLutOff = L::kPlainLutOff, kBarOff = L::kBarOff;
+    const int kLutOff = lut_off, kPlainLutOff = lut_off + kLutBytes;  // (lut_placement)
+    const int kBarOff = kPlainLutOff + 256;
     // FRAME with grey codes and a depth mask: the staging overwrites the stage's grey rows, so
     // the next grey box is loaded only once the descriptor store has read the staging (the
     // depth box goes first); without depth it uses the unused depth region, for the depth
@@ -297,6 +301,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
     if (tid == 0) {
+        // the host placed the LUT from the device's reserved shared memory size; a mismatch
+        // would misaddress every lookup, so it stops the kernel (LBP_E_CUDA) instead
+        if ((smem_u32(smem + kLutOff) & 0xFFFFu) != 0x6400u) __trap();
         for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         prefetch_tensormap(&grey_map);
@@ -323,7 +330,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // WINM 1
     const uint32_t mid2 = ((2 * win.lo + win.span) / 2) * 0x10001u;                 // WINM 2
     const uint32_t half2 = (win.span / 2) * 0x10001u;
-    const uint32_t lut_lane = opaque(smem_u32(smem + kLutOff) + 4 * lane - 0x6400u);
+    // LUT address of an offset half t: lutb | t (the LUT sits at 0x6400 mod 2^16)
+    const uint32_t lutb = opaque(smem_u32(smem + kLutOff) - 0x6400u);
+    const uint32_t base2 = opaque((0x6400u + 4u * lane) * 0x10001u);  // 1024.0 + 4 lane
     const int i0 = (warp * (kTile - 2)) / 8;                   // first interior row of cell row
     const int nrows = ((warp + 1) * (kTile - 2)) / 8 - i0;     // 15 or 16
 
@@ -387,14 +396,14 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             uint32_t t0, t1;
             if constexpr (DEPTH_SRC) {
                 t0 = lbp_offset2_cmp(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
-                                     bot.lh0, mid.lh0);
+                                     bot.lh0, mid.lh0, base2);
                 t1 = lbp_offset2_cmp(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
-                                     bot.mh, mid.mh);
+                                     bot.mh, mid.mh, base2);
             } else {
                 t0 = lbp_offset2(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
-                                 bot.lh0, mid.lh0);
+                                 bot.lh0, mid.lh0, base2);
                 t1 = lbp_offset2(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
-                                 bot.mh, mid.mh);
+                                 bot.mh, mid.mh, base2);
             }
             uint32_t val[4];
             if constexpr (HAS_DEPTH && FP16WIN) {
@@ -435,8 +444,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
 #pragma unroll
                 for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
             }
-            const uint32_t la[4] = {lut_lane + (t0 & 0xFFFFu), __umulhi(t0, 0x10000u) + lut_lane,
-                                    lut_lane + (t1 & 0xFFFFu), __umulhi(t1, 0x10000u) + lut_lane};
+            const uint32_t la[4] = {lutb | (t0 & 0xFFFFu), __umulhi(t0, 0x10000u) + lutb,
+                                    lutb | (t1 & 0xFFFFu), __umulhi(t1, 0x10000u) + lutb};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const uint32_t bin = ld_shared_u8(la[k]);
@@ -508,6 +517,27 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     if (gtid == 0 && pending >= 0) bulk_wait_all();
 }
 
+// Offset of the lane-banked LUT in the dynamic shared memory: the first offset >= lut_min
+// whose shared-window address is 0x6400 mod 2^16.  Dynamic shared memory starts at the
+// device's reserved shared memory per block (these kernels have no static shared memory),
+// and the kernel rounds its base up to 128 B.  False if the layout does not fit.
+inline bool lut_placement(int lut_min, int tail_bytes, int* lut_off, int* smem_bytes) {
+    static const int reserved = []() {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, dev) !=
+                cudaSuccess)
+            return -1;
+        return v;
+    }();
+    if (reserved < 0) return false;
+    const int base = (reserved + 127) & ~127;
+    const int off = lut_min + (((0x6400 - base - lut_min) % 65536) + 65536) % 65536;
+    *lut_off = off;
+    *smem_bytes = off + tail_bytes;
+    return *smem_bytes <= 227 * 1024;
+}
+
 inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* depth,
                                           const lbp_images_t& geom, const lbp_roi_t* rois,
                                           int32_t n_rois, const DepthWindow& win, uint16_t* desc,
@@ -544,12 +574,15 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
         return lbp_hist_lane59_kernel<false, false, 0, F>;
     };
     auto kern = frame ? pick(std::true_type{}) : pick(std::false_type{});
-    const int smem = frame ? l59::Layout<true>::kSmemBytes : l59::Layout<false>::kSmemBytes;
+    int lut_off = 0, smem = 0;
+    if (!lut_placement(frame ? l59::Layout<true>::kLutMin : l59::Layout<false>::kLutMin,
+                       l59::Layout<false>::kTailBytes, &lut_off, &smem))
+        return cudaErrorNotSupported;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(sms, n_rois));
     kern<<<grid, l59::kThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win,
-                                                 desc, desc_stride, roi_status);
+                                                 desc, desc_stride, roi_status, lut_off);
     return cudaGetLastError();
 }
 
