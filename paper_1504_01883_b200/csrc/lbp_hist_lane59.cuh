@@ -107,6 +107,12 @@ __device__ __forceinline__ uint32_t f16_fma(uint32_t a, uint32_t b, uint32_t c) 
     return r;
 }
 
+__device__ __forceinline__ uint32_t hsub2_sat(uint32_t a, uint32_t b) {
+    uint32_t r;  // sat(a - b) per half
+    asm("sub.rn.sat.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 struct LaneRow {
     uint32_t h0, h1;        // fp16x2 1024+g of columns (4l, 4l+1), (4l+2, 4l+3)
     uint32_t lh0, mh, rh1;  // (4l-1, 4l), (4l+1, 4l+2), (4l+3, 4l+4)
@@ -135,14 +141,14 @@ __device__ __forceinline__ LaneRow lane_row(uint32_t word_addr) {
 // masks at offsets 1024..4096 (each half <= 0x6400 + 8191: no carry between halves).
 __device__ __forceinline__ uint32_t lbp_offset2(uint32_t c, uint32_t tl, uint32_t t, uint32_t tr,
                                                 uint32_t r, uint32_t br, uint32_t b, uint32_t bl,
-                                                uint32_t l, uint32_t base2) {
-    constexpr uint32_t kOne = 0x3C003C00u, kMinusOne = 0xBC00BC00u;
-    const uint32_t negc1 = f16_fma(c, kMinusOne, kOne);                 // 1 - g_c
-    uint32_t f = f16_fma(f16_fma_sat(tl, kOne, negc1), kOne, base2);   // TL +1
-    f = f16_fma(f16_fma_sat(t, kOne, negc1), 0x40004000u, f);          // T  +2
-    f = f16_fma(f16_fma_sat(tr, kOne, negc1), 0x58005800u, f);         // TR +128
-    f = f16_fma(f16_fma_sat(r, kOne, negc1), 0x5C005C00u, f);          // R  +256
-    f = f16_fma(f16_fma_sat(br, kOne, negc1), 0x60006000u, f);         // BR +512 (<= 2047)
+                                                uint32_t l, uint32_t top2) {
+    // [g_p >= g_c] = 1 - sat(g_c - g_p) (integers): start from top2 = base2 + 899 (all five
+    // bits set) and subtract w_p sat(g_c - g_p) -- one HADD2.SAT per bit, no 1 - g_c term
+    uint32_t f = f16_fma(hsub2_sat(c, tl), 0xBC00BC00u, top2);        // TL -1
+    f = f16_fma(hsub2_sat(c, t), 0xC000C000u, f);                      // T  -2
+    f = f16_fma(hsub2_sat(c, tr), 0xD800D800u, f);                     // TR -128
+    f = f16_fma(hsub2_sat(c, r), 0xDC00DC00u, f);                      // R  -256
+    f = f16_fma(hsub2_sat(c, br), 0xE000E000u, f);                     // BR -512 (>= base2)
     uint32_t a = hge2_mask(b, c) & 0x04000400u;                        // B  +1024
     a |= hge2_mask(bl, c) & 0x08000800u;                               // BL +2048
     a |= hge2_mask(l, c) & 0x10001000u;                                // L  +4096
@@ -333,6 +339,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     // LUT address of an offset half t: lutb | t (the LUT sits at 0x6400 mod 2^16)
     const uint32_t lutb = opaque(smem_u32(smem + kLutOff) - 0x6400u);
     const uint32_t base2 = opaque((0x6400u + 4u * lane) * 0x10001u);  // 1024.0 + 4 lane
+    const uint32_t top2 = opaque((0x6400u + 4u * lane + 899u) * 0x10001u);  // + TL..BR
     const int i0 = (warp * (kTile - 2)) / 8;                   // first interior row of cell row
     const int nrows = ((warp + 1) * (kTile - 2)) / 8 - i0;     // 15 or 16
 
@@ -401,9 +408,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                                      bot.mh, mid.mh, base2);
             } else {
                 t0 = lbp_offset2(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
-                                 bot.lh0, mid.lh0, base2);
+                                 bot.lh0, mid.lh0, top2);
                 t1 = lbp_offset2(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
-                                 bot.mh, mid.mh, base2);
+                                 bot.mh, mid.mh, top2);
             }
             uint32_t val[4];
             if constexpr (HAS_DEPTH && FP16WIN) {
