@@ -421,6 +421,7 @@ def main():
                 "extraction (" + args.source + " source)", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak if peak else None,
                 "peak_source": peak_src, "bytes_per_crop": bpc,
+                "frac_of_nominal_8000": achieved / 8000.0,  # also vs 8 TB/s
                 "kernel_ms": ext_ms, "kernel_share_of_step": ext_ms / ms_per_step,
                 "traffic": load_traffic(args.workload) if source == 0 else None}
 
