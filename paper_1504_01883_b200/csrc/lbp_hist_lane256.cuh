@@ -1,0 +1,308 @@
+// lbp_hist_lane256.cuh -- the lane-private design of lbp_hist_lane59.cuh for the full 256-bin
+// histogram ("0-255"; bins = 256, 8x8 cells, 128x128 ROIs at 16-px aligned x): no LUT --
+// the code arithmetic produces the counter address itself.
+//
+//  * counters: u32 words [cell-row group g][bin 0..255 + dummy][lane], 4 cell rows per word
+//    as bytes (as lane59), 2 x 257 x 128 B = 65,792 B per 8-warp group;
+//  * codes: per 16-bit half t = 0x6400 + 4 col + 128 code (col = the pixel's counter lane:
+//    its own lane, or the first lane of the neighbouring cell for a spill-over column), built
+//    as in lane59: TL, T, TR (weights 128, 256, 512) on the FMA pipe as 1 - sat(g_c - g_p)
+//    accumulated down from 1024 + 4 col + 896 (exact fp16 integers <= 2044), R, BR, B, BL, L
+//    (1024 .. 16384) as HSET2 masks on the bits; the counter address is group base - 0x6400
+//    + t, and a masked-out pixel gets t of a dummy bin 256 in its own lane, so the update
+//    needs no select;
+//  * 2 groups x 8 warps, 2 TMA stages (stage == group: grey 16 KB + depth 32 KB); the 32-KB
+//    descriptor is staged in the stage's depth region after the rows are consumed (no room
+//    elsewhere; cell rows of 512 B with the 16-B chunks XOR-swizzled by cell x, so the
+//    epilogue's 8 cell-x lanes store to distinct banks), copied out by the group with 16-B
+//    loads and coalesced 16-B global stores; the next crop's grey box is issued at once,
+//    its depth box after the copy-out;
+//  * the per-pixel work is the code, one address op and one red.shared (lane59 also reads the
+//    LUT byte and forms the counter address): 59 instructions per lane-row.
+#pragma once
+#include "lbp_hist_lane59.cuh"
+
+namespace lbpf {
+
+namespace l256 {
+constexpr int kGroups = 2;
+constexpr int kGroupThreads = 256;
+constexpr int kThreads = kGroups * kGroupThreads;
+constexpr int kTile = 128;
+constexpr int kBins = 256;
+constexpr int kRows = kBins + 1;                             // + the dummy bin row
+constexpr int kStages = 2;
+constexpr int kGreyBytes = kTile * kTile;                    // 16,384
+constexpr int kStageBytes = kGreyBytes + 2 * kTile * kTile;  // 49,152
+constexpr int kHistBytes = 2 * kRows * 32 * 4;               // 65,792
+constexpr int kDescBytes = 64 * kBins * 2;                   // 32,768 (staged in the depth box)
+constexpr int kGroupOff = kStages * kStageBytes;             // 98,304
+constexpr int kLutOff = kGroupOff + kGroups * kHistBytes;    // 229,888: identity LUT (generic)
+constexpr int kBarOff = kLutOff + 256;
+constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;      // + 128-B alignment slack
+static_assert(kSmemBytes <= 227 * 1024, "shared memory");
+static_assert(kDescBytes <= kStageBytes - kGreyBytes, "staging fits the depth region");
+static_assert(kStages == kGroups, "stage == group");
+}  // namespace l256
+
+// Eq. 2 as the counter-address half 0x6400 + 4 col + 128 code (see the header)
+__device__ __forceinline__ uint32_t lbp_addr2_256(uint32_t c, uint32_t tl, uint32_t t,
+                                                  uint32_t tr, uint32_t r, uint32_t br,
+                                                  uint32_t b, uint32_t bl, uint32_t l,
+                                                  uint32_t top2) {
+    uint32_t f = f16_fma(hsub2_sat(c, tl), 0xD800D800u, top2);  // TL -128
+    f = f16_fma(hsub2_sat(c, t), 0xDC00DC00u, f);                // T  -256
+    f = f16_fma(hsub2_sat(c, tr), 0xE000E000u, f);               // TR -512
+    uint32_t a = hge2_mask(r, c) & 0x04000400u;                  // R  +1024
+    a |= hge2_mask(br, c) & 0x08000800u;                         // BR +2048
+    a |= hge2_mask(b, c) & 0x10001000u;                          // B  +4096
+    a |= hge2_mask(bl, c) & 0x20002000u;                         // BL +8192
+    a |= hge2_mask(l, c) & 0x40004000u;                          // L  +16384
+    return f + a;  // each half <= 0x6400 + 124 + 32640: no carry between halves
+}
+
+template <bool HAS_DEPTH, int WINM>
+__global__ void __launch_bounds__(l256::kThreads, 1)
+lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
+                        const __grid_constant__ CUtensorMap depth_map,
+                        const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
+                        lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
+                        DepthWindow win, uint16_t* __restrict__ desc, int64_t desc_stride,
+                        int32_t* __restrict__ roi_status) {
+    using namespace l256;
+    constexpr bool FP16WIN = HAS_DEPTH && WINM != 0;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                               ~uintptr_t(127));
+    const int tid = threadIdx.x;
+    const int group = tid / kGroupThreads, gtid = tid % kGroupThreads;
+    const int warp = gtid >> 5, lane = gtid & 31;
+    const uint32_t stages0 = smem_u32(smem);
+    const uint32_t hist0 = stages0 + kGroupOff + group * kHistBytes;
+    const uint32_t staging = stages0 + group * kStageBytes + kGreyBytes;  // the depth region
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+    const uint32_t bar_id = 1 + group;
+
+    const int n_pos = (n_rois > (int)blockIdx.x) ? (n_rois - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    auto crop_of = [&](int i) -> int32_t { return (int32_t)blockIdx.x + i * (int32_t)gridDim.x; };
+    // part bit 1: arrive + expect the stage's bytes + the grey box; bit 2: the depth box
+    // (late: the staging lives in the depth region)
+    auto issue = [&](int i, int part) {
+        if (i >= n_pos) return;
+        const int s = i % kStages;
+        const lbp_roi_t r = rois[crop_of(i)];
+        if (roi_is_fast(r, geom)) {
+            uint8_t* st = smem + s * kStageBytes;
+            if (part & 1) {
+                mbar_arrive_expect_tx(&bars[s], HAS_DEPTH ? kStageBytes : kGreyBytes);
+                tma_load_3d(st, &grey_map, &bars[s], r.x, r.y, r.img);
+            }
+            if (HAS_DEPTH && (part & 2))
+                tma_load_3d(st + kGreyBytes, &depth_map, &bars[s], r.x, r.y, r.img);
+        } else if (part & 1) {
+            mbar_arrive(&bars[s]);
+        }
+    };
+
+    // ---- one-time setup: identity LUT (generic path), zero counters, barriers, first stages
+    if (tid < 256) smem[kLutOff + tid] = (uint8_t)tid;
+    for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
+        st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        prefetch_tensormap(&grey_map);
+        if (HAS_DEPTH) prefetch_tensormap(&depth_map);
+        for (int i = 0; i < kStages; ++i) issue(i, 3);
+    }
+    __syncthreads();
+
+    // ---- per-lane / per-warp constants
+    const uint32_t byte_mult = 1u << (8 * (warp & 3));
+    uint32_t mult[4], mult_row[4], colk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int x = 4 * lane + k;
+        const bool inner = (x != 0) && (x != kTile - 1);  // the 1-px ROI border has no code
+        const int cx = inner ? (8 * x - 1) / (kTile - 2) : (lane >> 2);
+        colk[k] = (cx == (lane >> 2)) ? lane : 4 * cx;  // spill-over -> next cell's lane
+        mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
+        mult_row[k] = mult[k];
+    }
+    // start values (all of TL, T, TR set) and dummy-bin addresses per pixel pair
+    const uint32_t top_a = opaque(((0x6400u + 4u * colk[0] + 896u)) |
+                                  ((0x6400u + 4u * colk[1] + 896u) << 16));
+    const uint32_t top_b = opaque(((0x6400u + 4u * colk[2] + 896u)) |
+                                  ((0x6400u + 4u * colk[3] + 896u) << 16));
+    const uint32_t dum_a = (0x6400u + 128u * kBins + 4u * colk[0]) |
+                           ((0x6400u + 128u * kBins + 4u * colk[1]) << 16);
+    const uint32_t dum_b = (0x6400u + 128u * kBins + 4u * colk[2]) |
+                           ((0x6400u + 128u * kBins + 4u * colk[3]) << 16);
+    const uint32_t gbase = opaque(hist0 + (uint32_t)((warp >> 2) * kRows * 128) - 0x6400u);
+    const uint32_t lo16 = win.lo << 16;
+    const uint32_t span16 = (win.span << 16) | 0xFFFFu;
+    const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // WINM 1
+    const uint32_t mid2 = ((2 * win.lo + win.span) / 2) * 0x10001u;                 // WINM 2
+    const uint32_t half2 = (win.span / 2) * 0x10001u;
+    const int i0 = (warp * (kTile - 2)) / 8;
+    const int nrows = ((warp + 1) * (kTile - 2)) / 8 - i0;
+
+    struct GroupSync {
+        uint32_t id;
+        __device__ __forceinline__ void operator()() const {
+            named_barrier_sync(id, l256::kGroupThreads);
+        }
+    };
+
+    for (int i = group; i < n_pos; i += kGroups) {
+        const int32_t n = crop_of(i);
+        const lbp_roi_t roi = rois[n];
+        const int s = i % kStages;
+        mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
+        if (!roi_is_fast(roi, geom)) {
+            if (gtid == 0) issue(i + kStages, 3);  // stage s was never filled: release it
+            extract_roi_generic<kBins, kGroupThreads>(
+                CodePlane<uint8_t>{grey, geom.grey_pitch, geom.grey_img_stride},
+                HAS_DEPTH ? depth : nullptr, geom, roi, n, win, 8, 8, desc, desc_stride,
+                roi_status, reinterpret_cast<uint32_t*>(smem + (hist0 - stages0)),
+                kHistBytes / 4, smem + kLutOff, 0, gtid, GroupSync{bar_id});
+            named_barrier_sync(bar_id, kGroupThreads);
+            continue;
+        }
+        const uint32_t st = stages0 + s * kStageBytes;
+        const uint32_t g0 = opaque(st + i0 * kTile + 4 * lane);
+        const uint32_t d0 = opaque(st + kGreyBytes + (i0 + 1) * (kTile * 2) + 8 * lane);
+
+        auto do_row = [&](const LaneRow& top, const LaneRow& mid, const LaneRow& bot, int j) {
+            uint32_t t0 = lbp_addr2_256(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
+                                        bot.lh0, mid.lh0, top_a);
+            uint32_t t1 = lbp_addr2_256(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
+                                        bot.mh, mid.mh, top_b);
+            uint32_t val[4];
+            if constexpr (FP16WIN) {  // (the window tests of lane59's WINM 1 / 2)
+                const uint2 d = ld_shared_u32x2(d0 + j * (kTile * 2));
+                uint32_t m0, m1;
+                if constexpr (WINM == 2) {
+                    m0 = hle2_mask(habsdiff2(d.x, mid2), half2);
+                    m1 = hle2_mask(habsdiff2(d.y, mid2), half2);
+                } else {
+                    m0 = hge2_mask(d.x, lo2) & hle2_mask(d.x, hi2);
+                    m1 = hge2_mask(d.y, lo2) & hle2_mask(d.y, hi2);
+                }
+                t0 = (t0 & m0) | (dum_a & ~m0);
+                t1 = (t1 & m1) | (dum_b & ~m1);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
+            } else if (HAS_DEPTH) {
+                const uint2 d = ld_shared_u32x2(d0 + j * (kTile * 2));
+                const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
+                                       d.y - lo16};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) val[k] = (x[k] <= span16) ? mult_row[k] : 0u;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
+            }
+            const uint32_t a[4] = {gbase + (t0 & 0xFFFFu), __umulhi(t0, 0x10000u) + gbase,
+                                   gbase + (t1 & 0xFFFFu), __umulhi(t1, 0x10000u) + gbase};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) red_shared_add(a[k], val[k]);
+        };
+        LaneRow r0 = lane_row(g0), r1 = lane_row(g0 + kTile), r2;
+#pragma unroll
+        for (int j = 0; j < 15; j += 3) {
+            r2 = lane_row(g0 + (j + 2) * kTile); do_row(r0, r1, r2, j);
+            r0 = lane_row(g0 + (j + 3) * kTile); do_row(r1, r2, r0, j + 1);
+            r1 = lane_row(g0 + (j + 4) * kTile); do_row(r2, r0, r1, j + 2);
+        }
+        if (nrows < 16) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
+        }
+        r2 = lane_row(g0 + 17 * kTile);
+        do_row(r0, r1, r2, 15);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
+
+        named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
+        if (gtid == 0) {
+            issue(i + kStages, 1);  // the grey box (its region is free)
+            if (roi_status) roi_status[n] = LBP_OK;
+        }
+        // ---- epilogue: quad q = (g, bin, cx) as lane59 (conflict-free 16-B counter loads);
+        // counts go to the swizzled staging; the dummy row is only re-zeroed
+        for (int q = gtid; q < 2 * kRows * 8; q += kGroupThreads) {
+            const uint32_t qa = hist0 + q * 16;
+            const int g = q / (kRows * 8), rem = q - g * (kRows * 8);
+            const int bin = rem >> 3, cx = rem & 7;
+            if (bin == kBins) {
+                st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+                continue;
+            }
+            const uint4 w = ld_shared_u32x4(qa);
+            st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+            const uint32_t lo01 = prmt(w.x, w.y, 0x5140), hi01 = prmt(w.x, w.y, 0x7362);
+            const uint32_t lo23 = prmt(w.z, w.w, 0x5140), hi23 = prmt(w.z, w.w, 0x7362);
+            const uint32_t c0 = __dp4a(prmt(lo01, lo23, 0x5410), 0x01010101u, 0u);
+            const uint32_t c1 = __dp4a(prmt(lo01, lo23, 0x7632), 0x01010101u, 0u);
+            const uint32_t c2 = __dp4a(prmt(hi01, hi23, 0x5410), 0x01010101u, 0u);
+            const uint32_t c3 = __dp4a(prmt(hi01, hi23, 0x7632), 0x01010101u, 0u);
+            const uint32_t o = staging + ((4 * g) * 8 + cx) * (kBins * 2) +
+                               ((2u * bin) ^ ((uint32_t)cx << 4));
+            constexpr uint32_t kRow = 8 * kBins * 2;
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "h"((uint16_t)c0) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + kRow), "h"((uint16_t)c1) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 2 * kRow), "h"((uint16_t)c2) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 3 * kRow), "h"((uint16_t)c3) : "memory");
+        }
+        named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
+        {  // copy-out: 2,048 chunks of 16 B, un-swizzled, coalesced
+            uint16_t* out = desc + (int64_t)n * desc_stride;
+#pragma unroll 4
+            for (int idx = gtid; idx < kDescBytes / 16; idx += kGroupThreads) {
+                const int cell = idx >> 5, chunk = idx & 31;
+                const uint4 v = ld_shared_u32x4(staging + cell * (kBins * 2) +
+                                                ((chunk * 16) ^ ((cell & 7) << 4)));
+                *reinterpret_cast<uint4*>(out + cell * kBins + chunk * 8) = v;
+            }
+        }
+        fence_proxy_async_smem();                   // generic reads before the TMA overwrite
+        named_barrier_sync(bar_id, kGroupThreads);  // C: staging read
+        if (gtid == 0) issue(i + kStages, 2);       // the depth box into the staging region
+    }
+}
+
+inline cudaError_t launch_lbp_hist_lane256(const uint8_t* grey, const uint16_t* depth,
+                                           const lbp_images_t& geom, const lbp_roi_t* rois,
+                                           int32_t n_rois, const DepthWindow& win,
+                                           uint16_t* desc, int64_t desc_stride,
+                                           int32_t* roi_status, int sms, cudaStream_t stream) {
+    CUtensorMap gm, dm;
+    if (!encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
+                          geom.grey_img_stride))
+        return cudaErrorNotSupported;
+    if (depth) {
+        if (!encode_stack_map(&dm, depth, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, geom,
+                              geom.depth_pitch, geom.depth_img_stride))
+            return cudaErrorNotSupported;
+    } else {
+        dm = gm;
+    }
+    const bool fp16win = depth && !win.none_valid && win.lo + win.span <= 0x7BFEu;
+    const uint32_t whi = win.lo + win.span;
+    const bool centred = fp16win && whi < 2048u && ((win.lo + whi) & 1u) == 0;
+    auto kern = !depth    ? lbp_hist_lane256_kernel<false, 0>
+                : centred ? lbp_hist_lane256_kernel<true, 2>
+                : fp16win ? lbp_hist_lane256_kernel<true, 1>
+                          : lbp_hist_lane256_kernel<true, 0>;
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l256::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    const int grid = std::max(1, std::min(sms, n_rois));
+    kern<<<grid, l256::kThreads, l256::kSmemBytes, stream>>>(gm, dm, grey, depth, geom, rois,
+                                                            n_rois, win, desc, desc_stride,
+                                                            roi_status);
+    return cudaGetLastError();
+}
+
+}  // namespace lbpf

@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "lbp_hist_generic.cuh"
 #include "ptx.cuh"
+#include "tma_util.cuh"
 
 namespace lbpf {
 

@@ -6,8 +6,9 @@
 #include "common.cuh"
 #include "desc_pack.cuh"
 #include "lbp_hist_generic.cuh"
-#include "lbp_hist_fast.cuh"
+#include "tma_util.cuh"
 #include "lbp_hist_lane59.cuh"
+#include "lbp_hist_lane256.cuh"
 #include "lbp_resize.cuh"
 #include "lbp_recognize.cuh"
 #include "svm_fp64.cuh"
@@ -101,13 +102,17 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
         // that are not fully-inside 128x128 boxes take the generic code path inside it.
         if (fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc) &&
             ((desc_stride * 2) & 15) == 0) {
-            if (bins == 59)  // conflict-free lane-private kernel (the headline configuration)
-                return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win,
-                                                            desc, desc_stride, roi_status,
-                                                            num_sms(), stream, false, frame));
-            return launch_status(launch_lbp_hist_fast(grey, depth, geom, rois, n_rois, win, bins,
-                                                      desc, desc_stride, roi_status, num_sms(),
-                                                      stream));
+            // conflict-free lane-private kernels (59 bins: the headline configuration).
+            // cudaErrorNotSupported = refused on the host before any launch (a tensor map
+            // that cannot be encoded, a shared-memory layout that does not fit): the generic
+            // kernel below takes the batch.
+            const cudaError_t e =
+                bins == 59 ? launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win, desc,
+                                                    desc_stride, roi_status, num_sms(), stream,
+                                                    false, frame)
+                           : launch_lbp_hist_lane256(grey, depth, geom, rois, n_rois, win, desc,
+                                                     desc_stride, roi_status, num_sms(), stream);
+            if (e != cudaErrorNotSupported) return launch_status(e);
         }
     }
     // depth source, headline geometry: the same TMA kernel with the codes on the depth tile
@@ -115,10 +120,12 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
     if (depth_source && !small_batch && bins == 59 && win.span + win.lo <= 0x7BFEu &&
         !win.none_valid &&
         fast_path_applicable(geom, nullptr, depth, cells_x, cells_y, bins, desc) &&
-        ((desc_stride * 2) & 15) == 0)
-        return launch_status(launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win, desc,
-                                                    desc_stride, roi_status, num_sms(), stream,
-                                                    true, frame));
+        ((desc_stride * 2) & 15) == 0) {
+        const cudaError_t e = launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win, desc,
+                                                     desc_stride, roi_status, num_sms(), stream,
+                                                     true, frame);
+        if (e != cudaErrorNotSupported) return launch_status(e);
+    }
     // one CTA per (ROI, cell row) unit, grid-strided
     const int grid = (int)std::min<int64_t>((int64_t)n_rois * cells_y, (int64_t)num_sms() * 8);
     if (depth_source) {

@@ -14,7 +14,7 @@ if [ "${NCU:-0}" = "1" ]; then
   CMD="python bench.py --steps 3 --warmup 3 --skip-cpu --e2e-steps 1 $BENCH_ARGS"
   timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-  for K in ${NCU_KERNELS:-lbp_hist_fast svm_gemm}; do
+  for K in ${NCU_KERNELS:-lbp_hist_lane59 svm_gemm_kernel}; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s ${NCU_SKIP:-3} -c 1 -o gpurun_out/prof_$K $CMD > gpurun_out/ncu_full_$K.log 2>&1; echo "ncu full $K rc=$?"; tail -2 gpurun_out/ncu_full_$K.log
   done
 fi
