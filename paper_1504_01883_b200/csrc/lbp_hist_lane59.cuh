@@ -389,18 +389,38 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const uint32_t g0 = DEPTH_SRC ? opaque(st + kGreyBytes + i0 * kDRow + 8 * lane + (od2 & ~3u))
                                       : opaque(st + i0 * L::kGreyW + 4 * lane + (og & ~3u));
         const uint32_t d0 = opaque(st + kGreyBytes + (i0 + 1) * kDRow + 8 * lane + (od2 & ~3u));
-        auto load_depth = [&](uint32_t addr) {
-            if constexpr (FRAME) return ld_shared_funnel2(addr, dsel);
-            else return ld_shared_u32x2(addr);
+        // Raw shared-memory words of a row are loaded one row AHEAD of their use (the loop
+        // below is fully unrolled): a row's loads are issued before the previous row's
+        // counter updates, so their latency overlaps a whole row of arithmetic.
+        struct Raw { uint32_t a, b, c; };
+        auto raw_depth = [&](uint32_t addr) {  // 8 depth bytes of the lane (FRAME: 3 words)
+            Raw w{0u, 0u, 0u};
+            if constexpr (FRAME) {
+                w.a = ld_shared_u32(addr); w.b = ld_shared_u32(addr + 4); w.c = ld_shared_u32(addr + 8);
+            } else {
+                const uint2 v = ld_shared_u32x2(addr);
+                w.a = v.x; w.b = v.y;
+            }
+            return w;
         };
-        auto load_row = [&](uint32_t addr) {
-            if constexpr (DEPTH_SRC) return depth_row_w(load_depth(addr));
-            else if constexpr (FRAME) return lane_row_w(ld_shared_funnel1(addr, gsel));
-            else return lane_row(addr);
+        auto depth_words = [&](const Raw& w) {
+            if constexpr (FRAME) return make_uint2(prmt(w.a, w.b, dsel), prmt(w.b, w.c, dsel));
+            else return make_uint2(w.a, w.b);
         };
-        using Row = decltype(load_row(0u));
+        auto raw_row = [&](uint32_t addr) {
+            if constexpr (DEPTH_SRC) return raw_depth(addr);
+            Raw w{ld_shared_u32(addr), 0u, 0u};
+            if constexpr (FRAME) w.b = ld_shared_u32(addr + 4);
+            return w;
+        };
+        auto build_row = [&](const Raw& w) {
+            if constexpr (DEPTH_SRC) return depth_row_w(depth_words(w));
+            else if constexpr (FRAME) return lane_row_w(prmt(w.a, w.b, gsel));
+            else return lane_row_w(w.a);
+        };
+        using Row = decltype(build_row(Raw{}));
 
-        auto do_row = [&](const Row& top, const Row& mid, const Row& bot, int j) {
+        auto do_row = [&](const Row& top, const Row& mid, const Row& bot, const Raw& dc) {
             uint32_t t0, t1;
             if constexpr (DEPTH_SRC) {
                 t0 = lbp_offset2_cmp(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
@@ -423,7 +443,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                     c0 = mid.raw0;
                     c1 = mid.raw1;
                 } else {
-                    const uint2 d = load_depth(d0 + j * kDRow);
+                    const uint2 d = depth_words(dc);
                     c0 = d.x;
                     c1 = d.y;
                 }
@@ -442,7 +462,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             } else if (HAS_DEPTH) {
                 uint2 d;
                 if constexpr (DEPTH_SRC) d = make_uint2(mid.raw0, mid.raw1);  // centre row
-                else d = load_depth(d0 + j * kDRow);
+                else d = depth_words(dc);
                 // depth window on a u16 in either half of a word
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
@@ -462,19 +482,26 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         };
         // 16 rows, straight-line.  Cell rows with 15 rows run a 16th dummy row whose
         // increments are 0 (its pixels belong to the next warp; its rows exist in the crop).
-        Row r0 = load_row(g0), r1 = load_row(g0 + kRowStep), r2;
+        constexpr bool kMaskRow = HAS_DEPTH && !DEPTH_SRC;  // a separate depth centre row
+        Row r0 = build_row(raw_row(g0)), r1 = build_row(raw_row(g0 + kRowStep));
+        Raw wn = raw_row(g0 + 2 * kRowStep), dn{0u, 0u, 0u};
+        if constexpr (kMaskRow) dn = raw_depth(d0);
 #pragma unroll
-        for (int j = 0; j < 15; j += 3) {
-            r2 = load_row(g0 + (j + 2) * kRowStep); do_row(r0, r1, r2, j);
-            r0 = load_row(g0 + (j + 3) * kRowStep); do_row(r1, r2, r0, j + 1);
-            r1 = load_row(g0 + (j + 4) * kRowStep); do_row(r2, r0, r1, j + 2);
-        }
-        if (nrows < 16) {
+        for (int j = 0; j < 16; ++j) {
+            const Raw wc = wn, dc = dn;
+            if (j < 15) {
+                wn = raw_row(g0 + (j + 3) * kRowStep);
+                if constexpr (kMaskRow) dn = raw_depth(d0 + (j + 1) * kDRow);
+            }
+            if (j == 15 && nrows < 16) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
+                for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
+            }
+            const Row r2 = build_row(wc);
+            do_row(r0, r1, r2, dc);
+            r0 = r1;
+            r1 = r2;
         }
-        r2 = load_row(g0 + 17 * kRowStep);
-        do_row(r0, r1, r2, 15);
 #pragma unroll
         for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
 
