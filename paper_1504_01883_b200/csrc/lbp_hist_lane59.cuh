@@ -420,6 +420,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         };
         using Row = decltype(build_row(Raw{}));
 
+        // a row's counter updates are issued one row later (Pend: its bins and increments),
+        // so the LUT-byte loads' latency overlaps the next row's arithmetic
+        struct Pend { uint32_t bin[4], val[4]; };
         auto do_row = [&](const Row& top, const Row& mid, const Row& bot, const Raw& dc) {
             uint32_t t0, t1;
             if constexpr (DEPTH_SRC) {
@@ -474,17 +477,24 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             }
             const uint32_t la[4] = {lutb | (t0 & 0xFFFFu), __umulhi(t0, 0x10000u) + lutb,
                                     lutb | (t1 & 0xFFFFu), __umulhi(t1, 0x10000u) + lutb};
+            Pend p;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t bin = ld_shared_u8(la[k]);
-                red_shared_add(colb[k] + bin * (32 * 4), val[k]);
+                p.bin[k] = ld_shared_u8(la[k]);
+                p.val[k] = val[k];
             }
+            return p;
+        };
+        auto flush = [&](const Pend& p) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) red_shared_add(colb[k] + p.bin[k] * (32 * 4), p.val[k]);
         };
         // 16 rows, straight-line.  Cell rows with 15 rows run a 16th dummy row whose
         // increments are 0 (its pixels belong to the next warp; its rows exist in the crop).
         constexpr bool kMaskRow = HAS_DEPTH && !DEPTH_SRC;  // a separate depth centre row
         Row r0 = build_row(raw_row(g0)), r1 = build_row(raw_row(g0 + kRowStep));
         Raw wn = raw_row(g0 + 2 * kRowStep), dn{0u, 0u, 0u};
+        Pend pend;
         if constexpr (kMaskRow) dn = raw_depth(d0);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -498,10 +508,13 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
             }
             const Row r2 = build_row(wc);
-            do_row(r0, r1, r2, dc);
+            const Pend p = do_row(r0, r1, r2, dc);
+            if (j > 0) flush(pend);
+            pend = p;
             r0 = r1;
             r1 = r2;
         }
+        flush(pend);
 #pragma unroll
         for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
 
