@@ -173,14 +173,14 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         const uint32_t g0 = opaque(st + i0 * kTile + 4 * lane);
         const uint32_t d0 = opaque(st + kGreyBytes + (i0 + 1) * (kTile * 2) + 8 * lane);
 
-        auto do_row = [&](const LaneRow& top, const LaneRow& mid, const LaneRow& bot, int j) {
+        auto do_row = [&](const LaneRow& top, const LaneRow& mid, const LaneRow& bot,
+                          const uint2 d) {
             uint32_t t0 = lbp_addr2_256(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
                                         bot.lh0, mid.lh0, top_a);
             uint32_t t1 = lbp_addr2_256(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
                                         bot.mh, mid.mh, top_b);
             uint32_t val[4];
             if constexpr (FP16WIN) {  // (the window tests of lane59's WINM 1 / 2)
-                const uint2 d = ld_shared_u32x2(d0 + j * (kTile * 2));
                 uint32_t m0, m1;
                 if constexpr (WINM == 2) {
                     m0 = hle2_mask(habsdiff2(d.x, mid2), half2);
@@ -194,7 +194,6 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
 #pragma unroll
                 for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
             } else if (HAS_DEPTH) {
-                const uint2 d = ld_shared_u32x2(d0 + j * (kTile * 2));
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
 #pragma unroll
@@ -208,19 +207,28 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
 #pragma unroll
             for (int k = 0; k < 4; ++k) red_shared_add(a[k], val[k]);
         };
-        LaneRow r0 = lane_row(g0), r1 = lane_row(g0 + kTile), r2;
+        // raw words one row ahead of use (as lbp_hist_lane59.cuh)
+        LaneRow r0 = lane_row(g0), r1 = lane_row(g0 + kTile);
+        uint32_t wn = ld_shared_u32(g0 + 2 * kTile);
+        uint2 dn = make_uint2(0u, 0u);
+        if constexpr (HAS_DEPTH) dn = ld_shared_u32x2(d0);
 #pragma unroll
-        for (int j = 0; j < 15; j += 3) {
-            r2 = lane_row(g0 + (j + 2) * kTile); do_row(r0, r1, r2, j);
-            r0 = lane_row(g0 + (j + 3) * kTile); do_row(r1, r2, r0, j + 1);
-            r1 = lane_row(g0 + (j + 4) * kTile); do_row(r2, r0, r1, j + 2);
-        }
-        if (nrows < 16) {
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t wc = wn;
+            const uint2 dc = dn;
+            if (j < 15) {
+                wn = ld_shared_u32(g0 + (j + 3) * kTile);
+                if constexpr (HAS_DEPTH) dn = ld_shared_u32x2(d0 + (j + 1) * (kTile * 2));
+            }
+            if (j == 15 && nrows < 16) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
+                for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
+            }
+            const LaneRow r2 = lane_row_w(wc);
+            do_row(r0, r1, r2, dc);
+            r0 = r1;
+            r1 = r2;
         }
-        r2 = lane_row(g0 + 17 * kTile);
-        do_row(r0, r1, r2, 15);
 #pragma unroll
         for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
 
