@@ -11,12 +11,13 @@
 //    (1024 .. 16384) as HSET2 masks on the bits; the counter address is group base - 0x6400
 //    + t, and a masked-out pixel gets t of a dummy bin 256 in its own lane, so the update
 //    needs no select;
-//  * 2 groups x 8 warps, 2 TMA stages (stage == group: grey 16 KB + depth 32 KB); the 32-KB
-//    descriptor is staged in the stage's depth region after the rows are consumed (no room
-//    elsewhere; cell rows of 512 B with the 16-B chunks XOR-swizzled by cell x, so the
-//    epilogue's 8 cell-x lanes store to distinct banks), copied out by the group with 16-B
-//    loads and coalesced 16-B global stores; the next crop's grey box is issued at once,
-//    its depth box after the copy-out;
+//  * 2 groups x 8 warps, 2 TMA stages (stage == group: grey 16 KB + depth 32 KB), the next
+//    crop's boxes issued as soon as the rows are consumed; the 32-KB descriptor is staged
+//    over the consumed counters (no room elsewhere): the epilogue reads a cell-row group's
+//    counters into registers, and after a barrier writes the counts over them (cell rows of
+//    512 B with the 16-B chunks XOR-swizzled by cell x, so the 8 cell-x lanes store to
+//    distinct banks); the group copies the staging out with 16-B loads and coalesced 16-B
+//    global stores, re-zeroing it;
 //  * the per-pixel work is the code, one address op and one red.shared (lane59 also reads the
 //    LUT byte and forms the counter address): 59 instructions per lane-row.
 #pragma once
@@ -35,13 +36,13 @@ constexpr int kStages = 2;
 constexpr int kGreyBytes = kTile * kTile;                    // 16,384
 constexpr int kStageBytes = kGreyBytes + 2 * kTile * kTile;  // 49,152
 constexpr int kHistBytes = 2 * kRows * 32 * 4;               // 65,792
-constexpr int kDescBytes = 64 * kBins * 2;                   // 32,768 (staged in the depth box)
+constexpr int kDescBytes = 64 * kBins * 2;                   // 32,768 (staged over g = 0)
 constexpr int kGroupOff = kStages * kStageBytes;             // 98,304
 constexpr int kLutOff = kGroupOff + kGroups * kHistBytes;    // 229,888: identity LUT (generic)
 constexpr int kBarOff = kLutOff + 256;
 constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;      // + 128-B alignment slack
 static_assert(kSmemBytes <= 227 * 1024, "shared memory");
-static_assert(kDescBytes <= kStageBytes - kGreyBytes, "staging fits the depth region");
+static_assert(kDescBytes <= kRows * 128, "staging fits over the first cell-row group");
 static_assert(kStages == kGroups, "stage == group");
 }  // namespace l256
 
@@ -79,14 +80,12 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
     const int warp = gtid >> 5, lane = gtid & 31;
     const uint32_t stages0 = smem_u32(smem);
     const uint32_t hist0 = stages0 + kGroupOff + group * kHistBytes;
-    const uint32_t staging = stages0 + group * kStageBytes + kGreyBytes;  // the depth region
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     const uint32_t bar_id = 1 + group;
 
     const int n_pos = (n_rois > (int)blockIdx.x) ? (n_rois - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     auto crop_of = [&](int i) -> int32_t { return (int32_t)blockIdx.x + i * (int32_t)gridDim.x; };
     // part bit 1: arrive + expect the stage's bytes + the grey box; bit 2: the depth box
-    // (late: the staging lives in the depth region)
     auto issue = [&](int i, int part) {
         if (i >= n_pos) return;
         const int s = i % kStages;
@@ -234,49 +233,79 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
 
         named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
         if (gtid == 0) {
-            issue(i + kStages, 1);  // the grey box (its region is free)
+            issue(i + kStages, 3);  // the whole next stage: the staging is not in it
             if (roi_status) roi_status[n] = LBP_OK;
         }
-        // ---- epilogue: quad q = (g, bin, cx) as lane59 (conflict-free 16-B counter loads);
-        // counts go to the swizzled staging; the dummy row is only re-zeroed
-        for (int q = gtid; q < 2 * kRows * 8; q += kGroupThreads) {
-            const uint32_t qa = hist0 + q * 16;
-            const int g = q / (kRows * 8), rem = q - g * (kRows * 8);
-            const int bin = rem >> 3, cx = rem & 7;
-            if (bin == kBins) {
-                st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
-                continue;
-            }
+        // ---- epilogue in two halves, the staging inside the consumed counters: quad q =
+        // (bin, cx) of cell-row group g as lane59 (conflict-free 16-B loads) -> the 4 cells'
+        // counts in registers; g = 0's counts are written (swizzled) over g = 0's own
+        // counters once every thread has read them, g = 1's after them (cells 32..63)
+        constexpr int kQ = kRows * 8;                      // quads per cell-row group
+        constexpr int kQIter = (kQ + kGroupThreads - 1) / kGroupThreads;
+        const uint32_t staging = hist0;
+        auto counts = [&](uint32_t qa) {  // 4 cells' u16 counts of one quad, packed in 2 words
             const uint4 w = ld_shared_u32x4(qa);
-            st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
             const uint32_t lo01 = prmt(w.x, w.y, 0x5140), hi01 = prmt(w.x, w.y, 0x7362);
             const uint32_t lo23 = prmt(w.z, w.w, 0x5140), hi23 = prmt(w.z, w.w, 0x7362);
             const uint32_t c0 = __dp4a(prmt(lo01, lo23, 0x5410), 0x01010101u, 0u);
             const uint32_t c1 = __dp4a(prmt(lo01, lo23, 0x7632), 0x01010101u, 0u);
             const uint32_t c2 = __dp4a(prmt(hi01, hi23, 0x5410), 0x01010101u, 0u);
             const uint32_t c3 = __dp4a(prmt(hi01, hi23, 0x7632), 0x01010101u, 0u);
+            return make_uint2(c0 | (c1 << 16), c2 | (c3 << 16));
+        };
+        auto put = [&](int g, int q, uint2 c) {  // cells (4g + j, cx), j = 0..3
+            const int bin = q >> 3, cx = q & 7;
             const uint32_t o = staging + ((4 * g) * 8 + cx) * (kBins * 2) +
                                ((2u * bin) ^ ((uint32_t)cx << 4));
             constexpr uint32_t kRow = 8 * kBins * 2;
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "h"((uint16_t)c0) : "memory");
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + kRow), "h"((uint16_t)c1) : "memory");
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 2 * kRow), "h"((uint16_t)c2) : "memory");
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 3 * kRow), "h"((uint16_t)c3) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "h"((uint16_t)c.x) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + kRow), "h"((uint16_t)(c.x >> 16)) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 2 * kRow), "h"((uint16_t)c.y) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 3 * kRow), "h"((uint16_t)(c.y >> 16)) : "memory");
+        };
+        uint2 cnt[kQIter];
+#pragma unroll
+        for (int k = 0; k < kQIter; ++k) {  // g = 0: read (the dummy row is only re-zeroed)
+            const int q = gtid + k * kGroupThreads;
+            if (q < kQ) {
+                if ((q >> 3) == kBins) st_shared_u32x4(hist0 + q * 16, make_uint4(0, 0, 0, 0));
+                else cnt[k] = counts(hist0 + q * 16);
+            }
         }
-        named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-        {  // copy-out: 2,048 chunks of 16 B, un-swizzled, coalesced
+        named_barrier_sync(bar_id, kGroupThreads);  // every g = 0 counter read
+#pragma unroll
+        for (int k = 0; k < kQIter; ++k) {
+            const int q = gtid + k * kGroupThreads;
+            if (q < kQ && (q >> 3) < kBins) put(0, q, cnt[k]);
+        }
+        const uint32_t hist1 = hist0 + kRows * 128;
+#pragma unroll
+        for (int k = 0; k < kQIter; ++k) {  // g = 1: read and re-zero
+            const int q = gtid + k * kGroupThreads;
+            if (q < kQ) {
+                const uint32_t qa = hist1 + q * 16;
+                if ((q >> 3) < kBins) cnt[k] = counts(qa);
+                st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kQIter; ++k) {
+            const int q = gtid + k * kGroupThreads;
+            if (q < kQ && (q >> 3) < kBins) put(1, q, cnt[k]);
+        }
+        named_barrier_sync(bar_id, kGroupThreads);  // B: staging complete
+        {  // copy-out: 2,048 chunks of 16 B, un-swizzled, coalesced; each chunk re-zeroed
             uint16_t* out = desc + (int64_t)n * desc_stride;
 #pragma unroll 4
             for (int idx = gtid; idx < kDescBytes / 16; idx += kGroupThreads) {
                 const int cell = idx >> 5, chunk = idx & 31;
-                const uint4 v = ld_shared_u32x4(staging + cell * (kBins * 2) +
-                                                ((chunk * 16) ^ ((cell & 7) << 4)));
+                const uint32_t sa = staging + cell * (kBins * 2) + ((chunk * 16) ^ ((cell & 7) << 4));
+                const uint4 v = ld_shared_u32x4(sa);
+                st_shared_u32x4(sa, make_uint4(0, 0, 0, 0));
                 *reinterpret_cast<uint4*>(out + cell * kBins + chunk * 8) = v;
             }
         }
-        fence_proxy_async_smem();                   // generic reads before the TMA overwrite
-        named_barrier_sync(bar_id, kGroupThreads);  // C: staging read
-        if (gtid == 0) issue(i + kStages, 2);       // the depth box into the staging region
+        named_barrier_sync(bar_id, kGroupThreads);  // C: counters zero for the next crop
     }
 }
 
