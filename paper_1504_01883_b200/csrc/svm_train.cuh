@@ -137,31 +137,35 @@ svm_train_ovr_reg_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t d
         // steps ago, requests the counts of step t+2 into buf[(r+2)%3] from the index ids[..]
         // loaded one step ago, and loads the index of step t+3 into ids[r].
         auto idx = [&](int64_t j) { return __ldg(order + (j < T ? j : T - 1)); };
+        // (the visit-order index of step t+2 is loaded three steps earlier: slot (r+1) % 3 of
+        // ids holds it at step t and is then reloaded with the index of step t+5)
         uint32_t buf[3][PAIRS];
-        int32_t ids[3] = {idx(0), idx(1), idx(2)};
+        int32_t ids[3] = {idx(4), idx(2), idx(3)};
         int32_t labs[3];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
+            const int32_t i0 = idx(r);
 #pragma unroll
             for (int k = 0; k < PAIRS; ++k) {
                 const int p = t0 + k * NT;
-                buf[r][k] = p < half ? __ldg(d32 + (int64_t)ids[r] * half + p) : 0u;
+                buf[r][k] = p < half ? __ldg(d32 + (int64_t)i0 * half + p) : 0u;
             }
-            labs[r] = __ldg(labels + ids[r]);
+            labs[r] = __ldg(labels + i0);
         }
         for (int64_t t0s = 1; t0s <= T; t0s += 3) {
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
                 const int64_t t = t0s + r;
                 if (t > T) break;  // uniform
-                const int rn = (r + 2) % 3;
+                const int rn = (r + 2) % 3, ri = (r + 1) % 3;
+                const int32_t i_n = ids[ri];  // sample of step t+2
 #pragma unroll
                 for (int k = 0; k < PAIRS; ++k) {
                     const int p = t0 + k * NT;
-                    buf[rn][k] = p < half ? __ldg(d32 + (int64_t)ids[rn] * half + p) : 0u;
+                    buf[rn][k] = p < half ? __ldg(d32 + (int64_t)i_n * half + p) : 0u;
                 }
-                labs[rn] = __ldg(labels + ids[rn]);
-                ids[r] = idx(t + 2);
+                labs[rn] = __ldg(labels + i_n);
+                ids[ri] = idx(t + 4);          // sample of step t+5
                 const ZT y = (labs[r] == c) ? 1 : -1;
                 bool viol = true;
                 if (t > 1) {
