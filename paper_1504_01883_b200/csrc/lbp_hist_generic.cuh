@@ -46,8 +46,9 @@ struct CodePlane {
 // desc + n * desc_stride (desc_stride >= dim; the fused grey||depth layout passes 2 * dim and
 // a desc already offset to its block).
 // Only the cells [cell_begin, cell_end) (row-major cell indices) are computed and written;
-// the whole grid by default.  The unit holding cell 0 writes roi_status.
-template <int BINS, int NT, typename T, typename Sync>
+// the whole grid by default.  The unit holding cell 0 writes roi_status.  KEEP (one chunk
+// only): the counts stay in hist (not re-zeroed, no trailing sync) for the caller to read.
+template <int BINS, int NT, typename T, typename Sync, bool KEEP = false>
 __device__ __forceinline__ void extract_roi_generic(
     const CodePlane<T> plane, const uint16_t* __restrict__ depth, const lbp_images_t& geom,
     const lbp_roi_t roi, int32_t n, const DepthWindow& win, int32_t cells_x, int32_t cells_y,
@@ -114,9 +115,9 @@ __device__ __forceinline__ void extract_roi_generic(
         uint16_t* o = out + (int64_t)c0 * BINS;
         for (int i = t; i < (c1 - c0) * BINS; i += NT) {
             o[i] = (uint16_t)hist[i];
-            hist[i] = 0;
+            if (!KEEP) hist[i] = 0;
         }
-        sync();
+        if (!KEEP) sync();
     }
 }
 
