@@ -129,8 +129,10 @@ struct CtaSync {
 // Cell rows are disjoint in the descriptor, so units never share a counter and no global
 // atomics are needed; a handful of ROIs (the frame-stream and single-crop configs) still
 // spread over cells_y times as many SMs.
-template <int BINS, typename T>
-__global__ void __launch_bounds__(kGenericThreads)
+// NT = 512 for small batches of tall ROIs (one interior row per warp, one L2 round trip),
+// 256 otherwise.
+template <int BINS, typename T, int NT = kGenericThreads>
+__global__ void __launch_bounds__(NT)
 lbp_hist_generic_kernel(const CodePlane<T> plane, const uint16_t* __restrict__ depth,
                         lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
                         DepthWindow win, int32_t cells_x, int32_t cells_y,
@@ -147,7 +149,7 @@ lbp_hist_generic_kernel(const CodePlane<T> plane, const uint16_t* __restrict__ d
     const int64_t n_units = (int64_t)n_rois * cells_y;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int32_t n = (int32_t)(u / cells_y), cy = (int32_t)(u - (int64_t)n * cells_y);
-        extract_roi_generic<BINS, kGenericThreads>(plane, depth, geom, rois[n], n, win, cells_x,
+        extract_roi_generic<BINS, NT>(plane, depth, geom, rois[n], n, win, cells_x,
                                                    cells_y, desc, desc_stride, roi_status, hist,
                                                    kGenericHistCap, lut, 0, (int)threadIdx.x,
                                                    CtaSync{}, cy * cells_x, (cy + 1) * cells_x);

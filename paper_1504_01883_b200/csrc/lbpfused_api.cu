@@ -2,6 +2,7 @@
 // dispatch between kernel variants, launches on the caller's stream.
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "desc_pack.cuh"
@@ -126,29 +127,25 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
                                                      true, frame);
         if (e != cudaErrorNotSupported) return launch_status(e);
     }
-    // one CTA per (ROI, cell row) unit, grid-strided
+    // one CTA per (ROI, cell row) unit, grid-strided; 512 threads when the batch is small and
+    // the images tall (the frame-stream config: one interior row per warp)
     const int grid = (int)std::min<int64_t>((int64_t)n_rois * cells_y, (int64_t)num_sms() * 8);
-    if (depth_source) {
-        const CodePlane<uint16_t> plane{depth, geom.depth_pitch, geom.depth_img_stride};
-        if (bins == 59)
-            lbp_hist_generic_kernel<59><<<grid, kGenericThreads, 0, stream>>>(
-                plane, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, desc_stride,
-                roi_status);
-        else
-            lbp_hist_generic_kernel<256><<<grid, kGenericThreads, 0, stream>>>(
-                plane, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, desc_stride,
-                roi_status);
-    } else {
-        const CodePlane<uint8_t> plane{grey, geom.grey_pitch, geom.grey_img_stride};
-        if (bins == 59)
-            lbp_hist_generic_kernel<59><<<grid, kGenericThreads, 0, stream>>>(
-                plane, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, desc_stride,
-                roi_status);
-        else
-            lbp_hist_generic_kernel<256><<<grid, kGenericThreads, 0, stream>>>(
-                plane, depth, geom, rois, n_rois, win, cells_x, cells_y, desc, desc_stride,
-                roi_status);
-    }
+    const bool wide = (int64_t)n_rois * cells_y < 2 * num_sms() && geom.height >= 128;
+    auto band = [&](auto plane) {
+        using T = typename std::remove_const<
+            typename std::remove_pointer<decltype(plane.base)>::type>::type;
+        auto k = bins == 59 ? (wide ? lbp_hist_generic_kernel<59, T, 512>
+                                    : lbp_hist_generic_kernel<59, T, kGenericThreads>)
+                            : (wide ? lbp_hist_generic_kernel<256, T, 512>
+                                    : lbp_hist_generic_kernel<256, T, kGenericThreads>);
+        k<<<grid, wide ? 512 : kGenericThreads, 0, stream>>>(plane, depth, geom, rois, n_rois, win,
+                                                           cells_x, cells_y, desc, desc_stride,
+                                                           roi_status);
+    };
+    if (depth_source)
+        band(CodePlane<uint16_t>{depth, geom.depth_pitch, geom.depth_img_stride});
+    else
+        band(CodePlane<uint8_t>{grey, geom.grey_pitch, geom.grey_img_stride});
     return launch_status(cudaGetLastError());
 }
 
