@@ -18,7 +18,7 @@
 
 namespace lbpf {
 
-constexpr int kResizeThreads = 256;
+constexpr int kResizeThreads = 512;
 constexpr int kResizeMaxSize = 1024;
 constexpr int kResizeStageBytes = 28 * 1024;  // grey u8 + depth u16 rows of one chunk
 constexpr int kResizeHistCap = 4096;          // u32 counters per cell chunk (both planes)
