@@ -14,7 +14,7 @@ dev = torch.device("cuda", 0)
 g, d = synthgen.gpu_face_crops(150, 128, 128, seed=1, device=dev)
 r = torch.from_numpy(synthgen.full_rois(150, 128, 128)).to(dev)
 desc = lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 59)            # lane59 (TMA)
-lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 256)                   # fast v3 (256 bins)
+lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 256)                   # lane256 (256 bins)
 lb.lbp_fused_extract(g, None, r, 0, 0, 8, 8, 59)                      # lane59, no depth
 lb.lbp_extract_source(g, d, r, 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)  # + depth source
 lb.lbp_fused_extract(g, d, r[:8].contiguous(), 600, 1400, 8, 8, 59)   # band kernel
@@ -22,6 +22,11 @@ gf, df, rf = synthgen.kinect_frames(2, seed=2)
 gf, dft = torch.from_numpy(gf).to(dev), torch.from_numpy(df.view(np.int16)).to(dev).view(torch.uint16)
 rf = torch.from_numpy(rf).to(dev)
 lb.lbp_extract_resized(gf, dft, rf, 200, 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)
+gb, db, rb = synthgen.kinect_frames(40, seed=4)                           # FRAME variant (160 ROIs)
+gb, dbt = torch.from_numpy(gb).to(dev), torch.from_numpy(db.view(np.int16)).to(dev).view(torch.uint16)
+lb.lbp_extract_source(gb, dbt, torch.from_numpy(rb).to(dev), 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)
+pk, exc, cnt = lb.desc_pack_u8(desc, row_base=0, cap=64)                  # compaction
+lb.desc_unpack_u8(pk, exc, cnt, 64)
 for C in (10, 130):
     W, b = synthgen.svm_weights(C, 3776, seed=C)
     Wt, bt = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
