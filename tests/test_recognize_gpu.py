@@ -72,3 +72,15 @@ def test_large_batch_two_kernel_path(lb):
     grey, depth = synthgen.face_crops(200, 128, 128, seed=8)
     _run(lb, grey, depth, synthgen.full_rois(200, 128, 128), 8, 8, 59, 100, seed=8,
          prepared=True)
+
+
+def test_wide_cell_rows_and_small_images(lb):
+    """cells_x * bins above the 4,096 smem counters (the segment is scored from the written
+    descriptor instead of the CTA's histogram), more classes than warps (the W prefetch covers
+    only the first class of each warp), and 256- vs 512-thread CTAs (image height < / >= 128)"""
+    g, d, _ = synthgen.kinect_frames(1, seed=9)
+    rois = [[0, 10, 20, 200, 150], [0, 300, 200, 128, 128]]
+    _run(lb, g, d, rois, 20, 4, 256, 40, seed=9)   # 20 x 256 = 5,120 entries per cell row
+    _run(lb, g, d, rois, 16, 8, 256, 3, seed=10)   # exactly 4,096
+    grey, depth = synthgen.face_crops(3, 100, 120, seed=11)
+    _run(lb, grey, depth, synthgen.full_rois(3, 100, 120), 8, 8, 59, 25, seed=11)
