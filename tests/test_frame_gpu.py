@@ -102,3 +102,19 @@ def test_kinect_stream_batch(lb):
     grey, depth, rois = synthgen.kinect_frames(40, 4, seed=54)
     for source in (0, 1, 2):
         _check(lb, grey, depth, rois, 600, 1400, source)
+
+
+@pytest.mark.parametrize("bins", [59, 256])
+def test_small_batch_band_kernel_512(lb, bins):
+    """fewer ROIs than SMs on tall frames: the band kernel with 512-thread CTAs"""
+    grey, depth = synthgen.face_crops(3, 480, 640, seed=55)
+    rois = _frame_rois(3, 480, 640, 5, per_frame=5)
+    assert len(rois) * 8 < 2 * 148
+    for source in (0, 1, 2):
+        g = torch.from_numpy(grey).to(DEV)
+        d = _dev_u16(depth)
+        out = lb.lbp_extract_source(g, d, torch.from_numpy(rois).to(DEV), 600, 1400, 8, 8, bins,
+                                    source)
+        torch.cuda.synchronize()
+        ref = oracle.lbp_extract(grey, depth, rois, 600, 1400, 8, 8, bins, source=source)
+        assert np.array_equal(out.cpu().view(torch.int16).numpy().view(np.uint16), ref)
