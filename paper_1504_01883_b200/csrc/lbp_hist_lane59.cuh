@@ -299,6 +299,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
     };
 
+    // the dependent launch (the scorer) may be scheduled now: its CTAs take SMs as these
+    // CTAs exit, run their prologue, and wait for this grid's completion
+    launch_dependents();
     // ---- one-time setup: LUTs, zero counters, barriers, first three positions
     for (int i = tid; i < kLutBytes; i += kThreads) {
         const int code = (i >> 7) * 4 + (i & 3);

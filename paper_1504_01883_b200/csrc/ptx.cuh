@@ -59,6 +59,18 @@ __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start before its predecessor in the
+// stream completes; grid_dependency_wait() blocks until the predecessor grid has completed and
+// its memory is visible, and launch_dependents() lets this grid's dependents be scheduled
+// early (both no-ops when the launch is not programmatic)
+__device__ __forceinline__ void grid_dependency_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // value the compiler must keep in a register (no rematerialisation inside the hot loop)
 __device__ __forceinline__ uint32_t opaque(uint32_t v) {
     asm volatile("mov.b32 %0, %0;" : "+r"(v));

@@ -197,6 +197,9 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
     cluster_sync();  // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // programmatic dependent launch: the prologue above may overlap the tail of the kernel
+    // that wrote the descriptors; everything below reads them (no-op without PDL)
+    grid_dependency_wait();
 
     if (warp == 0) {
         // ===================== TMA producer (each CTA: its A rows and its half of B)
@@ -457,10 +460,18 @@ inline cudaError_t launch_svm_gemm(const uint16_t* desc, int32_t n, int32_t dim,
     if (e != cudaSuccess) return e;
     const int tiles = (n + 2 * kGemmM - 1) / (2 * kGemmM);
     const int pairs = tiles < sms / 2 ? tiles : sms / 2;
-    svm_gemm_kernel<<<2 * pairs, kGemmThreads, smem, stream>>>(am, bm, blm, desc, n, W, bias, ws, h,
-                                                               stages, stage_bytes, scores, labels,
-                                                               top, reject);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs, 1, 1);
+    cfg.blockDim = dim3(kGemmThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (grid_dependency_wait)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, svm_gemm_kernel, am, bm, blm, desc, n, W, bias, ws, h, stages,
+                              stage_bytes, scores, labels, top, reject);
 }
 
 }  // namespace lbpf

@@ -185,6 +185,9 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // programmatic dependent launch: the prologue above may overlap the tail of the kernel
+    // that wrote the descriptors; everything below reads them (no-op without PDL)
+    grid_dependency_wait();
 
     if (warp == 0) {
         // ===================== TMA producer: A = two 64-column u16 boxes, B = this CTA's half
@@ -472,10 +475,18 @@ inline cudaError_t launch_svm_gemm_i8(const uint16_t* desc, int32_t n, int32_t d
     if (e != cudaSuccess) return e;
     const int tiles = (n + 2 * kGemmM - 1) / (2 * kGemmM);
     const int pairs = tiles < sms / 2 ? tiles : sms / 2;
-    svm_gemm_i8_kernel<<<2 * pairs, kI8Threads, smem, stream>>>(am, bm, desc, n, W, bias, ws, h,
-                                                                stages, scores, labels, top,
-                                                                reject);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs, 1, 1);
+    cfg.blockDim = dim3(kI8Threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (grid_dependency_wait)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, svm_gemm_i8_kernel, am, bm, desc, n, W, bias, ws, h, stages,
+                              scores, labels, top, reject);
 }
 
 }  // namespace lbpf
