@@ -6,6 +6,7 @@ so that it travels to the GPU box with the repo snapshot.
 """
 from __future__ import annotations
 
+import fcntl
 import glob
 import os
 import subprocess
@@ -43,16 +44,25 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile when the library is missing or older than a source.  Concurrent callers (one
+    process per GPU) serialise on a lock file; the library is written to a temporary name and
+    renamed into place, so a loader never sees a partial file."""
     if not force and not needs_build():
         return LIB
-    extra = os.environ.get("LBP_NVCC_EXTRA", "").split()  # developer A/B builds only
-    cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-o", LIB, *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(PKG, "build.log")
-    with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed (see {log}):\n{res.stderr[-4000:]}")
+    with open(LIB + ".lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and not needs_build():  # built by another process meanwhile
+            return LIB
+        extra = os.environ.get("LBP_NVCC_EXTRA", "").split()  # developer A/B builds only
+        tmp = f"{LIB}.tmp{os.getpid()}"
+        cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-o", tmp, *sources()]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        log = os.path.join(PKG, "build.log")
+        with open(log, "w") as f:
+            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed (see {log}):\n{res.stderr[-4000:]}")
+        os.replace(tmp, LIB)
     if verbose:
         print(res.stderr)
     return LIB

@@ -160,11 +160,18 @@ _gpu_lib = None
 
 def build_gpu(force: bool = False) -> str:
     """nvcc-compile synth_gen.cu for sm_100a into synthgen/libsynthgen.so (in-tree)."""
-    if force or not _os.path.exists(_SO) or _os.path.getmtime(_SO) < _os.path.getmtime(_CU):
-        nvcc = _os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-        _subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
-                         "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-o", _SO, _CU],
-                        check=True)
+    stale = lambda: not _os.path.exists(_SO) or _os.path.getmtime(_SO) < _os.path.getmtime(_CU)
+    if force or stale():
+        import fcntl
+        with open(_SO + ".lock", "w") as lock:  # one build among concurrent processes
+            fcntl.flock(lock, fcntl.LOCK_EX)
+            if force or stale():
+                nvcc = _os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+                tmp = f"{_SO}.tmp{_os.getpid()}"
+                _subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                                 "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart",
+                                 "static", "-o", tmp, _CU], check=True)
+                _os.replace(tmp, _SO)
     return _SO
 
 

@@ -10,6 +10,18 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    # on a GPU box the in-tree libraries may be absent or older than their sources (a fresh
+    # checkout): build them once here (each build is a no-op when up to date)
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        has_gpu = False
+    if has_gpu:
+        from paper_1504_01883_b200 import build
+        build.build()
+        import synthgen
+        synthgen.build_gpu()
 
 
 def pytest_collection_modifyitems(config, items):
