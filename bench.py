@@ -874,10 +874,14 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
     gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
     glab = labels[:m].cpu().numpy()
     ok = gate_compare(gdesc, glab, odesc, olab, W_np, b_np)
+    # SURVEY §8(d) also asks for the single-threaded oracle: one thread, first 256 crops
+    r1, _, s1, _, _, _ = oracle_rate(g[:256], d[:256] if d is not None else None, r[:256], W_np,
+                                     b_np, cx, cy, bins, 2.0, 1, SOURCES[args.source])
     cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
            "sample": f"first {m} crops of this workload x {passes} passes = {done} crops "
                      f"(extraction + SVM), {threads} threads x unmodified single-threaded C "
                      f"oracle on disjoint shards, {secs:.1f} s",
+           "single_thread_value": r1,
            "cpu": cpu_model(), "equivalence_gate": "pass" if ok else "FAIL"}
     return cpu, ok
 
