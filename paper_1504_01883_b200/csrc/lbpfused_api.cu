@@ -430,6 +430,12 @@ int32_t lbp_desc_unpack_u8(const uint8_t* packed, int64_t n, int32_t dim, int64_
     return launch_status(cudaGetLastError());
 }
 
+#ifdef LBP_SVM_TRACE  // developer builds only (not declared in the public header)
+int32_t lbp_debug_svm_trace(unsigned long long* out32) {
+    return cudaMemcpyFromSymbol(out32, g_svm_trace, sizeof(g_svm_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim) {
     SvmPrepHeader h;
     if (!svm_choose_layout(n_classes, dim, &h)) return 0;

@@ -27,6 +27,9 @@
 // Classes are processed in TMEM passes of <= 124 classes (4 digits each + a ones block =
 // 512 fp32 columns); the running argmax of a crop lives in its epilogue thread's registers.
 #pragma once
+#ifdef LBP_SVM_TRACE
+__device__ unsigned long long g_svm_trace[32];
+#endif
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -157,6 +160,21 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                 int32_t* __restrict__ labels, float* __restrict__ top_score,
                 float reject_threshold) {
     extern __shared__ uint8_t smem_raw[];
+#ifdef LBP_SVM_TRACE  // developer phase timestamps (globaltimer) of cluster 0 and the last one:
+                      // entry, prologue done, last MMA issued, MMAs done, epilogue done, exit
+#define SVM_TRACE(slot)                                                                    \
+    do {                                                                                   \
+        const uint32_t cl_ = cluster_id_x();                                               \
+        if (cl_ == 0 || cl_ == n_clusters_x() - 1) {                                       \
+            unsigned long long gt;                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));                         \
+            g_svm_trace[(cl_ == 0 ? 0 : 1) * 16 + cluster_ctarank() * 8 + (slot)] = gt;    \
+        }                                                                                  \
+    } while (0)
+#else
+#define SVM_TRACE(slot) do {} while (0)
+#endif
+    if (threadIdx.x == 0) SVM_TRACE(0);
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     const GemmSmem L{stages, stage_bytes};
@@ -200,6 +218,7 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
     // programmatic dependent launch: the prologue above may overlap the tail of the kernel
     // that wrote the descriptors; everything below reads them (no-op without PDL)
     grid_dependency_wait();
+    if (threadIdx.x == 0) SVM_TRACE(1);
 
     if (warp == 0) {
         // ===================== TMA producer (each CTA: its A rows and its half of B)
@@ -269,6 +288,7 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                     }
                     if (elect_one()) mma_commit_pair(tmem_full, 0x3);  // pass accumulators done
                     __syncwarp();
+                    if (lane == 0) SVM_TRACE(2);
                 }
             }
         }
@@ -329,6 +349,7 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                                     : make_double2(0.0, 0.0);
                 const bool tile_big = named_barrier_or(1, 128, flag_or != 0);
                 mbar_wait(tmem_full, acc_ph);
+                if (et == 0) SVM_TRACE(3);
                 acc_ph ^= 1;
                 tc_fence_after();
                 const uint32_t lane_addr = tmem_base + ((uint32_t)(quarter * 32) << 16);
@@ -408,12 +429,14 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                 if (top_score) top_score[crop] = best;
                 if (labels) labels[crop] = (best < reject_threshold) ? -1 : best_c;
             }
+            if (et == 0) SVM_TRACE(4);
         }
     }
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // the peer's TMEM / smem are no longer used by the leader's MMAs
     if (warp == 1) tmem_dealloc_pair(tmem_base, 512);
+    if (threadIdx.x == 0) SVM_TRACE(5);
 }
 
 // ---------------------------------------------------------------------------- host side
