@@ -42,7 +42,7 @@ constexpr int kGemmM = 128;
 constexpr int kGemmK = 64;                  // K per pipeline stage (fp16 elements)
 constexpr int kRowBytes = kGemmK * 2;       // one swizzled smem row: 128 B (SWIZZLE_128B)
 constexpr int kDimAlign = 64;               // workspace dim padding
-constexpr int kGemmThreads = 224;
+constexpr int kGemmThreads = 352;  // 11 warps (see svm_gemm_kernel)
 constexpr uint32_t kPrepMagic = 0x53564D31u;  // "SVM1"
 
 struct SvmPrepHeader {
@@ -151,6 +151,53 @@ struct GemmSmem {
 //   empty[s]   both: pair MMAs and this CTA's 4 checker warps done with stage s (count 5)
 //   tmem_full  both: accumulators of the pass complete        (multicast commit)
 //   tmem_empty leader: both CTAs' epilogues drained TMEM      (count 8)
+// Epilogue of one pass for one accumulator row: the 8-class groups c8 = 8 par + 16 i (par 0:
+// the checker warp, 1: its helper), 32 TMEM columns per tcgen05.ld, double-buffered (the next
+// own group is in flight while the current one is combined).  Accumulators hold (integer
+// sum) * 2^-24, so digit k weighs 2^(16-9k); the fp64 combination is exact and
+// fma(scale, q, bias) rounds once.  Running argmax over ascending classes (ties -> lowest).
+__device__ __forceinline__ void svm_epilogue_groups(uint32_t lane_addr, const double2* tab,
+                                                    int nc, int par, bool live, float* scores,
+                                                    int64_t crop, int C, int class0,
+                                                    float& best, int& best_c) {
+    auto combine8 = [&](const uint32_t (&v)[32], int c8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int lc = c8 + j;
+            const double2 sb = tab[lc < kPassClasses ? lc : 0];
+            double q = (double)__uint_as_float(v[4 * j + 0]) * 0x1p16;
+            q = fma((double)__uint_as_float(v[4 * j + 1]), 0x1p7, q);
+            q = fma((double)__uint_as_float(v[4 * j + 2]), 0x1p-2, q);
+            q = fma((double)__uint_as_float(v[4 * j + 3]), 0x1p-11, q);
+            const float sc = (float)fma(sb.x, q, sb.y);
+            if (lc < nc && live) {
+                if (scores) scores[crop * C + class0 + lc] = sc;
+                if (best_c < 0 || sc > best) {
+                    best = sc;
+                    best_c = class0 + lc;
+                }
+            }
+        }
+    };
+    uint32_t va[32], vb[32];
+    int c8 = 8 * par;
+    if (c8 < nc) {
+        tmem_ld32(lane_addr + (uint32_t)(4 * c8), va);
+        tmem_ld_wait_regs(va);
+    }
+    for (; c8 < nc; c8 += 32) {
+        const bool has_b = c8 + 16 < nc, has_a2 = c8 + 32 < nc;  // warp-uniform
+        if (has_b) tmem_ld32(lane_addr + (uint32_t)(4 * (c8 + 16)), vb);
+        combine8(va, c8);
+        if (has_b) {
+            tmem_ld_wait_regs(vb);
+            if (has_a2) tmem_ld32(lane_addr + (uint32_t)(4 * (c8 + 32)), va);
+            combine8(vb, c8 + 16);
+            if (has_a2) tmem_ld_wait_regs(va);
+        }
+    }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap b_map,
                 const __grid_constant__ CUtensorMap b_last_map,
@@ -305,6 +352,43 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                 if (++s == stages) { s = 0; ph ^= 1; }
             }
         }
+    } else if (warp >= 7) {
+        // ===================== epilogue helpers (warps 7..10): the odd 8-class groups of the
+        // same TMEM lane quarter as checker warp (warp & 3); their per-row argmax is merged
+        // by the checker through shared memory
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        double2* epi_tab = reinterpret_cast<double2*>(smem + stages * stage_bytes + 512);
+        float* hbest = reinterpret_cast<float*>(epi_tab + 2 * kPassClasses);
+        int* hcls = reinterpret_cast<int*>(hbest + kGemmM);
+        const int* flag = hcls + kGemmM;
+        int pc = 0;
+        uint32_t acc_ph = 0;
+        for (int t = pair; t < n_tiles; t += n_pairs_grid) {
+            const int64_t crop = (int64_t)t * 2 * kGemmM + (int64_t)rank * kGemmM + row;
+            int class0 = 0;
+            for (int p = 0; p < h.n_pass; ++p) {
+                const int nc = pass_classes(C, p);
+                const double2* tab = epi_tab + (pc & 1) * kPassClasses;
+                named_barrier_sync(2, 256);  // the pass's (scale, bias) table is written
+                (void)flag;
+                mbar_wait(tmem_full, acc_ph);
+                acc_ph ^= 1;
+                tc_fence_after();
+                const uint32_t lane_addr = tmem_base + ((uint32_t)(quarter * 32) << 16);
+                const bool live = crop < n;
+                float best = 0.0f;
+                int best_c = -1;
+                svm_epilogue_groups(lane_addr, tab, nc, 1, live, scores, crop, C, class0, best,
+                                    best_c);
+                hbest[row] = best;
+                hcls[row] = best_c;
+                tc_fence_before();
+                named_barrier_sync(3, 256);  // partial argmaxes visible to the checkers
+                class0 += nc;
+                ++pc;
+            }
+        }
     } else {
         // ===================== checkers + epilogue (warps 2..5, 128 threads per CTA)
         const int et = threadIdx.x - 64;           // 0..127
@@ -348,6 +432,7 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                                                    (double)__ldg(bias + class0 + i))
                                     : make_double2(0.0, 0.0);
                 const bool tile_big = named_barrier_or(1, 128, flag_or != 0);
+                named_barrier_sync(2, 256);  // the table for the helper warps
                 mbar_wait(tmem_full, acc_ph);
                 if (et == 0) SVM_TRACE(3);
                 acc_ph ^= 1;
@@ -359,45 +444,20 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                 const float colsum = __uint_as_float(colsum_bits);
                 const bool exact = (colsum < 0x1p-8f) && !tile_big;
                 const bool live = crop < n;
-                // 8 classes (32 columns) per tcgen05.ld, double-buffered: the next load is in
-                // flight while the current 8 classes are combined.  Accumulators hold
-                // (integer sum) * 2^-24, so digit k weighs 2^(16-9k); the fp64 combination is
-                // exact and fma(scale, q, bias) rounds once.
-                auto combine8 = [&](const uint32_t (&v)[32], int c8) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int lc = c8 + j;
-                        const double2 sb = tab[lc < kPassClasses ? lc : 0];
-                        double q = (double)__uint_as_float(v[4 * j + 0]) * 0x1p16;
-                        q = fma((double)__uint_as_float(v[4 * j + 1]), 0x1p7, q);
-                        q = fma((double)__uint_as_float(v[4 * j + 2]), 0x1p-2, q);
-                        q = fma((double)__uint_as_float(v[4 * j + 3]), 0x1p-11, q);
-                        const float sc = (float)fma(sb.x, q, sb.y);
-                        if (lc < nc && live) {
-                            if (scores) scores[crop * C + class0 + lc] = sc;
-                            if (best_c < 0 || sc > best) {
-                                best = sc;
-                                best_c = class0 + lc;
-                            }
-                        }
-                    }
-                };
                 const float best_prev = best;  // argmax over the earlier passes
                 const int best_c_prev = best_c;
+                // the even 8-class groups here, the odd ones in the helper warp of this quarter
+                svm_epilogue_groups(lane_addr, tab, nc, 0, live, scores, crop, C, class0, best,
+                                    best_c);
+                named_barrier_sync(3, 256);  // the helper's partial argmax of this row
                 {
-                    uint32_t va[32], vb[32];
-                    tmem_ld32(lane_addr, va);
-                    tmem_ld_wait_regs(va);
-                    for (int c8 = 0; c8 < nc; c8 += 16) {
-                        const bool has_b = c8 + 8 < nc, has_a2 = c8 + 16 < nc;  // warp-uniform
-                        if (has_b) tmem_ld32(lane_addr + (uint32_t)(4 * (c8 + 8)), vb);
-                        combine8(va, c8);
-                        if (has_b) {
-                            tmem_ld_wait_regs(vb);
-                            if (has_a2) tmem_ld32(lane_addr + (uint32_t)(4 * (c8 + 16)), va);
-                            combine8(vb, c8 + 8);
-                            if (has_a2) tmem_ld_wait_regs(va);
-                        }
+                    float* hbest = reinterpret_cast<float*>(epi_tab + 2 * kPassClasses);
+                    const int* hcls = reinterpret_cast<const int*>(hbest + kGemmM);
+                    const float hb = hbest[row];
+                    const int hc = hcls[row];
+                    if (hc >= 0 && (best_c < 0 || hb > best || (hb == best && hc < best_c))) {
+                        best = hb;
+                        best_c = hc;
                     }
                 }
                 if (!exact && live) {
@@ -477,7 +537,8 @@ inline cudaError_t launch_svm_gemm(const uint16_t* desc, int32_t n, int32_t dim,
     stages = stages > 12 ? 12 : stages;
     if (stages < 2) return cudaErrorNotSupported;
     // + 1024 alignment slack + 512 barriers + epilogue table
-    const int smem = stages * stage_bytes + 1024 + 512 + 2 * kPassClasses * 16;
+    const int smem = stages * stage_bytes + 1024 + 512 + 2 * kPassClasses * 16 +
+                     2 * kGemmM * 4 + 16;  // + the helper warps' per-row argmax
     cudaError_t e = cudaFuncSetAttribute(svm_gemm_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
