@@ -37,7 +37,8 @@ constexpr int kI8OnesCol = kI8Digits * kI8PassClasses;  // 480
 constexpr int kI8K = 128;            // K per stage: one 128-B u8 row
 constexpr int kI8DimAlign = 128;
 constexpr int kI8MaxDim = 33000;     // 255 * 255 * dim < 2^31
-constexpr int kI8Threads = 192;      // warp 0 producer, 1 MMA, 2-5 converters + epilogue
+constexpr int kI8Threads = 320;      // warp 0 producer, 1 MMA, 2-5 converters + epilogue,
+                                     // 6-9 epilogue helpers
 constexpr uint32_t kPrep8Magic = 0x53564D38u;  // "SVM8"
 constexpr int kI8BigMax = 4;         // recorded entries above 255 per descriptor row
 constexpr int kI8Distinct = 40;      // distinct such columns per CTA tile with W staged in smem
@@ -127,6 +128,93 @@ constexpr int kI8StageA = 2 * kGemmM * 128;  // 32 KB
 constexpr int kI8StageB = 256 * 128;         // 32 KB
 constexpr int kI8StageBytes = kI8StageA + kI8StageB;
 
+// What one accumulator row's epilogue needs for a pass (svm_gemm_i8_kernel)
+struct I8Epi {
+    uint32_t lane_addr;   // TMEM address of the row's lane quarter
+    const double2* tab;   // (scale, bias) of the pass's classes
+    int nc, class0, C;
+    int32_t X;            // sum_d x_d (ones column)
+    bool live, staged;
+    int n_big, row;
+    double hi_r[kI8BigMax];
+    uint32_t woff[kI8BigMax];
+    const int32_t* big_d;
+    const int32_t* big_hi;
+    const float* W;
+    int dim;
+    float* scores;
+    int64_t crop;
+};
+
+// 16 classes [c0, c0 + 16) of the pass: Q by Horner over the 5 digit planes (x16 TMEM loads),
+// s = b + m (Q 2^-39 - X) [+ the exact high parts of entries above 255]; running argmax over
+// ascending classes (ties -> lowest).  kBig: the warp has rows with entries above 255.
+template <bool kBig>
+__device__ __forceinline__ void i8_combine16(const I8Epi& e, int c0, float& best, int& best_c) {
+    long long q[16];
+    uint32_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) q[j] = 0;
+#pragma unroll
+    for (int k = 0; k < kI8Digits; ++k) {
+        tmem_ld16(e.lane_addr + (uint32_t)(k * kI8PassClasses + c0), v);
+        tmem_ld_wait_regs(v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) q[j] = (q[j] << 8) + (int32_t)v[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int lc = c0 + j;
+        const double2 sb = e.tab[lc < kI8PassClasses ? lc : 0];
+        const double sm = fma((double)q[j], 0x1p-39, -(double)e.X);
+        double acc = fma(sb.x, sm, sb.y);
+        if (kBig && lc < e.nc) {
+            if (e.staged) {  // independent shared loads, no dependent chain
+#pragma unroll
+                for (int t = 0; t < kI8BigMax; ++t)
+                    acc = fma(e.hi_r[t],
+                              (double)__uint_as_float(ld_shared_u32(e.woff[t] + (uint32_t)lc * 4)),
+                              acc);
+            } else {
+                const float* wc = e.W + (size_t)(e.class0 + lc) * e.dim;
+                for (int t = 0; t < e.n_big; ++t)
+                    acc = fma((double)e.big_hi[e.row * kI8BigMax + t],
+                              (double)__ldg(wc + e.big_d[e.row * kI8BigMax + t]), acc);
+            }
+        }
+        const float sc = (float)acc;
+        if (lc < e.nc && e.live) {
+            if (e.scores) e.scores[e.crop * e.C + e.class0 + lc] = sc;
+            if (best_c < 0 || sc > best) {
+                best = sc;
+                best_c = e.class0 + lc;
+            }
+        }
+    }
+}
+
+// the row's correction terms (smem addresses of its staged W columns; zero weights beyond
+// n_big), hoisted out of the class loop
+__device__ __forceinline__ void i8_epi_corrections(I8Epi& e, const float* wcol) {
+    const uint32_t wcol0 = smem_u32(wcol);
+#pragma unroll
+    for (int t = 0; t < kI8BigMax; ++t) {
+        const bool on = e.staged && t < e.n_big;
+        e.hi_r[t] = on ? (double)e.big_hi[e.row * kI8BigMax + t] : 0.0;
+        e.woff[t] = on ? wcol0 + (uint32_t)e.big_d[e.row * kI8BigMax + t] * (kI8PassClasses * 4)
+                       : wcol0;
+    }
+}
+
+// the 16-class chunks c0 = 16 par + 32 i of the pass (par 0: converter warp, 1: its helper)
+__device__ __forceinline__ void i8_epi_chunks(const I8Epi& e, int par, float& best, int& best_c) {
+    const bool warp_big = __any_sync(0xFFFFFFFFu, e.n_big != 0);  // warp-uniform variant
+    for (int c0 = 16 * par; c0 < e.nc; c0 += 32) {
+        if (warp_big) i8_combine16<true>(e, c0, best, best_c);
+        else i8_combine16<false>(e, c0, best, best_c);
+    }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kI8Threads, 1)
 svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
                    const __grid_constant__ CUtensorMap b_map, const uint16_t* __restrict__ desc,
@@ -155,6 +243,10 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
     int32_t* dlist = reinterpret_cast<int32_t*>(dbits + kI8DbitsWords);
     int32_t* dcount = dlist + kI8Distinct;
     float* wcol = reinterpret_cast<float*>(dcount + 4);  // [kI8Distinct][kI8PassClasses]
+    // per row: its count of entries above 255 (for the helpers) and the helpers' argmax
+    int32_t* nbig = reinterpret_cast<int32_t*>(wcol + kI8Distinct * kI8PassClasses);
+    float* hbest = reinterpret_cast<float*>(nbig + kGemmM);
+    int32_t* hcls = reinterpret_cast<int32_t*>(hbest + kGemmM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -248,6 +340,46 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
                     if (elect_one()) mma_commit_pair(tmem_full, 0x3);
                     __syncwarp();
                 }
+            }
+        }
+    } else if (warp >= 6) {
+        // ===================== epilogue helpers (warps 6..9): the odd 16-class chunks of the
+        // TMEM lane quarter of converter warp (warp & 3); their per-row argmax is merged by
+        // the converter through shared memory
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        int pc = 0;
+        uint32_t acc_ph = 0;
+        for (int t = pair; t < n_tiles; t += n_pairs_grid) {
+            const int64_t crop = (int64_t)t * 2 * kGemmM + (int64_t)rank * kGemmM + row;
+            int class0 = 0;
+            for (int p = 0; p < h.n_pass; ++p) {
+                const int nc = i8_pass_classes(C, p);
+                named_barrier_sync(2, 256);
+                I8Epi e;
+                e.tab = epi_tab + (pc & 1) * kI8PassClasses;
+                e.nc = nc; e.class0 = class0; e.C = C;
+                e.live = crop < n; e.staged = *dcount <= kI8Distinct; e.n_big = nbig[row];
+                e.row = row; e.big_d = big_d; e.big_hi = big_hi; e.W = W; e.dim = h.dim;
+                e.scores = scores; e.crop = crop;
+                i8_epi_corrections(e, wcol);
+                mbar_wait(tmem_full, acc_ph);
+                acc_ph ^= 1;
+                tc_fence_after();
+                e.lane_addr = tmem_base + ((uint32_t)(quarter * 32) << 16);
+                e.X = (int32_t)tmem_ld1(e.lane_addr + kI8OnesCol);
+                tmem_ld_wait();
+                float best = 0.0f;
+                int best_c = -1;
+#ifndef LBP_I8_NOEPI
+                i8_epi_chunks(e, 1, best, best_c);
+#endif
+                hbest[row] = best;
+                hcls[row] = best_c;
+                tc_fence_before();
+                named_barrier_sync(3, 256);
+                class0 += nc;
+                ++pc;
             }
         }
     } else {
@@ -349,76 +481,34 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
                         }
                     named_barrier_sync(1, 128);  // W columns staged
                 }
+                if (p == 0) nbig[row] = n_big;  // final after pass 0's conversion
+                named_barrier_sync(2, 256);     // table, column lists and counts for the helpers
                 mbar_wait(tmem_full, acc_ph);
                 acc_ph ^= 1;
                 tc_fence_after();
-                const uint32_t lane_addr = tmem_base + ((uint32_t)(quarter * 32) << 16);
-                const int32_t X = (int32_t)tmem_ld1(lane_addr + kI8OnesCol);
+                I8Epi e;
+                e.lane_addr = tmem_base + ((uint32_t)(quarter * 32) << 16);
+                e.X = (int32_t)tmem_ld1(e.lane_addr + kI8OnesCol);
                 tmem_ld_wait();
-                const bool live = crop < n;
+                e.tab = tab; e.nc = nc; e.class0 = class0; e.C = C;
+                e.live = crop < n; e.staged = staged; e.n_big = n_big; e.row = row;
+                e.big_d = big_d; e.big_hi = big_hi; e.W = W; e.dim = h.dim;
+                e.scores = scores; e.crop = crop;
+                i8_epi_corrections(e, wcol);
+                const bool live = e.live;
                 const float best_prev = best;
                 const int best_c_prev = best_c;
-                // the row's correction terms, hoisted out of the class loop (smem addresses of
-                // its staged W columns; zero weights beyond n_big)
-                double hi_r[kI8BigMax];
-                uint32_t woff[kI8BigMax];
-                const uint32_t wcol0 = smem_u32(wcol);
-#pragma unroll
-                for (int e = 0; e < kI8BigMax; ++e) {
-                    const bool on = staged && e < n_big;
-                    hi_r[e] = on ? (double)big_hi[row * kI8BigMax + e] : 0.0;
-                    woff[e] = on ? wcol0 + (uint32_t)big_d[row * kI8BigMax + e] * (kI8PassClasses * 4)
-                                 : wcol0;
-                }
-                auto combine32 = [&](int c0, auto with_big) {
-                    constexpr bool kBig = decltype(with_big)::value;
-                    long long q[32];
-                    uint32_t v[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) q[j] = 0;
-#pragma unroll
-                    for (int k = 0; k < kI8Digits; ++k) {
-                        tmem_ld32(lane_addr + (uint32_t)(k * kI8PassClasses + c0), v);
-                        tmem_ld_wait_regs(v);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) q[j] = (q[j] << 8) + (int32_t)v[j];
+#ifndef LBP_I8_NOEPI  // (developer ablation: the class loops removed)
+                i8_epi_chunks(e, 0, best, best_c);
+#endif
+                named_barrier_sync(3, 256);  // the helper's partial argmax of this row
+                {
+                    const float hb = hbest[row];
+                    const int hc = hcls[row];
+                    if (hc >= 0 && (best_c < 0 || hb > best || (hb == best && hc < best_c))) {
+                        best = hb;
+                        best_c = hc;
                     }
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int lc = c0 + j;
-                        const double2 sb = tab[lc < kI8PassClasses ? lc : 0];
-                        // s = b + m (Q 2^-39 - X) [+ the high parts of entries above 255]
-                        const double sm = fma((double)q[j], 0x1p-39, -(double)X);
-                        double acc = fma(sb.x, sm, sb.y);
-                        if (kBig && lc < nc) {
-                            if (staged) {  // independent shared loads, no dependent chain
-#pragma unroll
-                                for (int e = 0; e < kI8BigMax; ++e)
-                                    acc = fma(hi_r[e],
-                                              (double)__uint_as_float(ld_shared_u32(
-                                                  woff[e] + (uint32_t)lc * 4)), acc);
-                            } else {
-                                const float* wc = W + (size_t)(class0 + lc) * h.dim;
-                                for (int e = 0; e < n_big; ++e)
-                                    acc = fma((double)big_hi[row * kI8BigMax + e],
-                                              (double)__ldg(wc + big_d[row * kI8BigMax + e]), acc);
-                            }
-                        }
-                        const float sc = (float)acc;
-                        if (lc < nc && live) {
-                            if (scores) scores[crop * C + class0 + lc] = sc;
-                            if (best_c < 0 || sc > best) {
-                                best = sc;
-                                best_c = class0 + lc;
-                            }
-                        }
-                    }
-                };
-                // tcgen05.ld is warp-collective: the whole warp runs one variant
-                const bool warp_big = __any_sync(0xFFFFFFFFu, n_big != 0);
-                for (int c0 = 0; c0 < nc; c0 += 32) {
-                    if (warp_big) combine32(c0, std::true_type{});
-                    else combine32(c0, std::false_type{});
                 }
                 if (row_over && live) {  // many entries above 255: the row in fp64
                     best = best_prev;
@@ -469,7 +559,7 @@ inline cudaError_t launch_svm_gemm_i8(const uint16_t* desc, int32_t n, int32_t d
     const int stages = 3;
     const int smem = stages * kI8StageBytes + 1024 + 512 + 2 * kI8PassClasses * 16 +
                      2 * kGemmM * kI8BigMax * 4 + kI8DbitsWords * 4 + (kI8Distinct + 4) * 4 +
-                     kI8Distinct * kI8PassClasses * 4;
+                     kI8Distinct * kI8PassClasses * 4 + 3 * kGemmM * 4;
     cudaError_t e = cudaFuncSetAttribute(svm_gemm_i8_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
