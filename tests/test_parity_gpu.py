@@ -354,3 +354,19 @@ def test_svm_prepare_i8_digit_roundtrip(lb):
         assert m[c] > np.abs(W[c]).max() and np.log2(m[c]) == np.round(np.log2(m[c]))
         assert np.abs(m[c] * (2 * u - 1) - W[c].astype(np.float64)).max() <= 2.0 ** -40 * m[c]
     assert (nat[:, 480, :D] == 1).all() and (nat[:, 480, D:] == 0).all()
+
+
+@pytest.mark.parametrize("C", [130, 8])
+def test_svm_fp16_multi_pass_wide_descriptors(lb, C):
+    """dim above the INT8 layout's limit (33,000): the fp16 scorer, in 2 passes for C = 130
+    (124 + 6 classes) -- both epilogue warps of each lane quarter on a short last pass -- and
+    one short pass for C = 8 (the helper warps have at most one 8-class group)"""
+    rng = np.random.default_rng(C)
+    n, D = 160, 16 * 16 * 256 * 2 // 2 + 4096  # 36,864 dims
+    desc = rng.integers(0, 3, (n, D)).astype(np.uint16)
+    W, b = synthgen.svm_weights(C, D, seed=C)
+    s, lab, top = _gpu_svm(lb, desc, W, b, prepared=True)
+    s_ref, lab_ref, _ = oracle.svm_score(desc, W, b)
+    ok, worst = svm_tolerance_ok(desc, W, b, s, s_ref)
+    assert ok, worst
+    assert labels_agree_away_from_ties(s_ref, lab, lab_ref, desc, W, b)
