@@ -492,8 +492,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
 #pragma unroll
             for (int k = 0; k < 4; ++k) red_shared_add(colb[k] + p.bin[k] * (32 * 4), p.val[k]);
         };
-        // 16 rows, straight-line.  Cell rows with 15 rows run a 16th dummy row whose
-        // increments are 0 (its pixels belong to the next warp; its rows exist in the crop).
+        // 16 rows, straight-line (the 15-row cell rows stop before the 16th).
         constexpr bool kMaskRow = HAS_DEPTH && !DEPTH_SRC;  // a separate depth centre row
         Row r0 = build_row(raw_row(g0)), r1 = build_row(raw_row(g0 + kRowStep));
         Raw wn = raw_row(g0 + 2 * kRowStep), dn{0u, 0u, 0u};
@@ -506,9 +505,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 wn = raw_row(g0 + (j + 3) * kRowStep);
                 if constexpr (kMaskRow) dn = raw_depth(d0 + (j + 1) * kDRow);
             }
-            if (j == 15 && nrows < 16) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
+            if (j == 15 && nrows < 16) {  // a 15-row cell row: no 16th row (warp-uniform)
+                flush(pend);
+                break;
             }
             const Row r2 = build_row(wc);
             const Pend p = do_row(r0, r1, r2, dc);
@@ -516,10 +515,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             pend = p;
             r0 = r1;
             r1 = r2;
+            if (j == 15) flush(pend);
         }
-        flush(pend);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
 
         if (gtid == 0) bulk_wait_read_all();        // previous descriptor left the staging
         named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
