@@ -355,9 +355,12 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     };
 
     int32_t pending = -1;  // last crop whose descriptor was bulk-stored
+    // the group's next ROI is loaded one crop ahead (its latency hidden by the current crop)
+    lbp_roi_t roi_next = group < n_pos ? rois[crop_of(group)] : lbp_roi_t{};
     for (int i = group; i < n_pos; i += kGroups) {
         const int32_t n = crop_of(i);
-        const lbp_roi_t roi = rois[n];
+        const lbp_roi_t roi = roi_next;
+        if (i + kGroups < n_pos) roi_next = rois[crop_of(i + kGroups)];
         const int s = i % kStages;
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
         if (!is_fast(roi)) {
