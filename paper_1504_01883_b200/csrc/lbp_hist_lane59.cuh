@@ -43,7 +43,7 @@ constexpr int kDescBytes = 64 * kBins * 2;                     // 7,552
 constexpr int kGroupBytes = (kHistBytes + kDescBytes + 255) / 256 * 256;  // 23,040 (+ staging)
 constexpr int kLutBytes = 65 * 128;  // 64 lane-banked rows + the dummy row (bin 59 everywhere)
 constexpr uint32_t kDummyOff2 = 0x84008400u;  // LUT offset of the dummy row, both halves
-static_assert(kStages >= kGroups, "every group needs a stage");
+static_assert(kStages == kGroups, "a group refills its own stage with its next crop");
 
 // Stage layout of the two variants.  FRAME (ROIs at any column of wider frames): the grey
 // box is 144 px wide at x & ~15 and the depth box 136 px at x & ~7 (TMA needs 16-B aligned
@@ -280,10 +280,10 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     };
     // part bit 1: arrive (+ expect the stage's bytes) and load all but a late grey box;
     // part bit 2: the late grey box (kLateGrey)
-    auto issue = [&](int i, int part) {
+    // (r: the ROI of position i, already loaded by the caller)
+    auto issue = [&](int i, int part, const lbp_roi_t& r) {
         if (i >= n_pos) return;
         const int s = i % kStages;
-        const lbp_roi_t r = rois[crop_of(i)];
         if (is_fast(r)) {
             uint8_t* st = smem + s * kStageBytes;
             const int gx = FRAME ? (r.x & ~15) : r.x, dx = FRAME ? (r.x & ~7) : r.x;
@@ -318,7 +318,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         fence_mbar_init();
         prefetch_tensormap(&grey_map);
         if (HAS_DEPTH) prefetch_tensormap(&depth_map);
-        for (int i = 0; i < kStages; ++i) issue(i, 3);
+        for (int i = 0; i < kStages; ++i)
+            if (i < n_pos) issue(i, 3, rois[crop_of(i)]);
     }
     __syncthreads();
 
@@ -355,7 +356,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     };
 
     int32_t pending = -1;  // last crop whose descriptor was bulk-stored
-    // the group's next ROI is loaded one crop ahead (its latency hidden by the current crop)
+    // the group's next ROI is loaded one crop ahead (its latency hidden by the current crop);
+    // with kStages == kGroups it is also the position whose TMA this group issues next
     lbp_roi_t roi_next = group < n_pos ? rois[crop_of(group)] : lbp_roi_t{};
     for (int i = group; i < n_pos; i += kGroups) {
         const int32_t n = crop_of(i);
@@ -366,7 +368,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (!is_fast(roi)) {
             if (gtid == 0) {  // stage s was never filled: release it at once
                 if (FRAME) bulk_wait_read_all();  // (the staging may live in the stage)
-                issue(i + kStages, 3);
+                issue(i + kStages, 3, roi_next);  // (position i + 3 = this group's next)
             }
             if (DEPTH_SRC)
                 extract_roi_generic<kBins, kGroupThreads>(
@@ -524,7 +526,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (gtid == 0) bulk_wait_read_all();        // previous descriptor left the staging
         named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
         if (gtid == 0) {
-            issue(i + kStages, 1);
+            issue(i + kStages, 1, roi_next);
             if (roi_status) roi_status[n] = LBP_OK;
         }
         // ---- epilogue: quad q = (g, bin, cx) holds the 4 lane columns of cells (4g + j, cx),
@@ -558,9 +560,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
             if (kLateGrey) {  // the grey box overwrites the staging: wait for the store's read
                 bulk_wait_read_all();
-                issue(i + kStages, 2);
-            } else if (FRAME) {
-                issue(i + kStages, 2);  // (no-op: nothing is late)
+                issue(i + kStages, 2, roi_next);
             }
         }
         pending = n;
