@@ -153,9 +153,12 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
     };
 
+    // the group's next ROI is loaded one crop ahead (its latency hidden by the current crop)
+    lbp_roi_t roi_next = group < n_pos ? rois[crop_of(group)] : lbp_roi_t{};
     for (int i = group; i < n_pos; i += kGroups) {
         const int32_t n = crop_of(i);
-        const lbp_roi_t roi = rois[n];
+        const lbp_roi_t roi = roi_next;
+        if (i + kGroups < n_pos) roi_next = rois[crop_of(i + kGroups)];
         const int s = i % kStages;
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
         if (!roi_is_fast(roi, geom)) {
@@ -219,17 +222,12 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
                 wn = ld_shared_u32(g0 + (j + 3) * kTile);
                 if constexpr (HAS_DEPTH) dn = ld_shared_u32x2(d0 + (j + 1) * (kTile * 2));
             }
-            if (j == 15 && nrows < 16) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) mult_row[k] = 0u;
-            }
+            if (j == 15 && nrows < 16) break;  // a 15-row cell row (warp-uniform)
             const LaneRow r2 = lane_row_w(wc);
             do_row(r0, r1, r2, dc);
             r0 = r1;
             r1 = r2;
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) mult_row[k] = mult[k];
 
         named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
         if (gtid == 0) {
