@@ -118,7 +118,7 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
 
     // ---- per-lane / per-warp constants
     const uint32_t byte_mult = 1u << (8 * (warp & 3));
-    uint32_t mult[4], mult_row[4], colk[4];
+    uint32_t mult[4], colk[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int x = 4 * lane + k;
@@ -126,7 +126,6 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int cx = inner ? (8 * x - 1) / (kTile - 2) : (lane >> 2);
         colk[k] = (cx == (lane >> 2)) ? lane : 4 * cx;  // spill-over -> next cell's lane
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
-        mult_row[k] = mult[k];
     }
     // start values (all of TL, T, TR set) and dummy-bin addresses per pixel pair
     const uint32_t top_a = opaque(((0x6400u + 4u * colk[0] + 896u)) |
@@ -194,15 +193,15 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
                 t0 = (t0 & m0) | (dum_a & ~m0);
                 t1 = (t1 & m1) | (dum_b & ~m1);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
+                for (int k = 0; k < 4; ++k) val[k] = mult[k];
             } else if (HAS_DEPTH) {
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) val[k] = (x[k] <= span16) ? mult_row[k] : 0u;
+                for (int k = 0; k < 4; ++k) val[k] = (x[k] <= span16) ? mult[k] : 0u;
             } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
+                for (int k = 0; k < 4; ++k) val[k] = mult[k];
             }
             const uint32_t a[4] = {gbase + (t0 & 0xFFFFu), __umulhi(t0, 0x10000u) + gbase,
                                    gbase + (t1 & 0xFFFFu), __umulhi(t1, 0x10000u) + gbase};

@@ -325,7 +325,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
 
     // ---- per-lane / per-warp constants
     const uint32_t byte_mult = 1u << (8 * (warp & 3));
-    uint32_t colb[4], mult[4], mult_row[4];
+    uint32_t colb[4], mult[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int x = 4 * lane + k;
@@ -334,7 +334,6 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int col = (cx == (lane >> 2)) ? lane : 4 * cx;  // spill-over -> next cell's lane
         colb[k] = opaque(hist0 + (uint32_t)(((warp >> 2) * kBinsAlloc * 32 + col) * 4));
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
-        mult_row[k] = mult[k];
     }
     const uint32_t lo16 = win.lo << 16;
     const uint32_t span16 = (win.span << 16) | 0xFFFFu;
@@ -469,7 +468,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 t0 = (t0 & m0) | (kDummyOff2 & ~m0);
                 t1 = (t1 & m1) | (kDummyOff2 & ~m1);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
+                for (int k = 0; k < 4; ++k) val[k] = mult[k];
             } else if (HAS_DEPTH) {
                 uint2 d;
                 if constexpr (DEPTH_SRC) d = make_uint2(mid.raw0, mid.raw1);  // centre row
@@ -478,10 +477,10 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
                                        d.y - lo16};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) val[k] = (x[k] <= span16) ? mult_row[k] : 0u;
+                for (int k = 0; k < 4; ++k) val[k] = (x[k] <= span16) ? mult[k] : 0u;
             } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) val[k] = mult_row[k];
+                for (int k = 0; k < 4; ++k) val[k] = mult[k];
             }
             const uint32_t la[4] = {lutb | (t0 & 0xFFFFu), __umulhi(t0, 0x10000u) + lutb,
                                     lutb | (t1 & 0xFFFFu), __umulhi(t1, 0x10000u) + lutb};
