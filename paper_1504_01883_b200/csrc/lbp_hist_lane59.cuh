@@ -48,8 +48,8 @@ static_assert(kStages == kGroups, "a group refills its own stage with its next c
 // Stage layout of the two variants.  FRAME (ROIs at any column of wider frames): the grey
 // box is 144 px wide at x & ~15 and the depth box 136 px at x & ~7 (TMA needs 16-B aligned
 // box starts), so each lane's 4 columns start og = x & 15 bytes (grey) / od = x & 7 pixels
-// (depth) into the staged row; the 7,552-B descriptor staging then lives inside the group's
-// own stage (stage == group since kStages == kGroups) to stay within shared memory.
+// (depth) into the staged row; the 7,552-B descriptor is then staged over the group's
+// consumed counters (no room for a separate buffer) and copied out by the group.
 template <bool FRAME>
 struct Layout {
     static constexpr int kGreyW = FRAME ? 144 : kTile;   // grey row bytes in a stage
@@ -69,8 +69,7 @@ struct Layout {
     static_assert(kStageBytes % 128 == 0 && kGreyBytes % 128 == 0 && kLutMin % 256 == 0,
                   "alignment");
     static_assert(kLutMin + kTailBytes <= 227 * 1024, "shared memory");
-    static_assert(!FRAME || kStages == kGroups, "frame staging lives in the group's stage");
-    static_assert(kDescBytes <= kGreyBytes, "staging fits a stage region");
+    static_assert(kDescBytes <= kBinsAlloc * 32 * 4, "FRAME staging fits over one cell-row group");
 };
 }  // namespace l59
 
@@ -255,8 +254,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     // the next grey box is loaded only once the descriptor store has read the staging (the
     // depth box goes first); without depth it uses the unused depth region, for the depth
     // source the unused grey region.
-    constexpr bool kLateGrey = FRAME && HAS_DEPTH && !DEPTH_SRC;
-    constexpr uint32_t kStagingOff = (FRAME && !HAS_DEPTH) ? kGreyBytes : 0;
+    // FRAME: no room for a staging buffer; the descriptor is staged over the group's consumed
+    // counters (see the epilogue) and copied out by the group, so, as for crop stacks, both
+    // boxes of the next crop are issued as soon as the rows are done
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
                                                ~uintptr_t(127));
@@ -265,8 +265,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const int warp = gtid >> 5, lane = gtid & 31;
     const uint32_t stages0 = smem_u32(smem);
     const uint32_t hist0 = stages0 + kGroupOff + group * kGroupBytes;
-    const uint32_t staging = FRAME ? stages0 + group * kStageBytes + kStagingOff
-                                   : hist0 + kHistBytes;
+    const uint32_t staging = FRAME ? hist0 : hist0 + kHistBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     const uint32_t bar_id = 1 + group;
 
@@ -278,23 +277,19 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     auto is_fast = [&](const lbp_roi_t& r) {
         return FRAME ? roi_is_fast_frame(r, geom) : roi_is_fast(r, geom);
     };
-    // part bit 1: arrive (+ expect the stage's bytes) and load all but a late grey box;
-    // part bit 2: the late grey box (kLateGrey)
+    // fill position i into its stage
     // (r: the ROI of position i, already loaded by the caller)
-    auto issue = [&](int i, int part, const lbp_roi_t& r) {
+    auto issue = [&](int i, const lbp_roi_t& r) {
         if (i >= n_pos) return;
         const int s = i % kStages;
         if (is_fast(r)) {
             uint8_t* st = smem + s * kStageBytes;
             const int gx = FRAME ? (r.x & ~15) : r.x, dx = FRAME ? (r.x & ~7) : r.x;
-            if (part & 1) {
-                mbar_arrive_expect_tx(&bars[s], DEPTH_SRC ? kStageBytes - kGreyBytes
-                                                          : HAS_DEPTH ? kStageBytes : kGreyBytes);
-                if (HAS_DEPTH) tma_load_3d(st + kGreyBytes, &depth_map, &bars[s], dx, r.y, r.img);
-            }
-            if (!DEPTH_SRC && (part & (kLateGrey ? 2 : 1)))
-                tma_load_3d(st, &grey_map, &bars[s], gx, r.y, r.img);
-        } else if (part & 1) {
+            mbar_arrive_expect_tx(&bars[s], DEPTH_SRC ? kStageBytes - kGreyBytes
+                                                      : HAS_DEPTH ? kStageBytes : kGreyBytes);
+            if (HAS_DEPTH) tma_load_3d(st + kGreyBytes, &depth_map, &bars[s], dx, r.y, r.img);
+            if (!DEPTH_SRC) tma_load_3d(st, &grey_map, &bars[s], gx, r.y, r.img);
+        } else {
             mbar_arrive(&bars[s]);
         }
     };
@@ -319,7 +314,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         prefetch_tensormap(&grey_map);
         if (HAS_DEPTH) prefetch_tensormap(&depth_map);
         for (int i = 0; i < kStages; ++i)
-            if (i < n_pos) issue(i, 3, rois[crop_of(i)]);
+            if (i < n_pos) issue(i, rois[crop_of(i)]);
     }
     __syncthreads();
 
@@ -366,8 +361,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
         if (!is_fast(roi)) {
             if (gtid == 0) {  // stage s was never filled: release it at once
-                if (FRAME) bulk_wait_read_all();  // (the staging may live in the stage)
-                issue(i + kStages, 3, roi_next);  // (position i + 3 = this group's next)
+                issue(i + kStages, roi_next);  // (position i + 3 = this group's next)
             }
             if (DEPTH_SRC)
                 extract_roi_generic<kBins, kGroupThreads>(
@@ -525,42 +519,87 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (gtid == 0) bulk_wait_read_all();        // previous descriptor left the staging
         named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
         if (gtid == 0) {
-            issue(i + kStages, 1, roi_next);
+            issue(i + kStages, roi_next);
             if (roi_status) roi_status[n] = LBP_OK;
         }
         // ---- epilogue: quad q = (g, bin, cx) holds the 4 lane columns of cells (4g + j, cx),
         // j = byte.  Byte-transpose the 4 words and sum each byte column with IDP4A.
-        for (int q = gtid; q < 2 * kBinsAlloc * 8; q += kGroupThreads) {
-            const uint32_t qa = hist0 + q * 16;
-            const int g = q / (kBinsAlloc * 8), rem = q - g * (kBinsAlloc * 8);
-            const int bin = rem >> 3, cx = rem & 7;
-            if (bin == kBins) {  // dummy bin (masked-out pixels): only re-zeroed
-                st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
-                continue;
-            }
+        auto counts = [&](uint32_t qa) {
             const uint4 w = ld_shared_u32x4(qa);
-            st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
             const uint32_t lo01 = prmt(w.x, w.y, 0x5140), hi01 = prmt(w.x, w.y, 0x7362);
             const uint32_t lo23 = prmt(w.z, w.w, 0x5140), hi23 = prmt(w.z, w.w, 0x7362);
-            const uint32_t c0 = __dp4a(prmt(lo01, lo23, 0x5410), 0x01010101u, 0u);
-            const uint32_t c1 = __dp4a(prmt(lo01, lo23, 0x7632), 0x01010101u, 0u);
-            const uint32_t c2 = __dp4a(prmt(hi01, hi23, 0x5410), 0x01010101u, 0u);
-            const uint32_t c3 = __dp4a(prmt(hi01, hi23, 0x7632), 0x01010101u, 0u);
-            const uint32_t o = staging + (((4 * g) * 8 + cx) * kBins + bin) * 2;  // cell (4g, cx)
-            constexpr uint32_t kRow = 8 * kBins * 2;                             // next cell row
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "h"((uint16_t)c0) : "memory");
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + kRow), "h"((uint16_t)c1) : "memory");
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 2 * kRow), "h"((uint16_t)c2) : "memory");
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 3 * kRow), "h"((uint16_t)c3) : "memory");
-        }
-        fence_proxy_async_smem();                   // staging writes -> async proxy
-        named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-        if (gtid == 0) {
-            bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
-            if (kLateGrey) {  // the grey box overwrites the staging: wait for the store's read
-                bulk_wait_read_all();
-                issue(i + kStages, 2, roi_next);
+            return make_uint4(__dp4a(prmt(lo01, lo23, 0x5410), 0x01010101u, 0u),
+                              __dp4a(prmt(lo01, lo23, 0x7632), 0x01010101u, 0u),
+                              __dp4a(prmt(hi01, hi23, 0x5410), 0x01010101u, 0u),
+                              __dp4a(prmt(hi01, hi23, 0x7632), 0x01010101u, 0u));
+        };
+        auto put = [&](int g, int bin, int cx, uint4 c) {  // cells (4g + j, cx), j = 0..3
+            const uint32_t o = staging + (((4 * g) * 8 + cx) * kBins + bin) * 2;
+            constexpr uint32_t kRow = 8 * kBins * 2;  // next cell row
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o), "h"((uint16_t)c.x) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + kRow), "h"((uint16_t)c.y) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 2 * kRow), "h"((uint16_t)c.z) : "memory");
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(o + 3 * kRow), "h"((uint16_t)c.w) : "memory");
+        };
+        if constexpr (FRAME) {
+            // staging over the consumed counters: g = 0's counts to registers, barrier, then
+            // written over g = 0's counters; g = 1's read (and re-zeroed) and written after
+            // them; the group copies the row out with 16-B stores and re-zeroes g = 0
+            constexpr int kQ = kBinsAlloc * 8;  // quads per cell-row group
+            constexpr int kIt = (kQ + kGroupThreads - 1) / kGroupThreads;
+            uint4 cnt[kIt];
+#pragma unroll
+            for (int k = 0; k < kIt; ++k) {
+                const int q = gtid + k * kGroupThreads;
+                if (q < kQ && (q >> 3) < kBins) cnt[k] = counts(hist0 + q * 16);
             }
+            named_barrier_sync(bar_id, kGroupThreads);  // every g = 0 counter read
+#pragma unroll
+            for (int k = 0; k < kIt; ++k) {
+                const int q = gtid + k * kGroupThreads;
+                if (q < kQ && (q >> 3) < kBins) put(0, q >> 3, q & 7, cnt[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < kIt; ++k) {
+                const int q = gtid + k * kGroupThreads;
+                if (q < kQ) {
+                    const uint32_t qa = hist0 + (kQ + q) * 16;
+                    if ((q >> 3) < kBins) cnt[k] = counts(qa);
+                    st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kIt; ++k) {
+                const int q = gtid + k * kGroupThreads;
+                if (q < kQ && (q >> 3) < kBins) put(1, q >> 3, q & 7, cnt[k]);
+            }
+            named_barrier_sync(bar_id, kGroupThreads);  // staging complete
+            uint16_t* out = desc + (int64_t)n * desc_stride;
+            for (int idx = gtid; idx < kQ; idx += kGroupThreads) {  // g = 0 region: 480 x 16 B
+                const uint32_t sa = hist0 + idx * 16;
+                if (idx < kDescBytes / 16) {
+                    const uint4 v = ld_shared_u32x4(sa);
+                    *reinterpret_cast<uint4*>(out + idx * 8) = v;
+                }
+                st_shared_u32x4(sa, make_uint4(0, 0, 0, 0));
+            }
+            named_barrier_sync(bar_id, kGroupThreads);  // counters zero for the next crop
+        } else {
+            for (int q = gtid; q < 2 * kBinsAlloc * 8; q += kGroupThreads) {
+                const uint32_t qa = hist0 + q * 16;
+                const int g = q / (kBinsAlloc * 8), rem = q - g * (kBinsAlloc * 8);
+                const int bin = rem >> 3, cx = rem & 7;
+                if (bin == kBins) {  // dummy bin (masked-out pixels): only re-zeroed
+                    st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+                    continue;
+                }
+                const uint4 c = counts(qa);
+                st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+                put(g, bin, cx, c);
+            }
+            fence_proxy_async_smem();                   // staging writes -> async proxy
+            named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
+            if (gtid == 0) bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
         }
         pending = n;
     }
