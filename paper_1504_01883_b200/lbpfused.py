@@ -96,6 +96,12 @@ def lbp_descriptor_dim(cells_x: int, cells_y: int, bins: int) -> int:
     return d
 
 
+def _require(ok: bool, what: str) -> None:
+    """Argument check that survives `python -O` (the C ABI trusts these sizes and types)."""
+    if not ok:
+        raise ValueError(f"lbpfused: argument check failed: {what}")
+
+
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
@@ -142,15 +148,19 @@ def lbp_fused_extract(grey: torch.Tensor, depth: torch.Tensor | None, rois: torc
                       stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Descriptors u16 [n_rois][cells_y*cells_x*bins] of the ROIs (int32 [n][5] = img,x,y,w,h)."""
     _check_cuda(grey, depth, rois, out, roi_status)
-    assert grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)
-    assert rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5
+    _require(grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16),
+             "grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)")
+    _require(rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5,
+             "rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5")
     n = rois.shape[0]
     dim = lbp_descriptor_dim(cells_x, cells_y, bins)
     if out is None:
         out = torch.empty((n, dim), dtype=torch.uint16, device=grey.device)
-    assert out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim
+    _require(out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim,
+             "out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim")
     if roi_status is not None:
-        assert roi_status.dtype == torch.int32 and roi_status.numel() >= n
+        _require(roi_status.dtype == torch.int32 and roi_status.numel() >= n,
+                 "roi_status.dtype == torch.int32 and roi_status.numel() >= n")
     st = lib().lbp_fused_extract(_ptr(grey), _ptr(depth), images_geometry(grey, depth),
                                  _ptr(rois), n, dmin, dmax, cells_x, cells_y, bins, _ptr(out),
                                  _ptr(roi_status), _stream(stream))
@@ -167,9 +177,11 @@ def lbp_extract_source(grey: torch.Tensor | None, depth: torch.Tensor | None,
     """Descriptors with the code source selectable (LBP_SRC_GREY / _DEPTH / _FUSED): u16
     [n_rois][dim] (grey or depth) or [n_rois][2*dim] (fused: grey block then depth block)."""
     _check_cuda(grey, depth, rois, out, roi_status)
-    assert grey is None or grey.dtype == torch.uint8
-    assert depth is None or depth.dtype == torch.uint16
-    assert rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5
+    _require(grey is None or grey.dtype == torch.uint8, "grey is None or grey.dtype == torch.uint8")
+    _require(depth is None or depth.dtype == torch.uint16,
+             "depth is None or depth.dtype == torch.uint16")
+    _require(rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5,
+             "rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5")
     if grey is None and depth is None:
         raise LbpError(LBP_E_ARG, "lbp_extract_source: no image plane")
     n = rois.shape[0]
@@ -177,9 +189,11 @@ def lbp_extract_source(grey: torch.Tensor | None, depth: torch.Tensor | None,
     dev = (grey if grey is not None else depth).device
     if out is None:
         out = torch.empty((n, dim), dtype=torch.uint16, device=dev)
-    assert out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim
+    _require(out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim,
+             "out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim")
     if roi_status is not None:
-        assert roi_status.dtype == torch.int32 and roi_status.numel() >= n
+        _require(roi_status.dtype == torch.int32 and roi_status.numel() >= n,
+                 "roi_status.dtype == torch.int32 and roi_status.numel() >= n")
     st = lib().lbp_extract_source(_ptr(grey), _ptr(depth), images_geometry(grey, depth),
                                   _ptr(rois), n, dmin, dmax, cells_x, cells_y, bins, source,
                                   _ptr(out), _ptr(roi_status), _stream(stream))
@@ -197,9 +211,11 @@ def lbp_extract_resized(grey: torch.Tensor | None, depth: torch.Tensor | None,
     """Descriptors of the ROIs cropped (clamped) and resized to size x size on the GPU
     (grey bilinear, depth nearest)."""
     _check_cuda(grey, depth, rois, out, roi_status)
-    assert grey is None or grey.dtype == torch.uint8
-    assert depth is None or depth.dtype == torch.uint16
-    assert rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5
+    _require(grey is None or grey.dtype == torch.uint8, "grey is None or grey.dtype == torch.uint8")
+    _require(depth is None or depth.dtype == torch.uint16,
+             "depth is None or depth.dtype == torch.uint16")
+    _require(rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5,
+             "rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5")
     if grey is None and depth is None:
         raise LbpError(LBP_E_ARG, "lbp_extract_resized: no image plane")
     n = rois.shape[0]
@@ -207,9 +223,11 @@ def lbp_extract_resized(grey: torch.Tensor | None, depth: torch.Tensor | None,
     dev = (grey if grey is not None else depth).device
     if out is None:
         out = torch.empty((n, dim), dtype=torch.uint16, device=dev)
-    assert out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim
+    _require(out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim,
+             "out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim")
     if roi_status is not None:
-        assert roi_status.dtype == torch.int32 and roi_status.numel() >= n
+        _require(roi_status.dtype == torch.int32 and roi_status.numel() >= n,
+                 "roi_status.dtype == torch.int32 and roi_status.numel() >= n")
     st = lib().lbp_extract_resized(_ptr(grey), _ptr(depth), images_geometry(grey, depth),
                                    _ptr(rois), n, size, dmin, dmax, cells_x, cells_y, bins,
                                    source, _ptr(out), _ptr(roi_status), _stream(stream))
@@ -228,9 +246,12 @@ def lbp_recognize(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.Te
     """Descriptors + SVM in one call (one fused launch for small batches):
     returns (desc u16 [n][dim], scores fp32 [n][C] or None, labels int32 [n], top fp32 [n])."""
     _check_cuda(grey, depth, rois, W, bias, prepared, desc, labels, top_score, roi_status)
-    assert grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)
-    assert rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5
-    assert W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32
+    _require(grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16),
+             "grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)")
+    _require(rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5,
+             "rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5")
+    _require(W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32,
+             "W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32")
     n = rois.shape[0]
     dim = lbp_descriptor_dim(cells_x, cells_y, bins)
     C = W.shape[0]
@@ -277,8 +298,10 @@ def svm_score(desc: torch.Tensor, W: torch.Tensor, bias: torch.Tensor, prepared=
               scores: torch.Tensor | None = None, stream=None):
     """(scores fp32 [n][C] or None, labels int32 [n], top fp32 [n]) of the linear OvR SVM."""
     _check_cuda(desc, W, bias, prepared)
-    assert desc.dtype == torch.uint16 and desc.is_contiguous()
-    assert W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32
+    _require(desc.dtype == torch.uint16 and desc.is_contiguous(),
+             "desc.dtype == torch.uint16 and desc.is_contiguous()")
+    _require(W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32,
+             "W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32")
     n, dim = desc.shape
     C = W.shape[0]
     if W.shape[1] != dim or bias.numel() != C:
@@ -330,8 +353,10 @@ def svm_score_l1(desc: torch.Tensor, W: torch.Tensor, bias: torch.Tensor, block:
                  stream=None):
     """(scores or None, labels, top) of the SVM on per-block L1-normalised descriptors."""
     _check_cuda(desc, W, bias)
-    assert desc.dtype == torch.uint16 and desc.is_contiguous()
-    assert W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32
+    _require(desc.dtype == torch.uint16 and desc.is_contiguous(),
+             "desc.dtype == torch.uint16 and desc.is_contiguous()")
+    _require(W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32,
+             "W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32")
     n, dim = desc.shape
     C = W.shape[0]
     if W.shape[1] != dim or bias.numel() != C:
@@ -352,8 +377,10 @@ def svm_train_ovr(desc: torch.Tensor, labels: torch.Tensor, n_classes: int, orde
     """One-vs-rest linear SVM training on the GPU (exact integer Pegasos form): returns
     (W fp32 [C][dim], bias fp32 [C]) (and z int64 [C][dim+1] when return_z)."""
     _check_cuda(desc, labels, order)
-    assert desc.dtype == torch.uint16 and desc.is_contiguous()
-    assert labels.dtype == torch.int32 and order.dtype == torch.int32 and order.is_contiguous()
+    _require(desc.dtype == torch.uint16 and desc.is_contiguous(),
+             "desc.dtype == torch.uint16 and desc.is_contiguous()")
+    _require(labels.dtype == torch.int32 and order.dtype == torch.int32 and order.is_contiguous(),
+             "labels.dtype == torch.int32 and order.dtype == torch.int32 and order.is_contiguous()")
     n, dim = desc.shape
     dev = desc.device
     W = torch.empty((n_classes, dim), dtype=torch.float32, device=dev)
@@ -374,7 +401,8 @@ def desc_pack_u8(desc: torch.Tensor, row_base: int = 0, cap: int = 4096,
     [cap][4] = lbp_desc_exc_t records (row lo, row hi, index, value), count int32 [1]).
     count > cap after the stream synchronises means the list was truncated."""
     _check_cuda(desc, packed, exc, count)
-    assert desc.dtype == torch.uint16 and desc.is_contiguous() and desc.dim() == 2
+    _require(desc.dtype == torch.uint16 and desc.is_contiguous() and desc.dim() == 2,
+             "desc.dtype == torch.uint16 and desc.is_contiguous() and desc.dim() == 2")
     n, dim = desc.shape
     dev = desc.device
     if packed is None:
@@ -383,8 +411,10 @@ def desc_pack_u8(desc: torch.Tensor, row_base: int = 0, cap: int = 4096,
         exc = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=dev)
     if count is None:
         count = torch.empty(1, dtype=torch.int32, device=dev)
-    assert packed.dtype == torch.uint8 and packed.is_contiguous() and packed.numel() >= n * dim
-    assert exc.dtype == torch.int32 and exc.is_contiguous() and exc.numel() >= 4 * cap
+    _require(packed.dtype == torch.uint8 and packed.is_contiguous() and packed.numel() >= n * dim,
+             "packed.dtype == torch.uint8 and packed.is_contiguous() and packed.numel() >= n * dim")
+    _require(exc.dtype == torch.int32 and exc.is_contiguous() and exc.numel() >= 4 * cap,
+             "exc.dtype == torch.int32 and exc.is_contiguous() and exc.numel() >= 4 * cap")
     st = lib().lbp_desc_pack_u8(_ptr(desc), n, dim, row_base, _ptr(packed), _ptr(exc), cap,
                                 _ptr(count), _stream(stream))
     if st != LBP_OK:
@@ -397,15 +427,19 @@ def desc_unpack_u8(packed: torch.Tensor, exc: torch.Tensor, counts: torch.Tensor
     """Inverse of desc_pack_u8 (lbp_desc_unpack_u8): u16 [n][dim] from packed u8 [n][dim] and
     len(counts) exception lists of `cap` records each (exc int32 [len(counts) * cap][4])."""
     _check_cuda(packed, exc, counts, out)
-    assert packed.dtype == torch.uint8 and packed.is_contiguous() and packed.dim() == 2
-    assert exc.dtype == torch.int32 and exc.is_contiguous()
-    assert counts.dtype == torch.int32 and counts.is_contiguous()
+    _require(packed.dtype == torch.uint8 and packed.is_contiguous() and packed.dim() == 2,
+             "packed.dtype == torch.uint8 and packed.is_contiguous() and packed.dim() == 2")
+    _require(exc.dtype == torch.int32 and exc.is_contiguous(),
+             "exc.dtype == torch.int32 and exc.is_contiguous()")
+    _require(counts.dtype == torch.int32 and counts.is_contiguous(),
+             "counts.dtype == torch.int32 and counts.is_contiguous()")
     n, dim = packed.shape
     n_lists = counts.numel()
-    assert exc.numel() >= 4 * n_lists * cap
+    _require(exc.numel() >= 4 * n_lists * cap, "exc.numel() >= 4 * n_lists * cap")
     if out is None:
         out = torch.empty((n, dim), dtype=torch.uint16, device=packed.device)
-    assert out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim
+    _require(out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim,
+             "out.dtype == torch.uint16 and out.is_contiguous() and out.numel() >= n * dim")
     st = lib().lbp_desc_unpack_u8(_ptr(packed), n, dim, row_base, _ptr(exc), _ptr(counts),
                                   n_lists, cap, _ptr(out), _stream(stream))
     if st != LBP_OK:
