@@ -42,7 +42,8 @@ constexpr int kGemmM = 128;
 constexpr int kGemmK = 64;                  // K per pipeline stage (fp16 elements)
 constexpr int kRowBytes = kGemmK * 2;       // one swizzled smem row: 128 B (SWIZZLE_128B)
 constexpr int kDimAlign = 64;               // workspace dim padding
-constexpr int kGemmThreads = 352;  // 11 warps (see svm_gemm_kernel)
+constexpr int kGemmThreads = 480;  // 15 warps (see svm_gemm_kernel)
+constexpr int kEpiWays = 3;        // epilogue warps per TMEM lane quarter (checker + 2 helpers)
 constexpr uint32_t kPrepMagic = 0x53564D31u;  // "SVM1"
 
 struct SvmPrepHeader {
@@ -151,19 +152,20 @@ struct GemmSmem {
 //   empty[s]   both: pair MMAs and this CTA's 4 checker warps done with stage s (count 5)
 //   tmem_full  both: accumulators of the pass complete        (multicast commit)
 //   tmem_empty leader: both CTAs' epilogues drained TMEM      (count 8)
-// Epilogue of one pass for one accumulator row: the 8-class groups c8 = 8 par + 16 i (par 0:
-// the checker warp, 1: its helper), 32 TMEM columns per tcgen05.ld, double-buffered (the next
-// own group is in flight while the current one is combined).  Accumulators hold (integer
-// sum) * 2^-24, so digit k weighs 2^(16-9k); the fp64 combination is exact and
-// fma(scale, q, bias) rounds once.  Running argmax over ascending classes (ties -> lowest).
+// Epilogue of one pass for one accumulator row: the 4-class groups c4 = 4 (par + kEpiWays i)
+// (par 0: the checker warp, 1..kEpiWays-1: its helpers), 16 TMEM columns per tcgen05.ld,
+// double-buffered (the next own group is in flight while the current one is combined).
+// Accumulators hold (integer sum) * 2^-24, so digit k weighs 2^(16-9k); the fp64 combination
+// is exact and fma(scale, q, bias) rounds once.  Running argmax over ascending classes (ties
+// -> lowest).
 __device__ __forceinline__ void svm_epilogue_groups(uint32_t lane_addr, const double2* tab,
                                                     int nc, int par, bool live, float* scores,
                                                     int64_t crop, int C, int class0,
                                                     float& best, int& best_c) {
-    auto combine8 = [&](const uint32_t (&v)[32], int c8) {
+    auto combine4 = [&](const uint32_t (&v)[16], int c4) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int lc = c8 + j;
+        for (int j = 0; j < 4; ++j) {
+            const int lc = c4 + j;
             const double2 sb = tab[lc < kPassClasses ? lc : 0];
             double q = (double)__uint_as_float(v[4 * j + 0]) * 0x1p16;
             q = fma((double)__uint_as_float(v[4 * j + 1]), 0x1p7, q);
@@ -179,20 +181,21 @@ __device__ __forceinline__ void svm_epilogue_groups(uint32_t lane_addr, const do
             }
         }
     };
-    uint32_t va[32], vb[32];
-    int c8 = 8 * par;
-    if (c8 < nc) {
-        tmem_ld32(lane_addr + (uint32_t)(4 * c8), va);
+    constexpr int kStep = 4 * kEpiWays;
+    uint32_t va[16], vb[16];
+    int c4 = 4 * par;
+    if (c4 < nc) {
+        tmem_ld16(lane_addr + (uint32_t)(4 * c4), va);
         tmem_ld_wait_regs(va);
     }
-    for (; c8 < nc; c8 += 32) {
-        const bool has_b = c8 + 16 < nc, has_a2 = c8 + 32 < nc;  // warp-uniform
-        if (has_b) tmem_ld32(lane_addr + (uint32_t)(4 * (c8 + 16)), vb);
-        combine8(va, c8);
+    for (; c4 < nc; c4 += 2 * kStep) {
+        const bool has_b = c4 + kStep < nc, has_a2 = c4 + 2 * kStep < nc;  // warp-uniform
+        if (has_b) tmem_ld16(lane_addr + (uint32_t)(4 * (c4 + kStep)), vb);
+        combine4(va, c4);
         if (has_b) {
             tmem_ld_wait_regs(vb);
-            if (has_a2) tmem_ld32(lane_addr + (uint32_t)(4 * (c8 + 32)), va);
-            combine8(vb, c8 + 16);
+            if (has_a2) tmem_ld16(lane_addr + (uint32_t)(4 * (c4 + 2 * kStep)), va);
+            combine4(vb, c4 + kStep);
             if (has_a2) tmem_ld_wait_regs(va);
         }
     }
@@ -359,9 +362,10 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         double2* epi_tab = reinterpret_cast<double2*>(smem + stages * stage_bytes + 512);
-        float* hbest = reinterpret_cast<float*>(epi_tab + 2 * kPassClasses);
-        int* hcls = reinterpret_cast<int*>(hbest + kGemmM);
-        const int* flag = hcls + kGemmM;
+        const int par = 1 + (warp - 7) / 4;  // helper set 1 (warps 7..10) or 2 (11..14)
+        float* hbest = reinterpret_cast<float*>(epi_tab + 2 * kPassClasses) + (par - 1) * kGemmM;
+        int* hcls = reinterpret_cast<int*>(reinterpret_cast<float*>(epi_tab + 2 * kPassClasses) +
+                                           (kEpiWays - 1) * kGemmM) + (par - 1) * kGemmM;
         int pc = 0;
         uint32_t acc_ph = 0;
         for (int t = pair; t < n_tiles; t += n_pairs_grid) {
@@ -370,8 +374,7 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
             for (int p = 0; p < h.n_pass; ++p) {
                 const int nc = pass_classes(C, p);
                 const double2* tab = epi_tab + (pc & 1) * kPassClasses;
-                named_barrier_sync(2, 256);  // the pass's (scale, bias) table is written
-                (void)flag;
+                named_barrier_sync(2, 128 * kEpiWays);  // the pass's (scale, bias) table
                 mbar_wait(tmem_full, acc_ph);
                 acc_ph ^= 1;
                 tc_fence_after();
@@ -379,12 +382,12 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                 const bool live = crop < n;
                 float best = 0.0f;
                 int best_c = -1;
-                svm_epilogue_groups(lane_addr, tab, nc, 1, live, scores, crop, C, class0, best,
+                svm_epilogue_groups(lane_addr, tab, nc, par, live, scores, crop, C, class0, best,
                                     best_c);
                 hbest[row] = best;
                 hcls[row] = best_c;
                 tc_fence_before();
-                named_barrier_sync(3, 256);  // partial argmaxes visible to the checkers
+                named_barrier_sync(3, 128 * kEpiWays);  // partial argmaxes for the checkers
                 class0 += nc;
                 ++pc;
             }
@@ -432,7 +435,7 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                                                    (double)__ldg(bias + class0 + i))
                                     : make_double2(0.0, 0.0);
                 const bool tile_big = named_barrier_or(1, 128, flag_or != 0);
-                named_barrier_sync(2, 256);  // the table for the helper warps
+                named_barrier_sync(2, 128 * kEpiWays);  // the table for the helper warps
                 mbar_wait(tmem_full, acc_ph);
                 if (et == 0) SVM_TRACE(3);
                 acc_ph ^= 1;
@@ -446,18 +449,21 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
                 const bool live = crop < n;
                 const float best_prev = best;  // argmax over the earlier passes
                 const int best_c_prev = best_c;
-                // the even 8-class groups here, the odd ones in the helper warp of this quarter
+                // the 4-class groups 0, 3, 6, .. here, the others in the two helper warps
                 svm_epilogue_groups(lane_addr, tab, nc, 0, live, scores, crop, C, class0, best,
                                     best_c);
-                named_barrier_sync(3, 256);  // the helper's partial argmax of this row
+                named_barrier_sync(3, 128 * kEpiWays);  // the helpers' partial argmaxes
                 {
-                    float* hbest = reinterpret_cast<float*>(epi_tab + 2 * kPassClasses);
-                    const int* hcls = reinterpret_cast<const int*>(hbest + kGemmM);
-                    const float hb = hbest[row];
-                    const int hc = hcls[row];
-                    if (hc >= 0 && (best_c < 0 || hb > best || (hb == best && hc < best_c))) {
-                        best = hb;
-                        best_c = hc;
+                    const float* hbest = reinterpret_cast<const float*>(epi_tab + 2 * kPassClasses);
+                    const int* hcls = reinterpret_cast<const int*>(hbest + (kEpiWays - 1) * kGemmM);
+#pragma unroll
+                    for (int hset = 0; hset < kEpiWays - 1; ++hset) {
+                        const float hb = hbest[hset * kGemmM + row];
+                        const int hc = hcls[hset * kGemmM + row];
+                        if (hc >= 0 && (best_c < 0 || hb > best || (hb == best && hc < best_c))) {
+                            best = hb;
+                            best_c = hc;
+                        }
                     }
                 }
                 if (!exact && live) {
@@ -538,7 +544,7 @@ inline cudaError_t launch_svm_gemm(const uint16_t* desc, int32_t n, int32_t dim,
     if (stages < 2) return cudaErrorNotSupported;
     // + 1024 alignment slack + 512 barriers + epilogue table
     const int smem = stages * stage_bytes + 1024 + 512 + 2 * kPassClasses * 16 +
-                     2 * kGemmM * 4 + 16;  // + the helper warps' per-row argmax
+                     2 * (kEpiWays - 1) * kGemmM * 4 + 16;  // + the helpers' per-row argmax
     cudaError_t e = cudaFuncSetAttribute(svm_gemm_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
