@@ -37,8 +37,10 @@ constexpr int kI8OnesCol = kI8Digits * kI8PassClasses;  // 480
 constexpr int kI8K = 128;            // K per stage: one 128-B u8 row
 constexpr int kI8DimAlign = 128;
 constexpr int kI8MaxDim = 33000;     // 255 * 255 * dim < 2^31
-constexpr int kI8Threads = 320;      // warp 0 producer, 1 MMA, 2-5 converters + epilogue,
-                                     // 6-9 epilogue helpers
+constexpr int kI8Threads = 448;      // warp 0 producer, 1 MMA, 2-5 converters + epilogue,
+                                     // 6-13 epilogue helpers (two per TMEM lane quarter)
+constexpr int kI8EpiWays = 3;        // epilogue warps per lane quarter
+constexpr int kI8Chunk = 8;          // classes per epilogue chunk (x8 TMEM loads)
 constexpr uint32_t kPrep8Magic = 0x53564D38u;  // "SVM8"
 constexpr int kI8BigMax = 4;         // recorded entries above 255 per descriptor row
 constexpr int kI8Distinct = 40;      // distinct such columns per CTA tile with W staged in smem
@@ -146,24 +148,24 @@ struct I8Epi {
     int64_t crop;
 };
 
-// 16 classes [c0, c0 + 16) of the pass: Q by Horner over the 5 digit planes (x16 TMEM loads),
+// kI8Chunk classes [c0, c0 + kI8Chunk) of the pass: Q by Horner over the 5 digit planes,
 // s = b + m (Q 2^-39 - X) [+ the exact high parts of entries above 255]; running argmax over
 // ascending classes (ties -> lowest).  kBig: the warp has rows with entries above 255.
 template <bool kBig>
 __device__ __forceinline__ void i8_combine16(const I8Epi& e, int c0, float& best, int& best_c) {
-    long long q[16];
-    uint32_t v[16];
+    long long q[kI8Chunk];
+    uint32_t v[kI8Chunk];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) q[j] = 0;
+    for (int j = 0; j < kI8Chunk; ++j) q[j] = 0;
 #pragma unroll
     for (int k = 0; k < kI8Digits; ++k) {
-        tmem_ld16(e.lane_addr + (uint32_t)(k * kI8PassClasses + c0), v);
+        tmem_ld8(e.lane_addr + (uint32_t)(k * kI8PassClasses + c0), v);
         tmem_ld_wait_regs(v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) q[j] = (q[j] << 8) + (int32_t)v[j];
+        for (int j = 0; j < kI8Chunk; ++j) q[j] = (q[j] << 8) + (int32_t)v[j];
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < kI8Chunk; ++j) {
         const int lc = c0 + j;
         const double2 sb = e.tab[lc < kI8PassClasses ? lc : 0];
         const double sm = fma((double)q[j], 0x1p-39, -(double)e.X);
@@ -206,10 +208,11 @@ __device__ __forceinline__ void i8_epi_corrections(I8Epi& e, const float* wcol) 
     }
 }
 
-// the 16-class chunks c0 = 16 par + 32 i of the pass (par 0: converter warp, 1: its helper)
+// the chunks c0 = kI8Chunk (par + kI8EpiWays i) of the pass (par 0: converter warp, 1..:
+// its helpers)
 __device__ __forceinline__ void i8_epi_chunks(const I8Epi& e, int par, float& best, int& best_c) {
     const bool warp_big = __any_sync(0xFFFFFFFFu, e.n_big != 0);  // warp-uniform variant
-    for (int c0 = 16 * par; c0 < e.nc; c0 += 32) {
+    for (int c0 = kI8Chunk * par; c0 < e.nc; c0 += kI8Chunk * kI8EpiWays) {
         if (warp_big) i8_combine16<true>(e, c0, best, best_c);
         else i8_combine16<false>(e, c0, best, best_c);
     }
@@ -245,8 +248,8 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
     float* wcol = reinterpret_cast<float*>(dcount + 4);  // [kI8Distinct][kI8PassClasses]
     // per row: its count of entries above 255 (for the helpers) and the helpers' argmax
     int32_t* nbig = reinterpret_cast<int32_t*>(wcol + kI8Distinct * kI8PassClasses);
-    float* hbest = reinterpret_cast<float*>(nbig + kGemmM);
-    int32_t* hcls = reinterpret_cast<int32_t*>(hbest + kGemmM);
+    float* hbest = reinterpret_cast<float*>(nbig + kGemmM);           // [helper set][row]
+    int32_t* hcls = reinterpret_cast<int32_t*>(hbest + (kI8EpiWays - 1) * kGemmM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -343,6 +346,7 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
             }
         }
     } else if (warp >= 6) {
+        const int par = 1 + (warp - 6) / 4;  // helper set 1 (warps 6..9) or 2 (10..13)
         // ===================== epilogue helpers (warps 6..9): the odd 16-class chunks of the
         // TMEM lane quarter of converter warp (warp & 3); their per-row argmax is merged by
         // the converter through shared memory
@@ -355,7 +359,7 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
             int class0 = 0;
             for (int p = 0; p < h.n_pass; ++p) {
                 const int nc = i8_pass_classes(C, p);
-                named_barrier_sync(2, 256);
+                named_barrier_sync(2, 128 * kI8EpiWays);
                 I8Epi e;
                 e.tab = epi_tab + (pc & 1) * kI8PassClasses;
                 e.nc = nc; e.class0 = class0; e.C = C;
@@ -372,12 +376,12 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
                 float best = 0.0f;
                 int best_c = -1;
 #ifndef LBP_I8_NOEPI
-                i8_epi_chunks(e, 1, best, best_c);
+                i8_epi_chunks(e, par, best, best_c);
 #endif
-                hbest[row] = best;
-                hcls[row] = best_c;
+                hbest[(par - 1) * kGemmM + row] = best;
+                hcls[(par - 1) * kGemmM + row] = best_c;
                 tc_fence_before();
-                named_barrier_sync(3, 256);
+                named_barrier_sync(3, 128 * kI8EpiWays);
                 class0 += nc;
                 ++pc;
             }
@@ -482,7 +486,7 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
                     named_barrier_sync(1, 128);  // W columns staged
                 }
                 if (p == 0) nbig[row] = n_big;  // final after pass 0's conversion
-                named_barrier_sync(2, 256);     // table, column lists and counts for the helpers
+                named_barrier_sync(2, 128 * kI8EpiWays);  // table, lists, counts for the helpers
                 mbar_wait(tmem_full, acc_ph);
                 acc_ph ^= 1;
                 tc_fence_after();
@@ -501,10 +505,11 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
 #ifndef LBP_I8_NOEPI  // (developer ablation: the class loops removed)
                 i8_epi_chunks(e, 0, best, best_c);
 #endif
-                named_barrier_sync(3, 256);  // the helper's partial argmax of this row
-                {
-                    const float hb = hbest[row];
-                    const int hc = hcls[row];
+                named_barrier_sync(3, 128 * kI8EpiWays);  // the helpers' partial argmaxes
+#pragma unroll
+                for (int hset = 0; hset < kI8EpiWays - 1; ++hset) {
+                    const float hb = hbest[hset * kGemmM + row];
+                    const int hc = hcls[hset * kGemmM + row];
                     if (hc >= 0 && (best_c < 0 || hb > best || (hb == best && hc < best_c))) {
                         best = hb;
                         best_c = hc;
@@ -559,7 +564,7 @@ inline cudaError_t launch_svm_gemm_i8(const uint16_t* desc, int32_t n, int32_t d
     const int stages = 3;
     const int smem = stages * kI8StageBytes + 1024 + 512 + 2 * kI8PassClasses * 16 +
                      2 * kGemmM * kI8BigMax * 4 + kI8DbitsWords * 4 + (kI8Distinct + 4) * 4 +
-                     kI8Distinct * kI8PassClasses * 4 + 3 * kGemmM * 4;
+                     kI8Distinct * kI8PassClasses * 4 + (1 + 2 * (kI8EpiWays - 1)) * kGemmM * 4;
     cudaError_t e = cudaFuncSetAttribute(svm_gemm_i8_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
