@@ -169,21 +169,30 @@ svm_train_ovr_reg_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t d
                 const ZT y = (labs[r] == c) ? 1 : -1;
                 bool viol = true;
                 if (t > 1) {
-                    long long part = 0;
+                    // two independent accumulators (even / odd entries): half the dependent
+                    // chain of 64-bit multiply-adds
+                    long long pe = 0, po = 0;
 #pragma unroll
                     for (int k = 0; k < PAIRS; ++k) {
-                        part += (long long)z[2 * k] * (long long)(buf[r][k] & 0xFFFFu);
-                        part += (long long)z[2 * k + 1] * (long long)(buf[r][k] >> 16);
+                        pe += (long long)z[2 * k] * (long long)(buf[r][k] & 0xFFFFu);
+                        po += (long long)z[2 * k + 1] * (long long)(buf[r][k] >> 16);
                     }
+                    long long part = pe + po;
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1)
                         part += __shfl_xor_sync(0xFFFFFFFFu, part, off);
                     const int rb = (int)(t & 1);
                     if (lane == 0) red[rb][warp] = part;
                     __syncthreads();
-                    long long dot = (long long)zb;
+                    // the warp partials summed as a tree (exact in int64, any order)
+                    long long rs[kWarps];
 #pragma unroll
-                    for (int w = 0; w < kWarps; ++w) dot += red[rb][w];
+                    for (int w = 0; w < kWarps; ++w) rs[w] = red[rb][w];
+#pragma unroll
+                    for (int h = kWarps / 2; h > 0; h >>= 1)
+#pragma unroll
+                        for (int w = 0; w < h; ++w) rs[w] += rs[w + h];
+                    const long long dot = (long long)zb + rs[0];
                     // (an incremental loop-carried threshold and a 32-bit division both
                     // measured slower: this form depends only on t and overlaps the reduction)
                     const long long thr = (long long)((t - 1 + inv_lambda - 1) / inv_lambda);
