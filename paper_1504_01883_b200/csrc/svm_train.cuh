@@ -178,9 +178,22 @@ svm_train_ovr_reg_kernel(const uint16_t* __restrict__ desc, int32_t n, int32_t d
                         po += (long long)z[2 * k + 1] * (long long)(buf[r][k] >> 16);
                     }
                     long long part = pe + po;
+                    if constexpr (Z32) {
+                        // |part| < 16 * 2^31 * 2^16 = 2^51: three 17-bit pieces (the top one
+                        // signed) each summed over the warp by one redux.sync -- exact (every
+                        // sum < 2^22) and without the five dependent shuffle rounds
+                        const unsigned long long u = (unsigned long long)part;
+                        const int pc = (int)(u & 0x1FFFFu), pb = (int)((u >> 17) & 0x1FFFFu);
+                        const int pa = (int)(part >> 34);
+                        const int sc = __reduce_add_sync(0xFFFFFFFFu, pc);
+                        const int sb = __reduce_add_sync(0xFFFFFFFFu, pb);
+                        const int sa = __reduce_add_sync(0xFFFFFFFFu, pa);
+                        part = (long long)sa * (1ll << 34) + (long long)sb * (1ll << 17) + sc;
+                    } else {
 #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1)
-                        part += __shfl_xor_sync(0xFFFFFFFFu, part, off);
+                        for (int off = 16; off > 0; off >>= 1)
+                            part += __shfl_xor_sync(0xFFFFFFFFu, part, off);
+                    }
                     const int rb = (int)(t & 1);
                     if (lane == 0) red[rb][warp] = part;
                     __syncthreads();
