@@ -102,6 +102,8 @@ def parse():
                    help="config5: extraction/all-gather overlap chunks (1 = serial)")
     p.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                    help="process-group backend for N > 1 (gloo: functional check only)")
+    p.add_argument("--launch-check", action="store_true",
+                   help="(tests) print each rank's RANK / WORLD_SIZE and exit")
     p.add_argument("--compact", action="store_true",
                    help="config5: all-gather u8 descriptors + exception lists (serial; "
                         "lbp_desc_pack_u8 / lbp_desc_unpack_u8), and time pack/unpack")
@@ -120,7 +122,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, device_index: int, period_s: float = 0.005):
+    def __init__(self, device_index: int, period_s: float = 0.0005):
         self.ok = False
         self.samples, self.reasons = [], set()
         self.period = period_s
@@ -263,7 +265,8 @@ def run_reference(args):
               f"{threads} threads x unmodified single-threaded oracle on disjoint shards")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+        "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": workload_config(args, n_gpu_crops, H, Wd, cx, cy, bins, C, desc_txt),
@@ -280,7 +283,7 @@ def workload_config(args, n, H, W, cx, cy, bins, C, desc_txt):
             "cells": f"{cx}x{cy}", "bins": bins, "classes": C, "dist": args.dist,
             "depth_mask": not args.no_depth, "depth_window_mm": [DMIN, DMAX],
             "source": getattr(args, "source", "grey"),
-            "parallelism": f"crop-sharded dp{args.gpus}",
+            "parallelism": f"crop-sharded dp{int(os.environ.get('WORLD_SIZE', '1'))}",
             "pipeline": "scoring of step k overlaps extraction of step k+1 (2 streams)"
                         if getattr(args, "pipeline", False) else "serial",
             "l2": "inputs larger than L2 (no flush needed)" if n * H * W * 3 > 126e6 else
@@ -298,8 +301,36 @@ def ensure_built():
     synthgen.build_gpu()
 
 
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args):
+    """`bench.py --gpus N` (N > 1) run as a plain command: re-execute it under
+    torch.distributed.run with N ranks (one process per GPU, rendezvous on 127.0.0.1), so the
+    line reports the world size it measured.  Returns the launcher's exit code."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ, LBP_BENCH_RELAUNCHED="1"))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if args.launch_check:  # CPU test of the launcher: every rank reports what it sees
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")),
+                          "world": int(os.environ.get("WORLD_SIZE", "1")),
+                          "relaunched": os.environ.get("LBP_BENCH_RELAUNCHED") == "1"}),
+              flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
     ensure_built()
@@ -376,8 +407,12 @@ def main():
         if args.pipeline:
             ext_done[buf].record(stream)
             svm_stream.wait_event(ext_done[buf])
+        if ev is not None and not args.pipeline:
+            ev[2].record(svm_stream)
         lb.svm_score(d_k, W, b, prepared=prepared, want_scores=False, labels=labels,
                      top_score=top, stream=svm_stream)
+        if ev is not None and not args.pipeline:
+            ev[3].record(svm_stream)
         if args.pipeline:
             svm_done[buf].record(svm_stream)
 
@@ -387,7 +422,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, barrier + sync on both sides, events on the launching stream
-    ev_ext = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev_ext = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4))
               for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -403,11 +438,13 @@ def main():
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
-    ext_ms = sum(a.elapsed_time(b_) for a, b_ in ev_ext) / args.steps
-    t = torch.tensor([ms, ext_ms], device=dev, dtype=torch.float64)
+    ext_ms = sum(e[0].elapsed_time(e[1]) for e in ev_ext) / args.steps
+    svm_ms = (sum(e[2].elapsed_time(e[3]) for e in ev_ext) / args.steps
+              if not args.pipeline else float("nan"))
+    t = torch.tensor([ms, ext_ms, svm_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, ext_ms = float(t[0]), float(t[1])
+    ms, ext_ms, svm_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = ms / args.steps
     value = n * world / (ms_per_step * 1e-3)
 
@@ -433,20 +470,45 @@ def main():
                 "peak_source": peak_src, "bytes_per_crop": bpc,
                 "frac_of_nominal_8000": achieved / 8000.0,  # also vs 8 TB/s
                 "kernel_ms": ext_ms, "kernel_share_of_step": ext_ms / ms_per_step,
-                "traffic": load_traffic(args.workload) if source == 0 else None}
+                "traffic": load_traffic(args.workload, bins, args.source,
+                                        depth is not None and not args.no_depth)}
+    # the scorer's own roofline (per-phase TF/s fractions): algorithmic flops
+    # 2 n C dim of s = W x + b over its event-timed launch; the INT8 digit-plane kernel
+    # (C > 124) takes the int8 peak = the measured bf16 burst x the nominal 2x ratio
+    if not args.pipeline and prepared is not None:
+        flops = 2.0 * n * C * dim
+        i8 = C > 124
+        bf16 = load_bf16_peak()
+        pk = bf16 * (2.0 if i8 else 1.0)
+        ach = flops / (svm_ms * 1e-3) / 1e12
+        roofline["scorer"] = {
+            "bound": "tensor", "kernel": "svm_gemm_i8 (INT8 digit planes)" if i8 else
+            "svm_gemm (fp16 digit planes)", "achieved": ach, "unit": "TFLOP/s",
+            "peak": pk, "frac": ach / pk, "frac_of_bf16_burst": ach / bf16,
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8:bf16 ratio)"
+                            if i8 else "MEASURED_PEAKS.json bf16_tflops (burst)"),
+            "flops_per_step": flops, "kernel_ms": svm_ms,
+            "kernel_share_of_step": svm_ms / ms_per_step}
 
     # ---- CPU oracle baseline (rank 0, N=1 only) + equivalence gate on its sample
     cpu = None
+    gate_m = 4096 if world == 1 else 512
+    gscores, gtop, same = gate_scores(lb, torch, descs[(step_no[0] - 1) & 1], W, b, prepared,
+                                      labels, top, min(gate_m, n))
+    if not same:
+        print(json.dumps({"error": "scorer with scores requested disagrees with the timed step"}),
+              flush=True)
+        return 3
     if rank == 0 and world == 1 and not args.skip_cpu:
-        cpu, gate_ok = run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np,
-                                   cx, cy, bins)
+        cpu, gate_ok = run_cpu_leg(args, torch, grey, depth, rois, descs[(step_no[0] - 1) & 1],
+                                   labels, W_np, b_np, cx, cy, bins, gscores, gtop)
         if not gate_ok:
             print(json.dumps({"error": "equivalence gate failed: GPU != oracle on the sample"}),
                   flush=True)
             return 3
     elif world > 1:  # every rank checks its own shard's first crops; any failure stops all
-        ok = rank_gate(torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins,
-                       source, 512)
+        ok = rank_gate(torch, grey, depth, rois, descs[(step_no[0] - 1) & 1], labels, W_np, b_np,
+                       cx, cy, bins, source, 512, gscores, gtop)
         flag = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag[0]) == 0:
@@ -737,9 +799,11 @@ def run_dbbuild(args):
                         "overlaps chunk k+1's extraction" if args.chunks > 1 else "serial"},
             "compact": compact,
             "allgather": {"bytes_out_per_rank": gathered,
-                          "algbw_GBps": gathered / (gat * 1e-3) / 1e9 if gat > 0 else None,
+                          # one rank moves nothing: no bandwidth to report
+                          "algbw_GBps": gathered / (gat * 1e-3) / 1e9
+                          if gat > 0 and world > 1 and args.chunks <= 1 else None,
                           "busbw_GBps": gathered * (world - 1) / world / (gat * 1e-3) / 1e9
-                          if gat > 0 else None},
+                          if gat > 0 and world > 1 and args.chunks <= 1 else None},
             "roofline": {"bound": "hbm", "kernel": "lbp_hist (extraction)",
                          "achieved": bpc * count / (ext * 1e-3) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": bpc * count / (ext * 1e-3) / 1e9 / peak,
@@ -859,9 +923,11 @@ def run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins,
             "api": "lbp_recognize_host (C ABI, pinned host buffers)"}
 
 
-def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins):
+def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins,
+                gscores=None, gtop=None):
     """Oracle timed on this host's cores on a bounded sample; the sample's oracle output is
-    also the equivalence gate (descriptors bit-exact, labels equal away from ties)."""
+    also the equivalence gate (descriptors bit-exact, scores within R13, labels equal away
+    from ties)."""
     threads = len(os.sched_getaffinity(0))
     n = grey.shape[0]
     m = min(n, 4096)
@@ -873,7 +939,9 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
                                                         SOURCES[args.source])
     gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
     glab = labels[:m].cpu().numpy()
-    ok = gate_compare(gdesc, glab, odesc, olab, W_np, b_np)
+    ok, detail = gate_compare(gdesc, glab, odesc, olab, W_np, b_np,
+                              None if gscores is None else gscores[:m],
+                              None if gtop is None else gtop[:m])
     # SURVEY §8(d) also asks for the single-threaded oracle: one thread, first 256 crops
     r1, _, s1, _, _, _ = oracle_rate(g[:256], d[:256] if d is not None else None, r[:256], W_np,
                                      b_np, cx, cy, bins, 2.0, 1, SOURCES[args.source])
@@ -882,7 +950,8 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
                      f"(extraction + SVM), {threads} threads x unmodified single-threaded C "
                      f"oracle on disjoint shards, {secs:.1f} s",
            "single_thread_value": r1,
-           "cpu": cpu_model(), "equivalence_gate": "pass" if ok else "FAIL"}
+           "cpu": cpu_model(), "equivalence_gate": "pass" if ok else "FAIL",
+           "gate_detail": detail}
     return cpu, ok
 
 
@@ -902,19 +971,32 @@ def db_sample_ok(full, n_total, H, Wd, cx, cy, bins, args, k=8):
     return True
 
 
-def gate_compare(gdesc, glab, odesc, olab, W_np, b_np):
-    """Equivalence gate: descriptors bit-exact, labels equal wherever the oracle's top-2 gap
-    is clear of the score tolerance."""
+def gate_compare(gdesc, glab, odesc, olab, W_np, b_np, gscores=None, gtop=None):
+    """Equivalence gate: descriptors bit-exact; scores and top scores within R13 and labels equal
+    away from ties (R14) -- the one definition in oracle/tolerance.py, shared with the tests and
+    smoke()."""
     if not np.array_equal(gdesc, odesc):
-        return False
+        return False, {"descriptors": "mismatch"}
     import oracle
+    from oracle.tolerance import check_svm
     s_ref, _, _ = oracle.svm_score(odesc, W_np, b_np)
-    srt = np.sort(s_ref, axis=1)
-    clear = (srt[:, -1] - srt[:, -2]) > 1e-4 * np.maximum(np.abs(srt[:, -1]), 1e-3)
-    return bool(np.array_equal(glab[clear], olab[clear]))
+    ok, detail = check_svm(odesc, W_np, b_np, s_ref, olab, glab, s_gpu=gscores, top_gpu=gtop)
+    detail["descriptors"] = "bit-exact"
+    return ok, detail
 
 
-def rank_gate(torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins, source, m):
+def gate_scores(lb, torch, desc, W, b, prepared, labels, top, m):
+    """Scores of the gate sample from the scorer in the bench's launch configuration (the whole
+    batch, scores requested); its labels / top scores must equal the timed step's."""
+    s_full, lab_full, top_full = lb.svm_score(desc, W, b, prepared=prepared, want_scores=True)
+    torch.cuda.synchronize()
+    same = bool(torch.equal(lab_full, labels)) and bool(
+        torch.equal(top_full.view(torch.int32), top.view(torch.int32)))
+    return s_full[:m].cpu().numpy(), top_full[:m].cpu().numpy(), same
+
+
+def rank_gate(torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins, source, m,
+              gscores=None, gtop=None):
     """The equivalence gate on every rank at N > 1 (no CPU timing): the oracle on this
     rank's first m crops."""
     import oracle
@@ -925,7 +1007,10 @@ def rank_gate(torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins, 
     odesc = oracle.lbp_extract(g, d, r, DMIN, DMAX, cx, cy, bins, source=source)
     _, olab, _ = oracle.svm_score(odesc, W_np, b_np)
     gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
-    return gate_compare(gdesc, labels[:m].cpu().numpy(), odesc, olab, W_np, b_np)
+    ok, _ = gate_compare(gdesc, labels[:m].cpu().numpy(), odesc, olab, W_np, b_np,
+                         None if gscores is None else gscores[:m],
+                         None if gtop is None else gtop[:m])
+    return ok
 
 
 def rank_device(torch, local, world, args):
@@ -952,11 +1037,21 @@ def load_peaks():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def load_traffic(workload):
-    """dram read+write bytes per launch of lbp_hist from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def load_bf16_peak():
     try:
-        return json.load(open(p)).get(workload)
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except Exception:
+        return 1590.0  # B200_PROFILING.md fallback
+
+
+def load_traffic(workload, bins=59, source="grey", depth=True):
+    """dram read+write bytes per launch of the extraction kernel from the committed ncu
+    --set full capture of exactly this workload, bin count, code source and mask (None when
+    no capture of that combination is committed)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    key = f"{workload}/bins{bins}/{source}/{'mask' if depth else 'nomask'}"
+    try:
+        return json.load(open(p)).get(key)
     except Exception:
         return None
 

@@ -41,6 +41,11 @@ enum {
     LBP_E_CUDA = -6         /* CUDA launch / copy error */
 };
 
+/* Label written by the scorers for every row when `prepared` does not belong to the call's
+ * model (its header -- layout and a fingerprint of W -- was written by svm_prepare() for
+ * another W or shape); top_score and scores are NaN then.  -1 stays "rejected". */
+#define LBP_LABEL_BAD_MODEL (-2)
+
 /* An ROI ("Rect r = boundingRect(...)") inside image `img` of the stack:
  * top-left (x, y), width w, height h, in pixels.  Clamped to the image. */
 typedef struct {
@@ -142,13 +147,18 @@ int32_t lbp_extract_resized(const uint8_t* grey, const uint16_t* depth, lbp_imag
  *   desc      u16 [n][dim]        W  fp32 [n_classes][dim] row-major   bias fp32 [n_classes]
  *   prepared  nullable: workspace filled by svm_prepare() for this W (enables the
  *             tensor-core path for n >= 128); NULL = CUDA-core path
+ *   prepared_bytes  size of the `prepared` allocation; < svm_workspace_bytes(n_classes, dim)
+ *             -> LBP_E_ARG (nothing enqueued).  The tensor-core kernels also check the
+ *             workspace header on the device before reading past it: a workspace prepared
+ *             for another shape or another W (8 sampled weights differ) is not used and every
+ *             row gets labels = LBP_LABEL_BAD_MODEL, NaN top score and scores.
  *   scores    out, nullable fp32 [n][n_classes]
  *   labels    out, nullable int32 [n];  top_score out, nullable fp32 [n]
  */
 int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W,
-                  const float* bias, int32_t n_classes, const void* prepared, float* scores,
-                  int32_t* labels, float* top_score, float reject_threshold,
-                  lbp_stream_t stream);
+                  const float* bias, int32_t n_classes, const void* prepared,
+                  size_t prepared_bytes, float* scores, int32_t* labels, float* top_score,
+                  float reject_threshold, lbp_stream_t stream);
 
 /*
  * lbp_recognize -- the whole device path in one call (lbp_fused_extract + svm_score, grey
@@ -159,15 +169,17 @@ int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W,
  * per-class partials over distributed shared memory; otherwise
  * it runs the two kernels of lbp_fused_extract and svm_score.
  *   desc       out, REQUIRED: u16 [n_rois][dim] (also the scorer's input)
- *   prepared   nullable svm_prepare() workspace (tensor-core scorer for large batches)
+ *   prepared   nullable svm_prepare() workspace (tensor-core scorer for large batches);
+ *              prepared_bytes and the device-side header check as in svm_score
  *   scores / roi_status / labels / top_score  nullable outputs as in svm_score / extract
  */
 int32_t lbp_recognize(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
                       const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
                       int32_t cells_x, int32_t cells_y, int32_t bins, const float* W,
                       const float* bias, int32_t n_classes, const void* prepared,
-                      float reject_threshold, uint16_t* desc, int32_t* roi_status, float* scores,
-                      int32_t* labels, float* top_score, lbp_stream_t stream);
+                      size_t prepared_bytes, float reject_threshold, uint16_t* desc,
+                      int32_t* roi_status, float* scores, int32_t* labels, float* top_score,
+                      lbp_stream_t stream);
 
 /*
  * svm_score_l1 -- the linear OvR SVM on per-block L1-normalised descriptors (SURVEY §8f-3
@@ -259,7 +271,7 @@ int32_t svm_prepare(const float* W, int32_t n_classes, int32_t dim, void* worksp
  * Host buffers should be pinned for the copies to be asynchronous; the caller
  * synchronises `stream` before reading labels_h / top_h.
  *   workspace  device scratch of >= lbp_recognize_workspace_bytes() bytes
- *   W, bias, prepared  device model as for svm_score
+ *   W, bias, prepared, prepared_bytes  device model as for svm_score
  */
 size_t lbp_recognize_workspace_bytes(lbp_images_t geom, int32_t has_depth, int32_t n_rois,
                                      int32_t cells_x, int32_t cells_y, int32_t bins);
@@ -267,9 +279,9 @@ int32_t lbp_recognize_host(const uint8_t* grey_h, const uint16_t* depth_h, lbp_i
                            const lbp_roi_t* rois_h, int32_t n_rois, uint16_t dmin,
                            uint16_t dmax, int32_t cells_x, int32_t cells_y, int32_t bins,
                            const float* W, const float* bias, int32_t n_classes,
-                           const void* prepared, float reject_threshold, void* workspace,
-                           size_t workspace_bytes, int32_t* labels_h, float* top_h,
-                           lbp_stream_t stream);
+                           const void* prepared, size_t prepared_bytes, float reject_threshold,
+                           void* workspace, size_t workspace_bytes, int32_t* labels_h,
+                           float* top_h, lbp_stream_t stream);
 
 /* Human-readable name of a status code (static string). */
 const char* lbp_status_string(int32_t status);

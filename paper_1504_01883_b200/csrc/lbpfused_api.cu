@@ -226,11 +226,13 @@ int32_t lbp_recognize(const uint8_t* grey, const uint16_t* depth, lbp_images_t g
                       const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
                       int32_t cells_x, int32_t cells_y, int32_t bins, const float* W,
                       const float* bias, int32_t n_classes, const void* prepared,
-                      float reject_threshold, uint16_t* desc, int32_t* roi_status, float* scores,
-                      int32_t* labels, float* top_score, lbp_stream_t stream_) {
+                      size_t prepared_bytes, float reject_threshold, uint16_t* desc,
+                      int32_t* roi_status, float* scores, int32_t* labels, float* top_score,
+                      lbp_stream_t stream_) {
     if (n_rois < 0 || n_classes < 1) return LBP_E_ARG;
     const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
     if (dim < 0) return dim;
+    if (prepared && prepared_bytes < svm_workspace_bytes(n_classes, dim)) return LBP_E_ARG;
     if (dmin > dmax) return LBP_E_ARG;
     if (n_rois == 0) return LBP_OK;
     if (!grey || !rois || !desc || !W || !bias) return LBP_E_ARG;
@@ -248,8 +250,8 @@ int32_t lbp_recognize(const uint8_t* grey, const uint16_t* depth, lbp_images_t g
     st = lbp_extract_source(grey, depth, geom, rois, n_rois, dmin, dmax, cells_x, cells_y, bins,
                             LBP_SRC_GREY, desc, roi_status, stream_);
     if (st != LBP_OK) return st;
-    return svm_score(desc, n_rois, dim, W, bias, n_classes, prepared, scores, labels, top_score,
-                     reject_threshold, stream_);
+    return svm_score(desc, n_rois, dim, W, bias, n_classes, prepared, prepared_bytes, scores,
+                     labels, top_score, reject_threshold, stream_);
 }
 
 int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
@@ -261,9 +263,11 @@ int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images
 }
 
 int32_t svm_score(const uint16_t* desc, int32_t n, int32_t dim, const float* W, const float* bias,
-                  int32_t n_classes, const void* prepared, float* scores, int32_t* labels,
-                  float* top_score, float reject_threshold, lbp_stream_t stream_) {
+                  int32_t n_classes, const void* prepared, size_t prepared_bytes, float* scores,
+                  int32_t* labels, float* top_score, float reject_threshold,
+                  lbp_stream_t stream_) {
     if (n < 0 || dim < 1 || n_classes < 1) return LBP_E_ARG;
+    if (prepared && prepared_bytes < svm_workspace_bytes(n_classes, dim)) return LBP_E_ARG;
     if (n == 0) return LBP_OK;
     if (!desc || !W || !bias) return LBP_E_ARG;
     cudaStream_t stream = (cudaStream_t)stream_;
@@ -507,8 +511,9 @@ int32_t lbp_recognize_host(const uint8_t* grey_h, const uint16_t* depth_h, lbp_i
                            const lbp_roi_t* rois_h, int32_t n_rois, uint16_t dmin, uint16_t dmax,
                            int32_t cells_x, int32_t cells_y, int32_t bins, const float* W,
                            const float* bias, int32_t n_classes, const void* prepared,
-                           float reject_threshold, void* workspace, size_t workspace_bytes,
-                           int32_t* labels_h, float* top_h, lbp_stream_t stream_) {
+                           size_t prepared_bytes, float reject_threshold, void* workspace,
+                           size_t workspace_bytes, int32_t* labels_h, float* top_h,
+                           lbp_stream_t stream_) {
     if (n_rois < 0 || n_classes < 1) return LBP_E_ARG;
     const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
     if (dim < 0) return dim;
@@ -536,8 +541,8 @@ int32_t lbp_recognize_host(const uint8_t* grey_h, const uint16_t* depth_h, lbp_i
     st = lbp_fused_extract(grey, depth, geom, rois, n_rois, dmin, dmax, cells_x, cells_y, bins,
                            desc, nullptr, stream_);
     if (st != LBP_OK) return st;
-    st = svm_score(desc, n_rois, dim, W, bias, n_classes, prepared, nullptr, labels, top,
-                   reject_threshold, stream_);
+    st = svm_score(desc, n_rois, dim, W, bias, n_classes, prepared, prepared_bytes, nullptr,
+                   labels, top, reject_threshold, stream_);
     if (st != LBP_OK) return st;
     if (labels_h) e = cudaMemcpyAsync(labels_h, labels, (size_t)n_rois * 4, cudaMemcpyDeviceToHost, stream);
     if (e == cudaSuccess && top_h)

@@ -46,11 +46,57 @@ constexpr int kGemmThreads = 480;  // 15 warps (see svm_gemm_kernel)
 constexpr int kEpiWays = 3;        // epilogue warps per TMEM lane quarter (checker + 2 helpers)
 constexpr uint32_t kPrepMagic = 0x53564D31u;  // "SVM1"
 
+constexpr int kPrepSamples = 8;
 struct SvmPrepHeader {
     uint32_t magic;
     int32_t n_classes, dim, dim_pad, n_pass, rows_max, total_rows;
     int32_t scale_off, q_off;  // byte offsets inside the workspace
+    // bits of W at kPrepSamples fixed positions (svm_prepare): the scorers compare them with
+    // the W of the call, so a workspace prepared for another model is refused (labels
+    // LBP_LABEL_BAD_MODEL) instead of silently scoring with the wrong digit planes
+    uint32_t w_sample[kPrepSamples];
 };
+
+__host__ __device__ inline int64_t w_sample_pos(int i, int32_t C, int32_t dim) {
+    return (int64_t)i * ((int64_t)C * dim - 1) / (kPrepSamples - 1);
+}
+
+// svm_prepare's header write (one thread): the layout plus the W fingerprint
+__device__ inline void write_prep_header(uint8_t* ws, SvmPrepHeader h, const float* W) {
+    for (int i = 0; i < kPrepSamples; ++i)
+        h.w_sample[i] = __float_as_uint(W[w_sample_pos(i, h.n_classes, h.dim)]);
+    *reinterpret_cast<SvmPrepHeader*>(ws) = h;
+}
+
+// The scorers' check (one thread, in the prologue, before any TMA of the workspace): the
+// workspace header must describe this call's layout (same magic, classes, dim, padding, row
+// count and offsets) and carry the bits of this call's W at the sample positions.
+__device__ inline bool prep_header_ok(const uint8_t* ws, const SvmPrepHeader& h,
+                                      const float* W) {
+    const SvmPrepHeader* g = reinterpret_cast<const SvmPrepHeader*>(ws);
+    if (g->magic != h.magic || g->n_classes != h.n_classes || g->dim != h.dim ||
+        g->dim_pad != h.dim_pad || g->n_pass != h.n_pass || g->total_rows != h.total_rows ||
+        g->scale_off != h.scale_off || g->q_off != h.q_off)
+        return false;
+    for (int i = 0; i < kPrepSamples; ++i)
+        if (g->w_sample[i] != __float_as_uint(W[w_sample_pos(i, h.n_classes, h.dim)]))
+            return false;
+    return true;
+}
+
+// Outputs of a refused call: label LBP_LABEL_BAD_MODEL, NaN top score and scores.
+__device__ inline void write_bad_model(int32_t n, int32_t C, float* scores, int32_t* labels,
+                                       float* top_score) {
+    const float nan = __uint_as_float(0x7FC00000u);
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t0; i < n; i += nt) {
+        if (labels) labels[i] = LBP_LABEL_BAD_MODEL;
+        if (top_score) top_score[i] = nan;
+    }
+    if (scores)
+        for (int64_t i = t0; i < (int64_t)n * C; i += nt) scores[i] = nan;
+}
 
 __host__ __device__ inline int pass_classes(int C, int p) {
     const int lo = p * kPassClasses;
@@ -82,7 +128,7 @@ __global__ void svm_prepare_kernel(const float* __restrict__ W, SvmPrepHeader h,
                                    uint8_t* __restrict__ ws) {
     __shared__ float red[32];
     const int row = blockIdx.x;
-    if (row == 0 && threadIdx.x == 0) *reinterpret_cast<SvmPrepHeader*>(ws) = h;
+    if (row == 0 && threadIdx.x == 0) write_prep_header(ws, h, W);
     // locate (pass, local row)
     int p = 0, base = 0;
     while (p < h.n_pass && row >= base + pass_rows(pass_classes(h.n_classes, p))) {
@@ -240,10 +286,10 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
     const int pair = (int)cluster_id_x(), n_pairs_grid = (int)n_clusters_x();
     const int C = h.n_classes;
     const int KC = h.dim_pad / kGemmK;
-    const int n_tiles = (n + 2 * kGemmM - 1) / (2 * kGemmM);
     const float* scales = reinterpret_cast<const float*>(ws + h.scale_off);
 
     if (threadIdx.x == 0) {
+        tmem_slot[1] = prep_header_ok(ws, h, W) ? 0u : 1u;  // (read after __syncthreads)
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&ready[s], 2);
@@ -265,6 +311,10 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
     cluster_sync();  // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // a workspace that does not belong to this model: no tile is scored (nothing of the
+    // workspace is read past its header), every row gets LBP_LABEL_BAD_MODEL below
+    const bool bad_model = tmem_slot[1] != 0u;
+    const int n_tiles = bad_model ? 0 : (n + 2 * kGemmM - 1) / (2 * kGemmM);
     // programmatic dependent launch: the prologue above may overlap the tail of the kernel
     // that wrote the descriptors; everything below reads them (no-op without PDL)
     grid_dependency_wait();
@@ -498,6 +548,7 @@ svm_gemm_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant
             if (et == 0) SVM_TRACE(4);
         }
     }
+    if (bad_model) write_bad_model(n, C, scores, labels, top_score);
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // the peer's TMEM / smem are no longer used by the leader's MMAs

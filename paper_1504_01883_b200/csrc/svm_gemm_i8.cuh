@@ -7,8 +7,9 @@
 //   d_k in [0, 255]  (|u - U 2^-40| <= 2^-41),
 // so  sum_d x_d W[c][d] = m_c (2 sum_d x_d u_d - X),  X = sum_d x_d, and the GEMM computes the
 // five digit products S_k = sum_d x_d d_k[d] and X (an all-ones row) EXACTLY in s32 (counts
-// <= 255 as u8 operands: 255 * 255 * dim < 2^31 for dim <= 33,000).  The epilogue forms
-// Q = sum_k S_k 2^(8(4-k)) in int64 (exact, < 2^60) and s = b + m_c (Q 2^-39 - X) in fp64,
+// <= 255 as u8 operands: 255 * 255 * dim < 2^31 for dim <= 32,768).  The epilogue forms
+// Q = sum_k S_k 2^(8(4-k)) = sum_d (x_d & 255) U_d in int64 (exact: < 255 * dim * 2^40 < 2^63
+// for dim <= 32,768) and s = b + m_c (Q 2^-39 - X) in fp64,
 // rounded once to fp32 -- the oracle's definition up to the 2^-40 m_c quantisation of W and
 // fp64 rounding.  A count above 255 enters the GEMM as its low byte; its
 // high part (x - (x & 255)) W is added exactly in fp64 by the row's epilogue thread (rows with
@@ -36,7 +37,8 @@ constexpr int kI8PassClasses = 96;   // digit planes of 96 classes + X = 481 of 
 constexpr int kI8OnesCol = kI8Digits * kI8PassClasses;  // 480
 constexpr int kI8K = 128;            // K per stage: one 128-B u8 row
 constexpr int kI8DimAlign = 128;
-constexpr int kI8MaxDim = 33000;     // 255 * 255 * dim < 2^31
+constexpr int kI8MaxDim = 32768;     // 255 * 255 * dim < 2^31 (digit products, s32) and
+                                     // Q = sum_d (x_d & 255) U_d < 255 * dim * 2^40 < 2^63
 constexpr int kI8Threads = 448;      // warp 0 producer, 1 MMA, 2-5 converters + epilogue,
                                      // 6-13 epilogue helpers (two per TMEM lane quarter)
 constexpr int kI8EpiWays = 3;        // epilogue warps per lane quarter
@@ -69,7 +71,7 @@ __global__ void svm_prepare_i8_kernel(const float* __restrict__ W, SvmPrepHeader
                                       uint8_t* __restrict__ ws) {
     __shared__ float red[32];
     const int row = blockIdx.x;
-    if (row == 0 && threadIdx.x == 0) *reinterpret_cast<SvmPrepHeader*>(ws) = h;
+    if (row == 0 && threadIdx.x == 0) write_prep_header(ws, h, W);
     const int p = row / 512, sr = row % 512;
     const int nc = i8_pass_classes(h.n_classes, p);
     // pair-major storage: 512 rows = 2 MMA halves of 256; CTA r holds rows hh*256 + r*128 + j
@@ -256,10 +258,10 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
     const int pair = (int)cluster_id_x(), n_pairs_grid = (int)n_clusters_x();
     const int C = h.n_classes;
     const int KC = h.dim_pad / kI8K;
-    const int n_tiles = (n + 2 * kGemmM - 1) / (2 * kGemmM);
     const float* scales = reinterpret_cast<const float*>(ws + h.scale_off);
 
     if (threadIdx.x == 0) {
+        tmem_slot[1] = prep_header_ok(ws, h, W) ? 0u : 1u;  // (read after __syncthreads)
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&conv[s], 8);  // 4 converter warps x 2 CTAs
@@ -280,6 +282,10 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // a workspace that does not belong to this model: nothing past its header is read, every
+    // row gets LBP_LABEL_BAD_MODEL below
+    const bool bad_model = tmem_slot[1] != 0u;
+    const int n_tiles = bad_model ? 0 : (n + 2 * kGemmM - 1) / (2 * kGemmM);
     // programmatic dependent launch: the prologue above may overlap the tail of the kernel
     // that wrote the descriptors; everything below reads them (no-op without PDL)
     grid_dependency_wait();
@@ -544,6 +550,7 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
             }
         }
     }
+    if (bad_model) write_bad_model(n, C, scores, labels, top_score);
     tc_fence_before();
     __syncthreads();
     cluster_sync();

@@ -18,6 +18,7 @@ from . import build as _build
 LBP_OK, LBP_E_ARG, LBP_E_ROI, LBP_E_GRID, LBP_E_OVERFLOW, LBP_E_UNSUPPORTED, LBP_E_CUDA = \
     0, -1, -2, -3, -4, -5, -6
 LBP_SRC_GREY, LBP_SRC_DEPTH, LBP_SRC_FUSED = 0, 1, 2
+LBP_LABEL_BAD_MODEL = -2  # labels of a call whose `prepared` belongs to another model
 
 
 class LbpError(RuntimeError):
@@ -59,9 +60,9 @@ def lib():
                                           i32, i32, P, P, P]
         L.lbp_extract_resized.restype = i32
         L.lbp_recognize.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, P, P,
-                                    i32, P, f32, P, P, P, P, P, P]
+                                    i32, P, sz, f32, P, P, P, P, P, P]
         L.lbp_recognize.restype = i32
-        L.svm_score.argtypes = [P, i32, i32, P, P, i32, P, P, P, P, f32, P]
+        L.svm_score.argtypes = [P, i32, i32, P, P, i32, P, sz, P, P, P, f32, P]
         L.svm_score.restype = i32
         L.svm_score_l1.argtypes = [P, i32, i32, i32, P, P, i32, P, P, P, f32, P]
         L.svm_score_l1.restype = i32
@@ -79,7 +80,7 @@ def lib():
         L.lbp_recognize_workspace_bytes.argtypes = [lbp_images_t, i32, i32, i32, i32, i32]
         L.lbp_recognize_workspace_bytes.restype = sz
         L.lbp_recognize_host.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32,
-                                         P, P, i32, P, f32, P, sz, P, P, P]
+                                         P, P, i32, P, sz, f32, P, sz, P, P, P]
         L.lbp_recognize_host.restype = i32
         _lib = L
     return _lib
@@ -100,6 +101,42 @@ def _require(ok: bool, what: str) -> None:
     """Argument check that survives `python -O` (the C ABI trusts these sizes and types)."""
     if not ok:
         raise ValueError(f"lbpfused: argument check failed: {what}")
+
+
+def _out(t, dtype, n, what: str, device=None) -> None:
+    """A caller-provided output (or input) buffer: dtype, contiguous, >= n elements, and on
+    `device` when given (the C ABI writes n elements through the raw pointer)."""
+    if t is None:
+        return
+    _require(t.dtype == dtype, f"{what}.dtype == {dtype}")
+    _require(t.is_contiguous(), f"{what}.is_contiguous()")
+    _require(t.numel() >= n, f"{what}.numel() >= {n}")
+    if device is not None:
+        _require(t.device == device, f"{what}.device == {device}")
+
+
+def _model(W, bias, dim, device, what):
+    """W fp32 [C][dim] contiguous and bias fp32 [C] contiguous on `device`."""
+    _require(W.dtype == torch.float32 and W.is_contiguous() and W.dim() == 2,
+             f"{what}: W fp32 contiguous [C][dim]")
+    C = W.shape[0]
+    if W.shape[1] != dim or bias.numel() != C:
+        raise LbpError(LBP_E_ARG, f"{what}: weight shape mismatch")
+    _out(bias, torch.float32, C, "bias", device)
+    _require(W.device == device, f"W.device == {device}")
+    return C
+
+
+def _prepared(prepared, C, dim, device):
+    """svm_prepare() workspace: uint8 on the device, at least svm_workspace_bytes(C, dim)."""
+    if prepared is None:
+        return 0
+    _require(prepared.dtype == torch.uint8 and prepared.is_contiguous(),
+             "prepared.dtype == torch.uint8 and prepared.is_contiguous()")
+    _require(prepared.device == device, f"prepared.device == {device}")
+    _require(prepared.numel() >= svm_workspace_bytes(C, dim),
+             "prepared.numel() >= svm_workspace_bytes(C, dim)")
+    return prepared.numel()
 
 
 def _ptr(t):
@@ -250,25 +287,29 @@ def lbp_recognize(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.Te
              "grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)")
     _require(rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5,
              "rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5")
-    _require(W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32,
-             "W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32")
     n = rois.shape[0]
     dim = lbp_descriptor_dim(cells_x, cells_y, bins)
-    C = W.shape[0]
-    if W.shape[1] != dim or bias.numel() != C:
-        raise LbpError(LBP_E_ARG, "lbp_recognize: weight shape mismatch")
     dev = grey.device
+    C = _model(W, bias, dim, dev, "lbp_recognize")
+    pbytes = _prepared(prepared, C, dim, dev)
     if desc is None:
         desc = torch.empty((n, dim), dtype=torch.uint16, device=dev)
     if labels is None:
         labels = torch.empty(n, dtype=torch.int32, device=dev)
     if top_score is None:
         top_score = torch.empty(n, dtype=torch.float32, device=dev)
+    _out(desc, torch.uint16, n * dim, "desc", dev)
+    _out(labels, torch.int32, n, "labels", dev)
+    _out(top_score, torch.float32, n, "top_score", dev)
+    _out(roi_status, torch.int32, n, "roi_status", dev)
+    _require(rois.device == dev and (depth is None or depth.device == dev),
+             "rois and depth on grey's device")
     scores = torch.empty((n, C), dtype=torch.float32, device=dev) if want_scores else None
     st = lib().lbp_recognize(_ptr(grey), _ptr(depth), images_geometry(grey, depth), _ptr(rois),
                              n, dmin, dmax, cells_x, cells_y, bins, _ptr(W), _ptr(bias), C,
-                             _ptr(prepared), reject_threshold, _ptr(desc), _ptr(roi_status),
-                             _ptr(scores), _ptr(labels), _ptr(top_score), _stream(stream))
+                             _ptr(prepared), pbytes, reject_threshold, _ptr(desc),
+                             _ptr(roi_status), _ptr(scores), _ptr(labels), _ptr(top_score),
+                             _stream(stream))
     if st != LBP_OK:
         raise LbpError(st, "lbp_recognize")
     return desc, scores, labels, top_score
@@ -298,22 +339,23 @@ def svm_score(desc: torch.Tensor, W: torch.Tensor, bias: torch.Tensor, prepared=
               scores: torch.Tensor | None = None, stream=None):
     """(scores fp32 [n][C] or None, labels int32 [n], top fp32 [n]) of the linear OvR SVM."""
     _check_cuda(desc, W, bias, prepared)
-    _require(desc.dtype == torch.uint16 and desc.is_contiguous(),
-             "desc.dtype == torch.uint16 and desc.is_contiguous()")
-    _require(W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32,
-             "W.dtype == torch.float32 and W.is_contiguous() and bias.dtype == torch.float32")
+    _require(desc.dtype == torch.uint16 and desc.is_contiguous() and desc.dim() == 2,
+             "desc.dtype == torch.uint16 and desc.is_contiguous() and desc.dim() == 2")
     n, dim = desc.shape
-    C = W.shape[0]
-    if W.shape[1] != dim or bias.numel() != C:
-        raise LbpError(LBP_E_ARG, "svm_score: dimension mismatch")
     dev = desc.device
+    C = _model(W, bias, dim, dev, "svm_score")
+    pbytes = _prepared(prepared, C, dim, dev)
     if want_scores and scores is None:
         scores = torch.empty((n, C), dtype=torch.float32, device=dev)
     if labels is None:
         labels = torch.empty(n, dtype=torch.int32, device=dev)
     if top_score is None:
         top_score = torch.empty(n, dtype=torch.float32, device=dev)
-    st = lib().svm_score(_ptr(desc), n, dim, _ptr(W), _ptr(bias), C, _ptr(prepared),
+    _out(labels, torch.int32, n, "labels", dev)
+    _out(top_score, torch.float32, n, "top_score", dev)
+    if want_scores:
+        _out(scores, torch.float32, n * C, "scores", dev)
+    st = lib().svm_score(_ptr(desc), n, dim, _ptr(W), _ptr(bias), C, _ptr(prepared), pbytes,
                          _ptr(scores if want_scores else None), _ptr(labels), _ptr(top_score),
                          reject_threshold, _stream(stream))
     if st != LBP_OK:
@@ -334,15 +376,26 @@ def lbp_recognize_host(grey_h: torch.Tensor, depth_h: torch.Tensor | None, rois_
                        reject_threshold: float = -math.inf, stream=None) -> None:
     """End-to-end call from (pinned) HOST tensors; results land in labels_h / top_h after a
     sync of `stream`."""
-    _check_cuda(W, bias, workspace)
+    _check_cuda(W, bias, workspace, prepared)
     for t in (grey_h, depth_h, rois_h, labels_h, top_h):
         if t is not None and t.is_cuda:
             raise ValueError("lbp_recognize_host takes host tensors")
+    _require(grey_h.dtype == torch.uint8 and (depth_h is None or depth_h.dtype == torch.uint16),
+             "grey_h u8 and depth_h u16")
+    _require(rois_h.dtype == torch.int32 and rois_h.is_contiguous() and rois_h.shape[-1] == 5,
+             "rois_h.dtype == torch.int32 and rois_h.is_contiguous() and rois_h.shape[-1] == 5")
+    _require(workspace.dtype == torch.uint8 and workspace.is_contiguous(),
+             "workspace.dtype == torch.uint8 and workspace.is_contiguous()")
     geom = images_geometry(grey_h, depth_h)
     n = rois_h.shape[0]
+    dim = lbp_descriptor_dim(cells_x, cells_y, bins)
+    C = _model(W, bias, dim, W.device, "lbp_recognize_host")
+    pbytes = _prepared(prepared, C, dim, W.device)
+    _out(labels_h, torch.int32, n, "labels_h")
+    _out(top_h, torch.float32, n, "top_h")
     st = lib().lbp_recognize_host(_ptr(grey_h), _ptr(depth_h), geom, _ptr(rois_h), n, dmin, dmax,
-                                  cells_x, cells_y, bins, _ptr(W), _ptr(bias), W.shape[0],
-                                  _ptr(prepared), reject_threshold, _ptr(workspace),
+                                  cells_x, cells_y, bins, _ptr(W), _ptr(bias), C,
+                                  _ptr(prepared), pbytes, reject_threshold, _ptr(workspace),
                                   workspace.numel(), _ptr(labels_h), _ptr(top_h), _stream(stream))
     if st != LBP_OK:
         raise LbpError(st, "lbp_recognize_host")

@@ -140,9 +140,13 @@ def test_svm_argument_errors(L):
     from paper_1504_01883_b200 import lbpfused as lb
     P = ctypes.c_void_p
     d = P(0x1000)
-    call = lambda n=4, dim=8, C=2, desc=d, W=d, b=d: L.svm_score(
-        desc, n, dim, W, b, C, None, None, None, None, float("-inf"), None)
+    call = lambda n=4, dim=8, C=2, desc=d, W=d, b=d, prep=None, pbytes=0: L.svm_score(
+        desc, n, dim, W, b, C, prep, pbytes, None, None, None, float("-inf"), None)
     assert call(n=0) == lb.LBP_OK
+    # a prepared workspace smaller than svm_workspace_bytes(C, dim) is refused on the host
+    need = lb.svm_workspace_bytes(100, 3776)
+    assert need > 0
+    assert call(dim=3776, C=100, prep=d, pbytes=need - 1) == lb.LBP_E_ARG
     assert call(n=-1) == lb.LBP_E_ARG
     assert call(dim=0) == lb.LBP_E_ARG
     assert call(C=0) == lb.LBP_E_ARG

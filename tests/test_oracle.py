@@ -72,17 +72,25 @@ def test_special_windows():
 
 
 def test_code_range_and_equal_neighbours_all_3pow9():
-    """All 3^9 windows over {0,1,2}: code in [0,255]; bit p set iff g_p >= g_c (per-bit pin
-    through the golden weights: a set bit's weight matches the neighbour's position)."""
+    """All 3^9 = 19,683 windows over {0,1,2} (SURVEY §8c brute force): bit p set iff
+    g_p >= g_c, checked through the golden Fig. 7 weights (a set bit's weight matches the
+    neighbour's position).  Every window goes through the oracle's map routine (the windows
+    side by side in 3x3 blocks of one strip, codes read at the block centres) and every 7th
+    also through the single-window entry point."""
     _, _, weights, _ = _golden_fig7()
     grid = np.array(np.meshgrid(*[np.arange(3)] * 9, indexing="ij")).reshape(9, -1).T
-    pos = [(r, c) for r in range(3) for c in range(3) if (r, c) != (1, 1)]
-    for k in range(0, grid.shape[0], 7):  # every 7th window keeps this fast (2812 windows)
-        win = grid[k].reshape(3, 3)
-        code = oracle.lbp_code_window(win)
-        assert 0 <= code <= 255
-        expect = sum(int(weights[r, c]) for (r, c) in pos if win[r, c] >= win[1, 1])
-        assert code == expect
+    nwin = grid.shape[0]
+    assert nwin == 3 ** 9
+    wins = grid.reshape(nwin, 3, 3)
+    strip = np.ascontiguousarray(wins.transpose(1, 0, 2).reshape(3, 3 * nwin)).astype(np.uint8)
+    codes = oracle.lbp_map_u8(strip)[0, 3 * np.arange(nwin)].astype(np.int64)
+    ge = (wins >= wins[:, 1:2, 1:2]).astype(np.int64)
+    ge[:, 1, 1] = 0
+    expect = (ge * weights[None, :, :]).reshape(nwin, 9).sum(1)
+    assert np.array_equal(codes, expect)
+    assert codes.min() >= 0 and codes.max() <= 255
+    for k in range(0, nwin, 7):
+        assert oracle.lbp_code_window(wins[k]) == expect[k]
 
 
 def test_map_rotation_and_flip_metamorphic():
@@ -254,6 +262,20 @@ def test_roi_clamp_equals_intersection():
     out = oracle.lbp_extract(grey, depth, [[1, -5, 40, 30, 30]], 600, 1400, 3, 2, 59)
     ref = oracle.lbp_extract(grey, depth, [[1, 0, 40, 25, 10]], 600, 1400, 3, 2, 59)
     assert np.array_equal(out, ref)
+    # every side, on noise with every pixel counted (no all-masked / all-equal descriptors)
+    rng = np.random.default_rng(3)
+    g = rng.integers(0, 256, (2, 50, 60), dtype=np.uint8)
+    d = np.full((2, 50, 60), 1000, np.uint16)
+    cases = [([1, -5, 3, 30, 30], [1, 0, 3, 25, 30]),     # left
+             ([0, 7, -9, 20, 30], [0, 7, 0, 20, 21]),     # top
+             ([1, 45, 10, 40, 12], [1, 45, 10, 15, 12]),  # right
+             ([0, 4, 41, 20, 40], [0, 4, 41, 20, 9]),     # bottom
+             ([1, -3, -4, 80, 90], [1, 0, 0, 60, 50])]    # all four
+    for roi, inter in cases:
+        for dep in (None, d):
+            a = oracle.lbp_extract(g, dep, [roi], 600, 1400, 3, 2, 59)
+            r = oracle.lbp_extract(g, dep, [inter], 600, 1400, 3, 2, 59)
+            assert a.sum() > 0 and np.array_equal(a, r), (roi, dep is None)
 
 
 def test_roi_error_statuses():
@@ -355,4 +377,10 @@ def test_svm_ties_and_reject():
     _, lab, _ = oracle.svm_score(desc, W, b, reject_threshold=3.0)
     assert lab.tolist() == [0, -1]
     _, lab, _ = oracle.svm_score(desc, W, b, reject_threshold=float("inf"))
+    assert lab.tolist() == [-1, -1]
+    # the boundary: a top score EQUAL to the threshold is kept (strict "<")
+    _, lab, _ = oracle.svm_score(desc, W, b, reject_threshold=6.0)
+    assert lab.tolist() == [0, -1]
+    _, lab, _ = oracle.svm_score(desc, W, b, reject_threshold=float(np.nextafter(np.float32(6.0),
+                                                                                 np.float32(7.0))))
     assert lab.tolist() == [-1, -1]

@@ -370,3 +370,34 @@ def test_svm_fp16_multi_pass_wide_descriptors(lb, C):
     ok, worst = svm_tolerance_ok(desc, W, b, s, s_ref)
     assert ok, worst
     assert labels_agree_away_from_ties(s_ref, lab, lab_ref, desc, W, b)
+
+
+@pytest.mark.parametrize("C", [100, 1000])  # fp16 and INT8 digit-plane layouts
+def test_svm_prepared_for_another_model_is_refused(lb, C):
+    """a workspace prepared for another W of the same shape, or for a larger model,
+    is detected on the device (header layout + 8 sampled weights): every row gets
+    LBP_LABEL_BAD_MODEL and NaN scores, nothing past the header is read.  The right workspace
+    still scores within R13; a workspace that is too small is refused by the binding and, on
+    the host, by the C ABI (tests/test_abi.py)."""
+    desc, W1, b = _svm_inputs(300, C, seed=7)
+    W2 = W1.copy()
+    W2[C - 1, desc.shape[1] - 1] += 0.25  # differs at a sampled position (the last weight)
+    W3, _ = synthgen.svm_weights(C + 40, desc.shape[1], seed=8)
+    d = torch.from_numpy(desc.view(np.int16)).to(DEV).view(torch.uint16)
+    W1t, W2t, W3t = (torch.from_numpy(x).to(DEV) for x in (W1, W2, W3))
+    bt = torch.from_numpy(b).to(DEV)
+    prep1 = lb.svm_prepare(W1t)
+    s, lab, top = lb.svm_score(d, W2t, bt, prepared=prep1)
+    torch.cuda.synchronize()
+    assert (lab == lb.lbpfused.LBP_LABEL_BAD_MODEL).all().item()
+    assert torch.isnan(top).all().item() and torch.isnan(s).all().item()
+    prep3 = lb.svm_prepare(W3t)  # larger: passes the size check, fails the header check
+    s, lab, top = lb.svm_score(d, W1t, bt, prepared=prep3)
+    torch.cuda.synchronize()
+    assert (lab == lb.lbpfused.LBP_LABEL_BAD_MODEL).all().item()
+    s, lab, top = lb.svm_score(d, W1t, bt, prepared=prep1)  # the right one
+    s_ref, lab_ref, _ = oracle.svm_score(desc, W1, b)
+    ok, worst = svm_tolerance_ok(desc, W1, b, s.cpu().numpy(), s_ref)
+    assert ok, worst
+    with pytest.raises(ValueError):
+        lb.svm_score(d, W1t, bt, prepared=prep1[:100])
