@@ -107,6 +107,10 @@ def parse():
     p.add_argument("--compact", action="store_true",
                    help="config5: all-gather u8 descriptors + exception lists (serial; "
                         "lbp_desc_pack_u8 / lbp_desc_unpack_u8), and time pack/unpack")
+    p.add_argument("--fused", action="store_true",
+                   help="config5: the fused database build (SURVEY §8e way 2): the extraction "
+                        "epilogue stores every row into every rank's symmetric-memory copy "
+                        "(NVLS multicast when available, else NVLink peer stores) + one barrier")
     return p.parse_args()
 
 
@@ -707,8 +711,12 @@ def run_dbbuild(args):
     stream = torch.cuda.current_stream(dev)
 
     comm = torch.cuda.Stream(dev)
-    if args.compact:
-        args.chunks = 1  # the compact exchange is serial: extract, pack, all-gather, unpack
+    if args.compact or args.fused:
+        args.chunks = 1  # serial exchanges: extract (+ pack), exchange (+ unpack)
+    fdb = None
+    if args.fused:
+        from paper_1504_01883_b200.parallel import FusedDatabase
+        fdb = FusedDatabase(n_total, dim, dev)
 
     def extract_chunk(lo, hi):
         lb.lbp_fused_extract(grey, depth, rois[lo:hi], DMIN, DMAX, cx, cy, bins,
@@ -718,6 +726,13 @@ def run_dbbuild(args):
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
+        if fdb is not None:  # one kernel writes every rank's copy, then the barrier
+            full, lab = fdb.build(grey, depth, rois, labels, DMIN, DMAX, cx, cy, bins,
+                                  stream=stream)
+            if ev is not None:
+                ev[1].record(stream)
+                ev[2].record(stream)
+            return full, lab
         if args.chunks <= 1:  # serial: extract everything, then one all-gather
             lb.lbp_fused_extract(grey, depth, rois, DMIN, DMAX, cx, cy, bins, out=desc,
                                  stream=stream)
@@ -792,7 +807,8 @@ def run_dbbuild(args):
             "config": {"workload": f"config5: {desc_txt}", "crops_total": n_total,
                        "crops_per_gpu": count, "crop": f"{H}x{Wd}", "cells": f"{cx}x{cy}",
                        "bins": bins, "n_ids": N_IDS, "parallelism": f"crop-sharded dp{world} + "
-                       "all-gather"},
+                       + (f"fused gather ({fdb.mode} stores from the extraction epilogue)"
+                          if fdb is not None else "all-gather")},
             "extract_ms": ext if args.chunks <= 1 else None,
             "allgather_ms": gat if args.chunks <= 1 else None,
             "overlap": {"chunks": args.chunks, "note": "chunk k's all-gather on a second stream "
@@ -809,7 +825,7 @@ def run_dbbuild(args):
                          "unit": "GB/s", "frac": bpc * count / (ext * 1e-3) / 1e9 / peak,
                          "peak_source": peak_src, "traffic": None},
             "cpu_baseline": None, "e2e": None,
-            "gpu_launches": args.steps * (max(1, args.chunks) +
+            "gpu_launches": args.steps * (2 if fdb is not None else max(1, args.chunks) +
                                             (3 if args.compact and world > 1 else 0)),
             "clocks": clk.summary(),
             "check": {"rows": int(full.shape[0]), "label_ok": bool(

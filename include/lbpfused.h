@@ -255,6 +255,44 @@ int32_t lbp_desc_unpack_u8(const uint8_t* packed, int64_t n, int32_t dim, int64_
                            const lbp_desc_exc_t* exc, const int32_t* exc_counts, int32_t n_lists,
                            int32_t exc_cap, uint16_t* desc, lbp_stream_t stream);
 
+/*
+ * The fused database build (SURVEY §8e way 2; "online database generation"):
+ * lbp_extract_gather computes the descriptors of this rank's ROIs and writes every row ONCE,
+ * from the extraction epilogue, into the gathered training matrix of EVERY rank -- no local
+ * descriptor write followed by an all-gather collective.
+ *   LBP_GATHER_MULTIMEM  base[0] is an NVLS multicast address of the ranks' buffers
+ *                        (multimem.st: the NVSwitch replicates each 16-B store); n_dst = 1
+ *   LBP_GATHER_PEERS     base[0..n_dst-1] are the ranks' buffers as mapped on this device
+ *                        (NVLink P2P): each 16-B chunk is stored to every one of them
+ * In every destination: rows of desc_pitch u16 at byte desc_offset (row = row_base + n for
+ * this call's ROI n; entries dim..desc_pitch-1 are zero), int32 labels at labels_offset
+ * (labels[n] copied to entry row_base + n; labels_offset < 0 or labels == NULL: none).
+ * The call ends with a system-scope fence; the caller runs a cross-rank barrier (e.g. the
+ * symmetric-memory barrier) before any rank reads another rank's rows.  Host-detectable
+ * errors (LBP_E_ARG): bad mode or n_dst (MULTIMEM: 1, PEERS: 1..8), a null base, desc_offset
+ * or a base not 16-B aligned, desc_pitch < dim or not a multiple of 8, labels_offset not a
+ * multiple of 4, scratch NULL.
+ *   scratch   device u16 [n_rois][dim]: rows of ROIs off the TMA fast path are extracted here
+ *             first (and the whole batch when the fast kernel does not apply: small batches,
+ *             other grids / bins / geometries -- then a forwarding kernel does the stores)
+ */
+enum { LBP_GATHER_MULTIMEM = 1, LBP_GATHER_PEERS = 2 };
+#define LBP_GATHER_MAX_DST 8
+typedef struct {
+    int32_t mode, n_dst;
+    uint64_t base[LBP_GATHER_MAX_DST];
+    int64_t desc_offset;   /* bytes */
+    int64_t desc_pitch;    /* u16 elements per gathered row */
+    int64_t labels_offset; /* bytes; < 0 = no labels */
+    int64_t row_base;      /* gathered row of this call's ROI 0 */
+} lbp_gather_dst_t;
+
+int32_t lbp_extract_gather(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                           const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                           int32_t cells_x, int32_t cells_y, int32_t bins,
+                           const int32_t* labels, lbp_gather_dst_t dst, uint16_t* scratch,
+                           int32_t* roi_status, lbp_stream_t stream);
+
 /* Bytes of device workspace svm_prepare() needs for a [n_classes][dim] model
  * (0 if the tensor-core path does not apply to this shape). */
 size_t svm_workspace_bytes(int32_t n_classes, int32_t dim);

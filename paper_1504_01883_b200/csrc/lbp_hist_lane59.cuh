@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "gather.cuh"
 #include "lbp_hist_generic.cuh"
 #include "ptx.cuh"
 #include "tma_util.cuh"
@@ -235,14 +236,21 @@ __device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uin
 // 2^-24 (value = bits * 2^-24), so the subtraction is exact there; for larger d either
 // mid/2 <= d <= 2 mid (exact by Sterbenz) or d > 2 mid, where the rounded difference is still
 // >= mid > half; NaN / inf / negative patterns fail the compare.
-template <bool HAS_DEPTH, bool DEPTH_SRC, int WINM, bool FRAME>
+// GATHER (the fused database build, gather.cuh): the descriptor rows go from the staging
+// buffer to every destination of `gd` (multicast or peer stores) instead of a bulk store to
+// `desc`; `desc` is then local scratch for the ROIs that take the generic code path, whose
+// rows are forwarded from there.
+template <bool HAS_DEPTH, bool DEPTH_SRC, int WINM, bool FRAME, bool GATHER = false>
 __global__ void __launch_bounds__(l59::kThreads, 1)
 lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const __grid_constant__ CUtensorMap depth_map,
                        const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
                        lbp_images_t geom, const lbp_roi_t* __restrict__ rois, int32_t n_rois,
                        DepthWindow win, uint16_t* __restrict__ desc, int64_t desc_stride,
-                       int32_t* __restrict__ roi_status, int32_t lut_off) {
+                       int32_t* __restrict__ roi_status, int32_t lut_off,
+                       const __grid_constant__ lbp_gather_dst_t gd,
+                       const int32_t* __restrict__ glabels) {
+    static_assert(!GATHER || !FRAME, "the fused gather uses the crop-stack epilogue");
     using namespace l59;
     using L = Layout<FRAME>;
     constexpr bool FP16WIN = WINM != 0;
@@ -376,6 +384,11 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 reinterpret_cast<uint32_t*>(smem + (hist0 - stages0)), kHistBytes / 4,
                 smem + kPlainLutOff, 0, gtid, GroupSync{bar_id});
             named_barrier_sync(bar_id, kGroupThreads);
+            if constexpr (GATHER) {  // forward the row written to the local scratch
+                gather_row_from_global<kGroupThreads>(gd, n, desc + (int64_t)n * desc_stride,
+                                                      kDescBytes / 2, gtid);
+                if (gtid == 0) gather_label(gd, n, glabels);
+            }
             continue;
         }
         const uint32_t st = stages0 + s * kStageBytes;
@@ -597,13 +610,23 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
                 put(g, bin, cx, c);
             }
-            fence_proxy_async_smem();                   // staging writes -> async proxy
-            named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-            if (gtid == 0) bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
+            if constexpr (GATHER) {
+                // every thread forwards 16-B chunks of the staged row to every destination
+                // (the staging is rewritten only after the next crop's barrier A, which every
+                // thread reaches after its loads here)
+                named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
+                gather_row_from_smem<kGroupThreads>(gd, n, staging, kDescBytes / 16, gtid);
+                if (gtid == 0) gather_label(gd, n, glabels);
+            } else {
+                fence_proxy_async_smem();                   // staging writes -> async proxy
+                named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
+                if (gtid == 0) bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
+            }
         }
         pending = n;
     }
     if (gtid == 0 && pending >= 0) bulk_wait_all();
+    if constexpr (GATHER) __threadfence_system();  // before the caller's cross-rank barrier
 }
 
 // Offset of the lane-banked LUT in the dynamic shared memory: the first offset >= lut_min
@@ -632,7 +655,10 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
                                           int32_t n_rois, const DepthWindow& win, uint16_t* desc,
                                           int64_t desc_stride, int32_t* roi_status, int sms,
                                           cudaStream_t stream, bool depth_source = false,
-                                          bool frame = false) {
+                                          bool frame = false,
+                                          const lbp_gather_dst_t* gather = nullptr,
+                                          const int32_t* glabels = nullptr) {
+    if (gather && (frame || depth_source)) return cudaErrorNotSupported;
     CUtensorMap gm, dm;
     if (!depth_source &&
         !encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
@@ -662,7 +688,14 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
                              : lbp_hist_lane59_kernel<true, false, 0, F>;
         return lbp_hist_lane59_kernel<false, false, 0, F>;
     };
-    auto kern = frame ? pick(std::true_type{}) : pick(std::false_type{});
+    auto pick_gather = [&]() {
+        if (depth)
+            return centred   ? lbp_hist_lane59_kernel<true, false, 2, false, true>
+                   : fp16win ? lbp_hist_lane59_kernel<true, false, 1, false, true>
+                             : lbp_hist_lane59_kernel<true, false, 0, false, true>;
+        return lbp_hist_lane59_kernel<false, false, 0, false, true>;
+    };
+    auto kern = gather ? pick_gather() : frame ? pick(std::true_type{}) : pick(std::false_type{});
     int lut_off = 0, smem = 0;
     if (!lut_placement(frame ? l59::Layout<true>::kLutMin : l59::Layout<false>::kLutMin,
                        l59::Layout<false>::kTailBytes, &lut_off, &smem))
@@ -670,8 +703,11 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(sms, n_rois));
+    lbp_gather_dst_t gd{};
+    if (gather) gd = *gather;
     kern<<<grid, l59::kThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win,
-                                                 desc, desc_stride, roi_status, lut_off);
+                                                 desc, desc_stride, roi_status, lut_off, gd,
+                                                 glabels);
     return cudaGetLastError();
 }
 

@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "desc_pack.cuh"
+#include "gather.cuh"
 #include "lbp_hist_generic.cuh"
 #include "tma_util.cuh"
 #include "lbp_hist_lane59.cuh"
@@ -252,6 +253,53 @@ int32_t lbp_recognize(const uint8_t* grey, const uint16_t* depth, lbp_images_t g
     if (st != LBP_OK) return st;
     return svm_score(desc, n_rois, dim, W, bias, n_classes, prepared, prepared_bytes, scores,
                      labels, top_score, reject_threshold, stream_);
+}
+
+int32_t lbp_extract_gather(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                           const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                           int32_t cells_x, int32_t cells_y, int32_t bins,
+                           const int32_t* labels, lbp_gather_dst_t dst, uint16_t* scratch,
+                           int32_t* roi_status, lbp_stream_t stream_) {
+    if (n_rois < 0) return LBP_E_ARG;
+    const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
+    if (dim < 0) return dim;
+    if (dmin > dmax) return LBP_E_ARG;
+    if (dst.mode == LBP_GATHER_MULTIMEM) {
+        if (dst.n_dst != 1) return LBP_E_ARG;
+    } else if (dst.mode == LBP_GATHER_PEERS) {
+        if (dst.n_dst < 1 || dst.n_dst > LBP_GATHER_MAX_DST) return LBP_E_ARG;
+    } else {
+        return LBP_E_ARG;
+    }
+    for (int r = 0; r < dst.n_dst; ++r)
+        if (dst.base[r] == 0 || (dst.base[r] & 15)) return LBP_E_ARG;
+    if (dst.desc_offset < 0 || (dst.desc_offset & 15) || dst.desc_pitch < dim ||
+        (dst.desc_pitch & 7) || dst.row_base < 0)
+        return LBP_E_ARG;
+    if (dst.labels_offset >= 0 && (dst.labels_offset & 3)) return LBP_E_ARG;
+    if (n_rois == 0) return LBP_OK;
+    if (!grey || !rois || !scratch) return LBP_E_ARG;
+    int32_t st = check_geometry(geom, true, depth != nullptr);
+    if (st != LBP_OK) return st;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const DepthWindow win = make_window(dmin, dmax);
+    // fused: the headline TMA kernel writes every row from its epilogue (crop stacks; frames
+    // wider than a crop, small batches and other geometries take extraction + forwarding)
+    const bool frame = geom.width >= l59::Layout<true>::kGreyW;
+    if (n_rois >= num_sms() && bins == 59 && !frame &&
+        fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, scratch)) {
+        const cudaError_t e = launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win, scratch,
+                                                     dim, roi_status, num_sms(), stream, false,
+                                                     false, &dst, labels);
+        if (e != cudaErrorNotSupported) return launch_status(e);
+    }
+    st = lbp_extract_source(grey, depth, geom, rois, n_rois, dmin, dmax, cells_x, cells_y, bins,
+                            LBP_SRC_GREY, scratch, roi_status, stream_);
+    if (st != LBP_OK) return st;
+    const int grid = (int)std::min<int64_t>(((int64_t)n_rois * 32 + 255) / 256,
+                                            (int64_t)num_sms() * 8);
+    lbp_gather_forward_kernel<<<grid, 256, 0, stream>>>(scratch, n_rois, dim, labels, dst);
+    return launch_status(cudaGetLastError());
 }
 
 int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,

@@ -34,6 +34,16 @@ class lbp_images_t(ctypes.Structure):
                 ("grey_img_stride", ctypes.c_int64), ("depth_img_stride", ctypes.c_int64)]
 
 
+LBP_GATHER_MULTIMEM, LBP_GATHER_PEERS, LBP_GATHER_MAX_DST = 1, 2, 8
+
+
+class lbp_gather_dst_t(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("n_dst", ctypes.c_int32),
+                ("base", ctypes.c_uint64 * LBP_GATHER_MAX_DST),
+                ("desc_offset", ctypes.c_int64), ("desc_pitch", ctypes.c_int64),
+                ("labels_offset", ctypes.c_int64), ("row_base", ctypes.c_int64)]
+
+
 _lib = None
 
 
@@ -73,6 +83,9 @@ def lib():
         L.lbp_desc_pack_u8.restype = i32
         L.lbp_desc_unpack_u8.argtypes = [P, i64, i32, i64, P, P, i32, i32, P, P]
         L.lbp_desc_unpack_u8.restype = i32
+        L.lbp_extract_gather.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, P,
+                                         lbp_gather_dst_t, P, P, P]
+        L.lbp_extract_gather.restype = i32
         L.svm_workspace_bytes.argtypes = [i32, i32]
         L.svm_workspace_bytes.restype = sz
         L.svm_prepare.argtypes = [P, i32, i32, P, sz, P]
@@ -237,6 +250,47 @@ def lbp_extract_source(grey: torch.Tensor | None, depth: torch.Tensor | None,
     if st != LBP_OK:
         raise LbpError(st, "lbp_extract_source")
     return out
+
+
+def gather_dst(mode: int, bases, desc_offset: int, desc_pitch: int, labels_offset: int,
+               row_base: int) -> lbp_gather_dst_t:
+    """lbp_gather_dst_t from plain integers (device addresses of the destinations)."""
+    bases = [int(b) for b in bases]
+    if not 1 <= len(bases) <= LBP_GATHER_MAX_DST:
+        raise ValueError("gather: 1..8 destinations")
+    arr = (ctypes.c_uint64 * LBP_GATHER_MAX_DST)(*(bases + [0] * (LBP_GATHER_MAX_DST - len(bases))))
+    return lbp_gather_dst_t(mode, len(bases), arr, desc_offset, desc_pitch, labels_offset,
+                            row_base)
+
+
+def lbp_extract_gather(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.Tensor,
+                       dmin: int, dmax: int, cells_x: int, cells_y: int, bins: int,
+                       labels: torch.Tensor | None, dst: lbp_gather_dst_t,
+                       scratch: torch.Tensor | None = None,
+                       roi_status: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Fused database build step (include/lbpfused.h lbp_extract_gather): descriptors of the
+    ROIs written by the extraction epilogue into every destination of `dst` (multicast or peer
+    addresses).  Returns the local scratch (rows of ROIs off the fast path live there)."""
+    _check_cuda(grey, depth, rois, labels, scratch, roi_status)
+    _require(grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16),
+             "grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)")
+    _require(rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5,
+             "rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5")
+    n = rois.shape[0]
+    dim = lbp_descriptor_dim(cells_x, cells_y, bins)
+    dev = grey.device
+    if scratch is None:
+        scratch = torch.empty((n, dim), dtype=torch.uint16, device=dev)
+    _out(scratch, torch.uint16, n * dim, "scratch", dev)
+    _out(labels, torch.int32, n, "labels", dev)
+    _out(roi_status, torch.int32, n, "roi_status", dev)
+    st = lib().lbp_extract_gather(_ptr(grey), _ptr(depth), images_geometry(grey, depth),
+                                  _ptr(rois), n, dmin, dmax, cells_x, cells_y, bins,
+                                  _ptr(labels), dst, _ptr(scratch), _ptr(roi_status),
+                                  _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_extract_gather")
+    return scratch
 
 
 def lbp_extract_resized(grey: torch.Tensor | None, depth: torch.Tensor | None,

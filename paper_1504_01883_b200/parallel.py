@@ -221,3 +221,91 @@ def build_database(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.T
     desc = lbpfused.lbp_fused_extract(grey, depth, rois, dmin, dmax, cells_x, cells_y, bins,
                                       stream=stream)
     return gather_database(desc, labels, n_total, group=group)
+
+
+# ---------------------------------------------------------------------------------------------
+# Fused database build (SURVEY §8e way 2): the extraction epilogue writes each descriptor row
+# ONCE into every rank's copy of the training matrix -- through an NVLS multicast address when
+# the platform gives one (multimem.st; the NVSwitch replicates), else as one store per rank
+# buffer mapped over NVLink (P2P).  No separate collective: one cross-rank barrier at the end.
+
+def fused_gather_layout(n_total: int, dim: int) -> dict:
+    """Byte layout of the gathered matrix inside one symmetric buffer: rows of `pitch` u16
+    (dim rounded up to a multiple of 8, so every row starts 16-B aligned), then int32 labels
+    at a 16-B aligned offset."""
+    if n_total < 0 or dim < 1:
+        raise ValueError("bad layout arguments")
+    pitch = -(-dim // 8) * 8
+    labels_offset = -(-(n_total * pitch * 2) // 16) * 16
+    return {"desc_offset": 0, "pitch": pitch, "labels_offset": labels_offset,
+            "bytes": labels_offset + 4 * n_total}
+
+
+def fused_gather_plan(n_total: int, rank: int, world: int, dim: int, multicast_ptr: int,
+                      buffer_ptrs) -> dict:
+    """lbp_extract_gather destinations of `rank`: MULTIMEM with the multicast address when it
+    is non-zero, else PEERS with every rank's buffer address as mapped on this device."""
+    from .lbpfused import LBP_GATHER_MAX_DST, LBP_GATHER_MULTIMEM, LBP_GATHER_PEERS
+    lay = fused_gather_layout(n_total, dim)
+    first, count = shard_range(n_total, rank, world)
+    if multicast_ptr:
+        mode, bases = LBP_GATHER_MULTIMEM, [int(multicast_ptr)]
+    else:
+        if len(buffer_ptrs) != world or world > LBP_GATHER_MAX_DST:
+            raise ValueError("peer gather needs one mapped buffer per rank (world <= 8)")
+        mode, bases = LBP_GATHER_PEERS, [int(p) for p in buffer_ptrs]
+    return {"mode": mode, "bases": bases, "desc_offset": lay["desc_offset"],
+            "pitch": lay["pitch"], "labels_offset": lay["labels_offset"], "row_base": first,
+            "count": count, "bytes": lay["bytes"]}
+
+
+class FusedDatabase:
+    """The training matrix [n_total][dim] u16 + labels [n_total] int32 in symmetric memory
+    (torch.distributed._symmetric_memory: one allocation per rank, mapped on every peer, plus
+    the multicast mapping when NVLS is available).  `build()` extracts this rank's shard with
+    lbp_extract_gather straight into every rank's copy, then runs the symmetric-memory barrier;
+    after it every rank holds the whole database (global crop order)."""
+
+    def __init__(self, n_total: int, dim: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.n_total, self.dim = n_total, dim
+        lay = fused_gather_layout(n_total, dim)
+        self.buf = symm_mem.empty(lay["bytes"], dtype=torch.uint8, device=device)
+        self.handle = symm_mem.rendezvous(self.buf, self.group)
+        ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        self.plan = fused_gather_plan(n_total, self.rank, self.world, dim,
+                                      int(self.handle.multicast_ptr), ptrs)
+        self.scratch = None
+
+    @property
+    def mode(self) -> str:
+        from .lbpfused import LBP_GATHER_MULTIMEM
+        return "multimem" if self.plan["mode"] == LBP_GATHER_MULTIMEM else "peers"
+
+    def views(self):
+        p = self.plan
+        rows = self.buf[:self.n_total * p["pitch"] * 2].view(torch.uint16).view(
+            self.n_total, p["pitch"])
+        lab = self.buf[p["labels_offset"]:p["labels_offset"] + 4 * self.n_total].view(torch.int32)
+        return rows[:, :self.dim], lab
+
+    def build(self, grey, depth, rois, labels, dmin: int, dmax: int, cells_x: int, cells_y: int,
+              bins: int, stream=None):
+        from . import lbpfused
+        p = self.plan
+        if rois.shape[0] != p["count"]:
+            raise ValueError(f"rank {self.rank}: {rois.shape[0]} ROIs, shard has {p['count']}")
+        dst = lbpfused.gather_dst(p["mode"], p["bases"], p["desc_offset"], p["pitch"],
+                                  p["labels_offset"] if labels is not None else -1, p["row_base"])
+        if self.scratch is None or self.scratch.shape[0] < p["count"]:
+            self.scratch = torch.empty((max(p["count"], 1), self.dim), dtype=torch.uint16,
+                                       device=grey.device)
+        s = stream if stream is not None else torch.cuda.current_stream(grey.device)
+        lbpfused.lbp_extract_gather(grey, depth, rois, dmin, dmax, cells_x, cells_y, bins,
+                                    labels, dst, scratch=self.scratch[:p["count"]], stream=s)
+        with torch.cuda.stream(s):
+            self.handle.barrier(channel=0)  # every rank's rows have landed everywhere
+        return self.views()

@@ -186,3 +186,35 @@ def test_desc_pack_host_errors(L):
     assert L.lbp_desc_unpack_u8(fake, 4, 8, 0, None, fake, 1, 8, fake, None) == lb.LBP_E_ARG
     assert L.lbp_desc_unpack_u8(fake, 4, 8, 0, fake, fake, -1, 8, fake, None) == lb.LBP_E_ARG
     assert L.lbp_desc_unpack_u8(fake, 0, 8, 0, fake, fake, 1, 8, fake, None) == lb.LBP_OK
+
+
+def test_extract_gather_argument_errors(L):
+    """lbp_extract_gather (the fused database build): destination descriptor checks, all before
+    any CUDA call."""
+    from paper_1504_01883_b200 import lbpfused as lb
+    P = ctypes.c_void_p
+    dummy = P(0x1000)
+    g = _geom(lb)
+    base = 0x10000
+
+    def call(mode=lb.LBP_GATHER_PEERS, bases=(base,), off=0, pitch=64, lab=-1, row0=0, n=1,
+             bins=59, scratch=dummy, grey=dummy):
+        dst = lb.gather_dst(mode, list(bases), off, pitch, lab, row0)
+        return L.lbp_extract_gather(grey, None, g, dummy, n, 0, 10, 1, 1, bins, None, dst,
+                                    scratch, None, None)
+    assert call(n=0) == lb.LBP_OK
+    assert call(mode=0) == lb.LBP_E_ARG
+    assert call(mode=lb.LBP_GATHER_MULTIMEM, bases=(base, base)) == lb.LBP_E_ARG
+    assert call(bases=(base + 4,)) == lb.LBP_E_ARG
+    assert call(bases=(0,)) == lb.LBP_E_ARG
+    assert call(off=8) == lb.LBP_E_ARG
+    assert call(pitch=56) == lb.LBP_E_ARG   # < dim 59
+    assert call(pitch=60) == lb.LBP_E_ARG   # not a multiple of 8
+    assert call(lab=2) == lb.LBP_E_ARG
+    assert call(row0=-1) == lb.LBP_E_ARG
+    assert call(bins=60) == lb.LBP_E_ARG
+    assert call(n=-1) == lb.LBP_E_ARG
+    assert call(scratch=None) == lb.LBP_E_ARG
+    assert call(grey=None) == lb.LBP_E_ARG
+    with pytest.raises(ValueError):
+        lb.gather_dst(lb.LBP_GATHER_PEERS, [base] * 9, 0, 64, -1, 0)

@@ -175,3 +175,49 @@ def test_gather_database_compact_gloo(tmp_path, world, n_total, cap):
     for r in range(world):
         assert np.array_equal(np.load(tmp_path / f"desc{r}.npy").view(np.uint16), ref)
         assert np.array_equal(np.load(tmp_path / f"lab{r}.npy"), np.arange(n_total) % 4)
+
+
+# ---- fused database build (SURVEY §8e way 2): the host plan, checked by emulating the
+# kernel's stores (every ROI row to every destination at the planned offsets) in numpy
+def test_fused_gather_layout():
+    from paper_1504_01883_b200.parallel import fused_gather_layout
+    lay = fused_gather_layout(10, 3776)
+    assert lay["pitch"] == 3776 and lay["labels_offset"] == 10 * 3776 * 2
+    lay = fused_gather_layout(3, 59)
+    assert lay["pitch"] == 64 and lay["labels_offset"] % 16 == 0
+    assert lay["bytes"] == lay["labels_offset"] + 12
+    with pytest.raises(ValueError):
+        fused_gather_layout(3, 0)
+
+
+@pytest.mark.parametrize("world,n_total,dim,multicast", [(2, 11, 236, False), (3, 10, 59, False),
+                                                        (4, 9, 3776, True), (1, 5, 944, False)])
+def test_fused_gather_plan_emulated(world, n_total, dim, multicast):
+    """Every rank's plan, applied as the kernel applies it, yields the full database in every
+    rank's buffer (uneven shards, padded pitch, multicast = one address for all)."""
+    from paper_1504_01883_b200 import lbpfused
+    from paper_1504_01883_b200.parallel import fused_gather_plan
+    rng = np.random.default_rng(world * 100 + n_total)
+    db = rng.integers(0, 300, (n_total, dim)).astype(np.uint16)
+    labels = rng.integers(0, 50, n_total).astype(np.int32)
+    plans = [fused_gather_plan(n_total, r, world, dim, 0xABC0 if multicast else 0,
+                               [0x1000 * (r2 + 1) for r2 in range(world)]) for r in range(world)]
+    size = plans[0]["bytes"]
+    bufs = {0x1000 * (r + 1): np.full(size, 0xEE, np.uint8) for r in range(world)}
+    for r, p in enumerate(plans):
+        assert p["mode"] == (lbpfused.LBP_GATHER_MULTIMEM if multicast else lbpfused.LBP_GATHER_PEERS)
+        targets = list(bufs) if multicast else p["bases"]  # multicast reaches every rank
+        for n in range(p["count"]):
+            row = np.zeros(p["pitch"], np.uint16)
+            row[:dim] = db[p["row_base"] + n]
+            off = p["desc_offset"] + (p["row_base"] + n) * p["pitch"] * 2
+            lab_off = p["labels_offset"] + 4 * (p["row_base"] + n)
+            for t in targets:
+                bufs[t][off:off + 2 * p["pitch"]] = row.view(np.uint8)
+                bufs[t][lab_off:lab_off + 4] = labels[p["row_base"] + n:p["row_base"] + n + 1].view(np.uint8)
+    assert sum(p["count"] for p in plans) == n_total
+    for b in bufs.values():
+        rows = b[:n_total * plans[0]["pitch"] * 2].view(np.uint16).reshape(n_total, -1)
+        assert np.array_equal(rows[:, :dim], db) and not rows[:, dim:].any()
+        lab_off = plans[0]["labels_offset"]
+        assert np.array_equal(b[lab_off:lab_off + 4 * n_total].view(np.int32), labels)

@@ -18,22 +18,35 @@ def driver_probe():
     err, v = d.cuDeviceGetAttribute(
         d.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev)
     out["attr_multicast_supported"] = int(v)
-    prop = d.CUmulticastObjectProp()
-    prop.numDevices = 1
-    prop.size = 2 << 20
-    prop.handleTypes = d.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
-    err, gran = d.cuMulticastGetGranularity(
-        prop, d.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED)
-    out["granularity"] = [str(err), int(gran) if err == d.CUresult.CUDA_SUCCESS else None]
-    if err != d.CUresult.CUDA_SUCCESS:
-        return out
-    prop.size = max(int(gran), 2 << 20)
-    err, mc = d.cuMulticastCreate(prop)
-    out["create"] = str(err)
-    if err != d.CUresult.CUDA_SUCCESS:
-        return out
-    (err,) = d.cuMulticastAddDevice(mc, dev)
-    out["add_device"] = str(err)
+    err, ctx = d.cuDevicePrimaryCtxRetain(dev)
+    d.cuCtxSetCurrent(ctx)
+    for attr in ("CU_DEVICE_ATTRIBUTE_HANDLE_TYPE_FABRIC_SUPPORTED",
+                 "CU_DEVICE_ATTRIBUTE_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR_SUPPORTED"):
+        a = getattr(d.CUdevice_attribute, attr, None)
+        if a is not None:
+            out[attr] = int(d.cuDeviceGetAttribute(a, dev)[1])
+    H = d.CUmemAllocationHandleType
+    for name, ht in (("none", 0), ("posix_fd", H.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+                     ("fabric", getattr(H, "CU_MEM_HANDLE_TYPE_FABRIC", None))):
+        if ht is None:
+            continue
+        r = {}
+        prop = d.CUmulticastObjectProp()
+        prop.numDevices = 1
+        prop.size = 2 << 20
+        prop.handleTypes = ht
+        prop.flags = 0
+        err, gran = d.cuMulticastGetGranularity(
+            prop, d.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED)
+        r["granularity"] = [str(err), int(gran) if err == d.CUresult.CUDA_SUCCESS else None]
+        if err == d.CUresult.CUDA_SUCCESS:
+            prop.size = max(int(gran), 2 << 20)
+            err, mc = d.cuMulticastCreate(prop)
+            r["create"] = str(err)
+            if err == d.CUresult.CUDA_SUCCESS:
+                (err,) = d.cuMulticastAddDevice(mc, dev)
+                r["add_device"] = str(err)
+        out[name] = r
     return out
 
 
@@ -50,7 +63,9 @@ def symm_probe():
         t = symm_mem.empty(1 << 22, dtype=torch.uint8, device=dev)
         h = symm_mem.rendezvous(t, dist.group.WORLD)
         out["world"] = h.world_size
-        out["has_multicast_support"] = bool(h.has_multicast_support())
+        from torch._C._distributed_c10d import _SymmetricMemory
+        out["has_multicast_support"] = bool(_SymmetricMemory.has_multicast_support(
+            torch._C._autograd.DeviceType.CUDA, 0)) if hasattr(torch._C, "_autograd") else None
         out["multicast_ptr"] = int(h.multicast_ptr)
         out["buffer_ptr0"] = int(h.buffer_ptrs[0])
     except Exception as e:  # noqa: BLE001
