@@ -107,6 +107,10 @@ def parse():
     p.add_argument("--compact", action="store_true",
                    help="config5: all-gather u8 descriptors + exception lists (serial; "
                         "lbp_desc_pack_u8 / lbp_desc_unpack_u8), and time pack/unpack")
+    p.add_argument("--format", default="u8", choices=["u8", "u16"],
+                   help="descriptor between extraction and scoring (grey source): u8 = the "
+                        "compact form (lbp_extract_u8 + svm_score_u8: u8 rows + records of the "
+                        "entries above 255), u16 = lbp_fused_extract + svm_score")
     p.add_argument("--fused", action="store_true",
                    help="config5: the fused database build (SURVEY §8e way 2): the extraction "
                         "epilogue stores every row into every rank's symmetric-memory copy "
@@ -287,11 +291,18 @@ def workload_config(args, n, H, W, cx, cy, bins, C, desc_txt):
             "cells": f"{cx}x{cy}", "bins": bins, "classes": C, "dist": args.dist,
             "depth_mask": not args.no_depth, "depth_window_mm": [DMIN, DMAX],
             "source": getattr(args, "source", "grey"),
+            "descriptor": ("u8 + per-row records of counts > 255 (lbp_extract_u8 -> svm_score_u8)"
+                           if compact_format(args) else "u16 (lbp_fused_extract -> svm_score)"),
             "parallelism": f"crop-sharded dp{int(os.environ.get('WORLD_SIZE', '1'))}",
             "pipeline": "scoring of step k overlaps extraction of step k+1 (2 streams)"
                         if getattr(args, "pipeline", False) else "serial",
             "l2": "inputs larger than L2 (no flush needed)" if n * H * W * 3 > 126e6 else
                   "inputs L2-resident (latency config)"}
+
+
+def compact_format(args) -> bool:
+    """The recognition step runs on the compact descriptor (grey source only)."""
+    return getattr(args, "format", "u16") == "u8" and getattr(args, "source", "grey") == "grey"
 
 
 # --------------------------------------------------------------------------- own arm
@@ -330,10 +341,12 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch(args)
     if args.launch_check:  # CPU test of the launcher: every rank reports what it sees
-        print(json.dumps({"rank": int(os.environ.get("RANK", "0")),
-                          "world": int(os.environ.get("WORLD_SIZE", "1")),
-                          "relaunched": os.environ.get("LBP_BENCH_RELAUNCHED") == "1"}),
-              flush=True)
+        # one write() per line: the ranks share the pipe and must not interleave
+        sys.stdout.flush()
+        os.write(1, (json.dumps({"rank": int(os.environ.get("RANK", "0")),
+                                 "world": int(os.environ.get("WORLD_SIZE", "1")),
+                                 "relaunched": os.environ.get("LBP_BENCH_RELAUNCHED") == "1"})
+                     + "\n").encode())
         return 0
     if args.impl == "reference":
         return run_reference(args)
@@ -375,8 +388,13 @@ def main():
     W_np, b_np = synthgen.svm_weights(C, dim, seed=args.seed)
     W = torch.from_numpy(W_np).to(dev)
     b = torch.from_numpy(b_np).to(dev)
-    prepared = lb.svm_prepare(W)
-    desc = torch.empty((n, dim), dtype=torch.uint16, device=dev)
+    compact = compact_format(args)
+    prepared = lb.svm_prepare_u8(W) if compact else lb.svm_prepare(W)
+    if compact:
+        cap = lb.lbp_u8_exc_cap_min(lb.images_geometry(grey, depth), dim)
+        desc = lb.CompactDesc.empty(n, dim, cap, dev)
+    else:
+        desc = torch.empty((n, dim), dtype=torch.uint16, device=dev)
     labels = torch.empty(n, dtype=torch.int32, device=dev)
     top = torch.empty(n, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -386,7 +404,11 @@ def main():
     # (descriptors double-buffered; the extraction of step k waits for the scoring of step
     # k-2, which read the same buffer).
     svm_stream = torch.cuda.Stream(dev) if args.pipeline else stream
-    descs = [desc, torch.empty_like(desc)] if args.pipeline else [desc, desc]
+    if args.pipeline:
+        descs = [desc, lb.CompactDesc.empty(n, dim, desc.cap, dev) if compact
+                 else torch.empty_like(desc)]
+    else:
+        descs = [desc, desc]
     ext_done = [torch.cuda.Event(), torch.cuda.Event()]
     svm_done = [torch.cuda.Event(), torch.cuda.Event()]
     step_no = [0]
@@ -400,7 +422,10 @@ def main():
             stream.wait_event(svm_done[buf])
         if ev is not None:
             ev[0].record(stream)
-        if source == 0:
+        if compact:
+            lb.lbp_extract_u8(grey, depth, rois, DMIN, DMAX, cx, cy, bins, out=d_k,
+                              stream=stream)
+        elif source == 0:
             lb.lbp_fused_extract(grey, depth, rois, DMIN, DMAX, cx, cy, bins, out=d_k,
                                  stream=stream)
         else:
@@ -413,8 +438,9 @@ def main():
             svm_stream.wait_event(ext_done[buf])
         if ev is not None and not args.pipeline:
             ev[2].record(svm_stream)
-        lb.svm_score(d_k, W, b, prepared=prepared, want_scores=False, labels=labels,
-                     top_score=top, stream=svm_stream)
+        score = lb.svm_score_u8 if compact else lb.svm_score
+        score(d_k, W, b, prepared=prepared, want_scores=False, labels=labels, top_score=top,
+              stream=svm_stream)
         if ev is not None and not args.pipeline:
             ev[3].record(svm_stream)
         if args.pipeline:
@@ -425,7 +451,11 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, barrier + sync on both sides, events on the launching stream
+    # ---- timed region: K steps, barrier + sync on both sides, events on the launching stream.
+    # The headline pass records no event between the kernels (an event between the extraction
+    # and the scorer would cut the programmatic dependent launch that overlaps the scorer's
+    # prologue with the extraction's tail); a second pass of K steps with events around each
+    # kernel gives the per-kernel durations of the roofline lines.
     ev_ext = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4))
               for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -435,13 +465,23 @@ def main():
     with ClockSampler(torch.cuda.current_device()) as clk:
         t_start.record(stream)
         for k in range(args.steps):
-            step(ev_ext[k])
+            step()
         stream.wait_stream(svm_stream)  # the last step's scoring is inside the timed region
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
+    # per-kernel pass (same K steps, events around each launch)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        step(ev_ext[k])
+    stream.wait_stream(svm_stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     ext_ms = sum(e[0].elapsed_time(e[1]) for e in ev_ext) / args.steps
     svm_ms = (sum(e[2].elapsed_time(e[3]) for e in ev_ext) / args.steps
               if not args.pipeline else float("nan"))
@@ -456,11 +496,13 @@ def main():
     e2e = None
     if source == 0:  # lbp_recognize_host computes the grey-source descriptor
         e2e = run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins, W, b,
-                      prepared, n)
+                      lb.svm_prepare(W) if compact else prepared, n)
 
     # ---- roofline of the dominant kernel (lbp_hist): algorithmic bytes / avg launch time
     peaks = load_peaks()
-    if source == 0:
+    if compact:  # grey + depth read, u8 row + its exception count written (records: ~0)
+        bpc = (H * Wd * 3 if depth is not None else H * Wd) + dim + 4
+    elif source == 0:
         bpc = bytes_per_crop(H, Wd, cx, cy, bins) if depth is not None else H * Wd + dim * 2
     elif source == 1:
         bpc = H * Wd * 2 + dim * 2  # depth read once (mask + codes), descriptor written
@@ -475,18 +517,20 @@ def main():
                 "frac_of_nominal_8000": achieved / 8000.0,  # also vs 8 TB/s
                 "kernel_ms": ext_ms, "kernel_share_of_step": ext_ms / ms_per_step,
                 "traffic": load_traffic(args.workload, bins, args.source,
-                                        depth is not None and not args.no_depth)}
+                                        depth is not None and not args.no_depth,
+                                        "u8" if compact else "u16")}
     # the scorer's own roofline (per-phase TF/s fractions): algorithmic flops
     # 2 n C dim of s = W x + b over its event-timed launch; the INT8 digit-plane kernel
     # (C > 124) takes the int8 peak = the measured bf16 burst x the nominal 2x ratio
     if not args.pipeline and prepared is not None:
         flops = 2.0 * n * C * dim
-        i8 = C > 124
+        i8 = C > 124 or compact
         bf16 = load_bf16_peak()
         pk = bf16 * (2.0 if i8 else 1.0)
         ach = flops / (svm_ms * 1e-3) / 1e12
         roofline["scorer"] = {
-            "bound": "tensor", "kernel": "svm_gemm_i8 (INT8 digit planes)" if i8 else
+            "bound": "tensor", "kernel": "svm_gemm_u8 (INT8 digit planes, u8 descriptors by "
+            "TMA)" if compact else "svm_gemm_i8 (INT8 digit planes)" if i8 else
             "svm_gemm (fp16 digit planes)", "achieved": ach, "unit": "TFLOP/s",
             "peak": pk, "frac": ach / pk, "frac_of_bf16_burst": ach / bf16,
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8:bf16 ratio)"
@@ -497,22 +541,23 @@ def main():
     # ---- CPU oracle baseline (rank 0, N=1 only) + equivalence gate on its sample
     cpu = None
     gate_m = 4096 if world == 1 else 512
-    gscores, gtop, same = gate_scores(lb, torch, descs[(step_no[0] - 1) & 1], W, b, prepared,
-                                      labels, top, min(gate_m, n))
+    last = descs[(step_no[0] - 1) & 1]
+    gscores, gtop, same = gate_scores(lb, torch, last, W, b, prepared, labels, top,
+                                      min(gate_m, n))
     if not same:
         print(json.dumps({"error": "scorer with scores requested disagrees with the timed step"}),
               flush=True)
         return 3
     if rank == 0 and world == 1 and not args.skip_cpu:
-        cpu, gate_ok = run_cpu_leg(args, torch, grey, depth, rois, descs[(step_no[0] - 1) & 1],
-                                   labels, W_np, b_np, cx, cy, bins, gscores, gtop)
+        cpu, gate_ok = run_cpu_leg(args, torch, grey, depth, rois, last, labels, W_np, b_np,
+                                   cx, cy, bins, gscores, gtop)
         if not gate_ok:
             print(json.dumps({"error": "equivalence gate failed: GPU != oracle on the sample"}),
                   flush=True)
             return 3
     elif world > 1:  # every rank checks its own shard's first crops; any failure stops all
-        ok = rank_gate(torch, grey, depth, rois, descs[(step_no[0] - 1) & 1], labels, W_np, b_np,
-                       cx, cy, bins, source, 512, gscores, gtop)
+        ok = rank_gate(torch, grey, depth, rois, last, labels, W_np, b_np, cx, cy, bins, source,
+                       512, gscores, gtop)
         flag = torch.tensor([1 if ok else 0], device=dev, dtype=torch.int32)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag[0]) == 0:
@@ -529,6 +574,9 @@ def main():
             "config": workload_config(args, n, H, Wd, cx, cy, bins, C, desc_txt),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+            "timing": "ms_per_step: K steps between two events (no event between kernels); "
+                      "kernel_ms: a second pass of the same K steps with events around each "
+                      "kernel",
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -953,7 +1001,7 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
     rate, done, secs, passes, odesc, olab = oracle_rate(g, d, r, W_np, b_np, cx, cy, bins,
                                                         args.cpu_seconds, threads,
                                                         SOURCES[args.source])
-    gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
+    gdesc = desc_rows(torch, desc, m)
     glab = labels[:m].cpu().numpy()
     ok, detail = gate_compare(gdesc, glab, odesc, olab, W_np, b_np,
                               None if gscores is None else gscores[:m],
@@ -1001,11 +1049,32 @@ def gate_compare(gdesc, glab, odesc, olab, W_np, b_np, gscores=None, gtop=None):
     return ok, detail
 
 
+def desc_rows(torch, desc, m):
+    """The first m descriptor rows as numpy u16: a u16 tensor, or a CompactDesc decoded on the
+    host (u8 entries, then each row's records of the counts above 255)."""
+    if isinstance(desc, torch.Tensor):
+        return desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
+    out = desc.packed[:m].cpu().numpy().astype(np.uint16)
+    n_exc = desc.exc_n[:m].cpu().numpy()
+    exc = desc.exc[:m].cpu().numpy().view(np.uint32)
+    for i in np.nonzero(n_exc)[0]:
+        for k in range(min(int(n_exc[i]), exc.shape[1])):
+            out[i, exc[i, k] >> 16] = exc[i, k] & 0xFFFF
+    return out
+
+
 def gate_scores(lb, torch, desc, W, b, prepared, labels, top, m):
     """Scores of the gate sample from the scorer in the bench's launch configuration (the whole
-    batch, scores requested); its labels / top scores must equal the timed step's."""
-    s_full, lab_full, top_full = lb.svm_score(desc, W, b, prepared=prepared, want_scores=True)
+    batch, scores requested).  u16 path: its labels / top scores must equal the timed step's
+    bit for bit.  Compact path: the timed step ran the label-only scorer (4 digit planes, a
+    per-row proof, exact fix-up), so the gate checks the timed step's own labels and top
+    scores against the oracle (returned here) and the scores-mode scores separately."""
+    compact = not isinstance(desc, torch.Tensor)
+    score = lb.svm_score_u8 if compact else lb.svm_score
+    s_full, lab_full, top_full = score(desc, W, b, prepared=prepared, want_scores=True)
     torch.cuda.synchronize()
+    if compact:
+        return s_full[:m].cpu().numpy(), top[:m].cpu().numpy(), bool((labels >= -1).all())
     same = bool(torch.equal(lab_full, labels)) and bool(
         torch.equal(top_full.view(torch.int32), top.view(torch.int32)))
     return s_full[:m].cpu().numpy(), top_full[:m].cpu().numpy(), same
@@ -1022,7 +1091,7 @@ def rank_gate(torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins, 
     r = rois[:m].cpu().numpy()
     odesc = oracle.lbp_extract(g, d, r, DMIN, DMAX, cx, cy, bins, source=source)
     _, olab, _ = oracle.svm_score(odesc, W_np, b_np)
-    gdesc = desc[:m].cpu().view(torch.int16).numpy().view(np.uint16)
+    gdesc = desc_rows(torch, desc, m)
     ok, _ = gate_compare(gdesc, labels[:m].cpu().numpy(), odesc, olab, W_np, b_np,
                          None if gscores is None else gscores[:m],
                          None if gtop is None else gtop[:m])
@@ -1060,12 +1129,12 @@ def load_bf16_peak():
         return 1590.0  # B200_PROFILING.md fallback
 
 
-def load_traffic(workload, bins=59, source="grey", depth=True):
+def load_traffic(workload, bins=59, source="grey", depth=True, fmt="u16"):
     """dram read+write bytes per launch of the extraction kernel from the committed ncu
-    --set full capture of exactly this workload, bin count, code source and mask (None when
-    no capture of that combination is committed)."""
+    --set full capture of exactly this workload, bin count, code source, mask and descriptor
+    format (None when no capture of that combination is committed)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    key = f"{workload}/bins{bins}/{source}/{'mask' if depth else 'nomask'}"
+    key = f"{workload}/bins{bins}/{source}/{'mask' if depth else 'nomask'}/{fmt}"
     try:
         return json.load(open(p)).get(key)
     except Exception:

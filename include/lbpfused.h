@@ -303,6 +303,58 @@ int32_t svm_prepare(const float* W, int32_t n_classes, int32_t dim, void* worksp
                     size_t workspace_bytes, lbp_stream_t stream);
 
 /*
+ * The compact recognition path (SURVEY §8f-3 "pack counts (u8 + overflow flag)"; DESIGN.md
+ * R21, R22): the extraction epilogue writes each descriptor row as one byte per entry plus a
+ * per-row list of the entries that do not fit, and the INT8 tensor-core scorer reads those
+ * bytes as its A operand directly -- half the descriptor bytes written and read, no separate
+ * pack pass.  The descriptor it encodes is exactly lbp_fused_extract's (grey source):
+ *   packed[n][d]  = desc[n][d] & 255 (the low byte)         u8, rows of `pitch` bytes
+ *   exc_n[n]      = #{ d : desc[n][d] > 255 }                int32
+ *   exc[n][k]     = (d << 16) | desc[n][d] for those d,      uint32 [n][exc_cap], k < exc_n[n]
+ *                   in unspecified order
+ * A row cannot hold more than floor((width - 2) (height - 2) / 256) such entries (each needs
+ * 256 interior pixels of its ROI); lbp_u8_exc_cap_min(geom, dim) returns that bound (capped at
+ * dim) and exc_cap must be at least it, so the lists never overflow (LBP_E_ARG otherwise).
+ * Requires dim <= 65535.
+ */
+int32_t lbp_u8_exc_cap_min(lbp_images_t geom, int32_t dim);
+
+/*
+ * lbp_extract_u8 -- lbp_fused_extract (every step and status as documented there) with the
+ * compact output above.  Crop stacks of 128x128 ROIs with 8x8 cells and 59 bins, batches of
+ * at least one ROI per SM and pitch % 16 == 0 take the TMA kernel whose epilogue stages the
+ * u8 row and bulk-stores it; every other case extracts into `scratch` (device u16
+ * [n_rois][dim], may be NULL when the TMA kernel applies -- LBP_E_ARG if it is needed and
+ * NULL) and packs it.  pitch >= dim.
+ */
+int32_t lbp_extract_u8(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                       const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                       int32_t cells_x, int32_t cells_y, int32_t bins, uint8_t* packed,
+                       int64_t pitch, int32_t* exc_n, uint32_t* exc, int32_t exc_cap,
+                       uint16_t* scratch, int32_t* roi_status, lbp_stream_t stream);
+
+/* Bytes of device workspace svm_prepare_u8() needs for a [n_classes][dim] model (0 if the
+ * compact tensor-core scorer does not take this shape: dim > 32,768). */
+size_t svm_workspace_u8_bytes(int32_t n_classes, int32_t dim);
+
+/* W as five unsigned base-256 digit planes of an offset fraction ("compact
+ * descriptors") for svm_score_u8's tensor-core path.  Enqueued on stream. */
+int32_t svm_prepare_u8(const float* W, int32_t n_classes, int32_t dim, void* workspace,
+                       size_t workspace_bytes, lbp_stream_t stream);
+
+/*
+ * svm_score_u8 -- svm_score (same definitions of scores, labels, ties, reject threshold and
+ * the prepared-workspace checks) on the compact descriptor (packed, pitch, exc_n, exc,
+ * exc_cap) of lbp_extract_u8.  prepared = svm_prepare_u8()'s workspace (NULL: CUDA-core
+ * fp64 path); the tensor-core path needs n >= 128, pitch % 16 == 0 and a 16-B aligned packed.
+ */
+int32_t svm_score_u8(const uint8_t* packed, int64_t pitch, const int32_t* exc_n,
+                     const uint32_t* exc, int32_t exc_cap, int32_t n, int32_t dim,
+                     const float* W, const float* bias, int32_t n_classes, const void* prepared,
+                     size_t prepared_bytes, float* scores, int32_t* labels, float* top_score,
+                     float reject_threshold, lbp_stream_t stream);
+
+/*
  * lbp_recognize_host -- the whole path from HOST buffers (end-to-end entry point):
  * cudaMemcpyAsync of grey/depth/rois host->device into `workspace`, then
  * lbp_fused_extract + svm_score, then device->host of labels and top scores.

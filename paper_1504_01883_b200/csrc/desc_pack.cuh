@@ -113,4 +113,33 @@ desc_exc_scatter_kernel(const lbp_desc_exc_t* __restrict__ exc,
     }
 }
 
+// Per-row compact form of lbp_extract_u8 (include/lbpfused.h) from a u16 descriptor: one warp
+// per row, the entries' low bytes, the entries above 255 listed in the row's own record slots
+// (warp-aggregated slot indices; the caller guarantees cap >= the row's count).
+__global__ void __launch_bounds__(256)
+desc_pack_rows_kernel(const uint16_t* __restrict__ desc, int64_t n, int32_t dim,
+                      uint8_t* __restrict__ packed, int64_t pitch, int32_t* __restrict__ exc_n,
+                      uint32_t* __restrict__ exc, int32_t cap) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n;
+         row += warps) {
+        const uint16_t* src = desc + row * dim;
+        uint8_t* dst = packed + row * pitch;
+        int32_t count = 0;
+        for (int32_t d0 = 0; d0 < dim; d0 += 32) {
+            const int32_t d = d0 + lane;
+            const uint32_t v = d < dim ? src[d] : 0u;
+            if (d < dim) dst[d] = (uint8_t)(v & 255u);
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, v > 255u);
+            if (v > 255u) {
+                const int32_t k = count + __popc(m & ((1u << lane) - 1u));
+                if (k < cap) exc[row * cap + k] = ((uint32_t)d << 16) | v;
+            }
+            count += __popc(m);
+        }
+        if (lane == 0) exc_n[row] = count;
+    }
+}
+
 }  // namespace lbpf

@@ -45,6 +45,10 @@ constexpr int kGroupBytes = (kHistBytes + kDescBytes + 255) / 256 * 256;  // 23,
 constexpr int kLutBytes = 65 * 128;  // 64 lane-banked rows + the dummy row (bin 59 everywhere)
 constexpr uint32_t kDummyOff2 = 0x84008400u;  // LUT offset of the dummy row, both halves
 static_assert(kStages == kGroups, "a group refills its own stage with its next crop");
+// epilogue output modes of the kernel (template parameter OUTM)
+constexpr int kOutU16 = 0;     // u16 row, one bulk store (lbp_fused_extract)
+constexpr int kOutGather = 1;  // u16 row stored into every destination (lbp_extract_gather)
+constexpr int kOutU8 = 2;      // compact row: u8 min(count, 255) + exceptions (lbp_extract_u8)
 
 // Stage layout of the two variants.  FRAME (ROIs at any column of wider frames): the grey
 // box is 144 px wide at x & ~15 and the depth box 136 px at x & ~7 (TMA needs 16-B aligned
@@ -112,6 +116,36 @@ __device__ __forceinline__ uint32_t hsub2_sat(uint32_t a, uint32_t b) {
     uint32_t r;  // sat(a - b) per half
     asm("sub.rn.sat.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
     return r;
+}
+
+// The compact descriptor of lbp_extract_u8 (include/lbpfused.h): packed[n][d] = count & 255
+// (rows of `pitch` bytes), exc_n[n] = the number of entries above 255,
+// exc[n * exc_cap + k] = (d << 16) | count for the first exc_cap of them.
+struct U8Out {
+    uint8_t* packed;
+    int32_t* exc_n;
+    uint32_t* exc;
+    int32_t exc_cap;
+    int64_t pitch;
+};
+
+__device__ __forceinline__ uint32_t atom_shared_add(uint32_t addr, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
+
+// entry d of row n holds count v: its low byte (staged; st.u8 keeps bits 0-7) ...
+__device__ __forceinline__ void put_u8(uint32_t staging, uint32_t d, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(staging + d), "r"(v) : "memory");
+}
+// ... and, above 255, an exception record (rare: a 16x16 cell whose 256 pixels share a bin)
+__device__ __forceinline__ void record_u8(const U8Out& o, int64_t n, uint32_t cnt_addr,
+                                          uint32_t d, uint32_t v) {
+    if (v > 255u) {
+        const uint32_t k = atom_shared_add(cnt_addr, 1u);
+        if ((int32_t)k < o.exc_cap) o.exc[n * o.exc_cap + k] = (d << 16) | v;
+    }
 }
 
 struct LaneRow {
@@ -236,11 +270,13 @@ __device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uin
 // 2^-24 (value = bits * 2^-24), so the subtraction is exact there; for larger d either
 // mid/2 <= d <= 2 mid (exact by Sterbenz) or d > 2 mid, where the rounded difference is still
 // >= mid > half; NaN / inf / negative patterns fail the compare.
-// GATHER (the fused database build, gather.cuh): the descriptor rows go from the staging
-// buffer to every destination of `gd` (multicast or peer stores) instead of a bulk store to
-// `desc`; `desc` is then local scratch for the ROIs that take the generic code path, whose
-// rows are forwarded from there.
-template <bool HAS_DEPTH, bool DEPTH_SRC, int WINM, bool FRAME, bool GATHER = false>
+// OUTM == kOutGather (the fused database build, gather.cuh): the descriptor rows go from the
+// staging buffer to every destination of `gd` (multicast or peer stores) instead of a bulk
+// store to `desc`; `desc` is then local scratch for the ROIs that take the generic code path,
+// whose rows are forwarded from there.  OUTM == kOutU8: the compact row (U8Out) is staged
+// and bulk-stored; `desc` is unused (the generic path counts into the group's counters and
+// stages its row the same way).
+template <bool HAS_DEPTH, bool DEPTH_SRC, int WINM, bool FRAME, int OUTM = l59::kOutU16>
 __global__ void __launch_bounds__(l59::kThreads, 1)
 lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const __grid_constant__ CUtensorMap depth_map,
@@ -249,8 +285,10 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        DepthWindow win, uint16_t* __restrict__ desc, int64_t desc_stride,
                        int32_t* __restrict__ roi_status, int32_t lut_off,
                        const __grid_constant__ lbp_gather_dst_t gd,
-                       const int32_t* __restrict__ glabels) {
-    static_assert(!GATHER || !FRAME, "the fused gather uses the crop-stack epilogue");
+                       const int32_t* __restrict__ glabels, const __grid_constant__ U8Out u8o) {
+    constexpr bool GATHER = OUTM == l59::kOutGather;
+    constexpr bool U8 = OUTM == l59::kOutU8;
+    static_assert(OUTM == l59::kOutU16 || !FRAME, "the gather / u8 outputs use the crop-stack epilogue");
     using namespace l59;
     using L = Layout<FRAME>;
     constexpr bool FP16WIN = WINM != 0;
@@ -274,6 +312,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t stages0 = smem_u32(smem);
     const uint32_t hist0 = stages0 + kGroupOff + group * kGroupBytes;
     const uint32_t staging = FRAME ? hist0 : hist0 + kHistBytes;
+    const uint32_t exc_cnt = staging + kDescBytes;  // U8: the crop's exception count (slack)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     const uint32_t bar_id = 1 + group;
 
@@ -313,6 +352,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     if (tid < 256) smem[kPlainLutOff + tid] = kUniformLutDev.v[tid];
     for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
+    if (U8 && gtid == 0) st_shared_u32(exc_cnt, 0u);
     if (tid == 0) {
         // the host placed the LUT from the device's reserved shared memory size; a mismatch
         // would misaddress every lookup, so it stops the kernel (LBP_E_CUDA) instead
@@ -370,6 +410,35 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (!is_fast(roi)) {
             if (gtid == 0) {  // stage s was never filled: release it at once
                 issue(i + kStages, roi_next);  // (position i + 3 = this group's next)
+            }
+            if constexpr (U8) {
+                // counts stay in the group's counters (KEEP; 64 cells x 59 bins fit one chunk),
+                // then the row is staged as u8 + exceptions like the fast path's
+                if (gtid == 0) bulk_wait_read_all();        // previous row left the staging
+                named_barrier_sync(bar_id, kGroupThreads);
+                uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (hist0 - stages0));
+                uint16_t* zrow = reinterpret_cast<uint16_t*>(smem + (staging - stages0));
+                extract_roi_generic<kBins, kGroupThreads, uint8_t, GroupSync, true>(
+                    CodePlane<uint8_t>{grey, geom.grey_pitch, geom.grey_img_stride},
+                    HAS_DEPTH ? depth : nullptr, geom, roi, 0, win, 8, 8, zrow, 0, nullptr,
+                    hist, kHistBytes / 4, smem + kPlainLutOff, 0, gtid, GroupSync{bar_id});
+                if (gtid == 0 && roi_status) roi_status[n] = clamp_roi(roi, geom, 8, 8).status;
+                named_barrier_sync(bar_id, kGroupThreads);  // counts complete
+                for (int d = gtid; d < 64 * kBins; d += kGroupThreads) {
+                    const uint32_t v = hist[d];
+                    hist[d] = 0u;
+                    put_u8(staging, (uint32_t)d, v);
+                    record_u8(u8o, n, exc_cnt, (uint32_t)d, v);
+                }
+                fence_proxy_async_smem();
+                named_barrier_sync(bar_id, kGroupThreads);  // staging complete, counters zero
+                if (gtid == 0) {
+                    bulk_store_s2g(u8o.packed + (int64_t)n * u8o.pitch, staging, kDescBytes / 2);
+                    u8o.exc_n[n] = (int32_t)ld_shared_u32(exc_cnt);
+                    st_shared_u32(exc_cnt, 0u);
+                }
+                pending = n;
+                continue;
             }
             if (DEPTH_SRC)
                 extract_roi_generic<kBins, kGroupThreads>(
@@ -608,9 +677,32 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 }
                 const uint4 c = counts(qa);
                 st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
-                put(g, bin, cx, c);
+                if constexpr (U8) {
+                    const uint32_t d0 = (uint32_t)(((4 * g) * 8 + cx) * kBins + bin);
+                    constexpr uint32_t kRowE = 8 * kBins;  // next cell row
+                    put_u8(staging, d0, c.x);
+                    put_u8(staging, d0 + kRowE, c.y);
+                    put_u8(staging, d0 + 2 * kRowE, c.z);
+                    put_u8(staging, d0 + 3 * kRowE, c.w);
+                    if ((c.x | c.y | c.z | c.w) > 255u) {  // one test per quad
+                        record_u8(u8o, n, exc_cnt, d0, c.x);
+                        record_u8(u8o, n, exc_cnt, d0 + kRowE, c.y);
+                        record_u8(u8o, n, exc_cnt, d0 + 2 * kRowE, c.z);
+                        record_u8(u8o, n, exc_cnt, d0 + 3 * kRowE, c.w);
+                    }
+                } else {
+                    put(g, bin, cx, c);
+                }
             }
-            if constexpr (GATHER) {
+            if constexpr (U8) {
+                fence_proxy_async_smem();                   // staging writes -> async proxy
+                named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
+                if (gtid == 0) {
+                    bulk_store_s2g(u8o.packed + (int64_t)n * u8o.pitch, staging, kDescBytes / 2);
+                    u8o.exc_n[n] = (int32_t)ld_shared_u32(exc_cnt);
+                    st_shared_u32(exc_cnt, 0u);
+                }
+            } else if constexpr (GATHER) {
                 // every thread forwards 16-B chunks of the staged row to every destination
                 // (the staging is rewritten only after the next crop's barrier A, which every
                 // thread reaches after its loads here)
@@ -657,8 +749,9 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
                                           cudaStream_t stream, bool depth_source = false,
                                           bool frame = false,
                                           const lbp_gather_dst_t* gather = nullptr,
-                                          const int32_t* glabels = nullptr) {
-    if (gather && (frame || depth_source)) return cudaErrorNotSupported;
+                                          const int32_t* glabels = nullptr,
+                                          const U8Out* u8out = nullptr) {
+    if ((gather || u8out) && (frame || depth_source)) return cudaErrorNotSupported;
     CUtensorMap gm, dm;
     if (!depth_source &&
         !encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
@@ -688,14 +781,18 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
                              : lbp_hist_lane59_kernel<true, false, 0, F>;
         return lbp_hist_lane59_kernel<false, false, 0, F>;
     };
-    auto pick_gather = [&]() {
+    auto pick_out = [&](auto out_tag) {  // crop stacks, grey codes, gather or u8 output
+        constexpr int O = decltype(out_tag)::value;
         if (depth)
-            return centred   ? lbp_hist_lane59_kernel<true, false, 2, false, true>
-                   : fp16win ? lbp_hist_lane59_kernel<true, false, 1, false, true>
-                             : lbp_hist_lane59_kernel<true, false, 0, false, true>;
-        return lbp_hist_lane59_kernel<false, false, 0, false, true>;
+            return centred   ? lbp_hist_lane59_kernel<true, false, 2, false, O>
+                   : fp16win ? lbp_hist_lane59_kernel<true, false, 1, false, O>
+                             : lbp_hist_lane59_kernel<true, false, 0, false, O>;
+        return lbp_hist_lane59_kernel<false, false, 0, false, O>;
     };
-    auto kern = gather ? pick_gather() : frame ? pick(std::true_type{}) : pick(std::false_type{});
+    auto kern = gather  ? pick_out(std::integral_constant<int, l59::kOutGather>{})
+                : u8out ? pick_out(std::integral_constant<int, l59::kOutU8>{})
+                : frame ? pick(std::true_type{})
+                        : pick(std::false_type{});
     int lut_off = 0, smem = 0;
     if (!lut_placement(frame ? l59::Layout<true>::kLutMin : l59::Layout<false>::kLutMin,
                        l59::Layout<false>::kTailBytes, &lut_off, &smem))
@@ -705,9 +802,11 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     const int grid = std::max(1, std::min(sms, n_rois));
     lbp_gather_dst_t gd{};
     if (gather) gd = *gather;
+    U8Out uo{};
+    if (u8out) uo = *u8out;
     kern<<<grid, l59::kThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win,
                                                  desc, desc_stride, roi_status, lut_off, gd,
-                                                 glabels);
+                                                 glabels, uo);
     return cudaGetLastError();
 }
 

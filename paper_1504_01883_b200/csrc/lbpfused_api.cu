@@ -16,6 +16,7 @@
 #include "svm_fp64.cuh"
 #include "svm_gemm.cuh"
 #include "svm_gemm_i8.cuh"
+#include "svm_gemm_u8.cuh"
 #include "svm_train.cuh"
 
 using namespace lbpf;
@@ -302,6 +303,49 @@ int32_t lbp_extract_gather(const uint8_t* grey, const uint16_t* depth, lbp_image
     return launch_status(cudaGetLastError());
 }
 
+int32_t lbp_u8_exc_cap_min(lbp_images_t geom, int32_t dim) {
+    if (dim < 1 || geom.width < 1 || geom.height < 1) return LBP_E_ARG;
+    const int64_t inner = (int64_t)std::max(geom.width - 2, 0) * std::max(geom.height - 2, 0);
+    return (int32_t)std::min<int64_t>(inner / 256, dim);
+}
+
+int32_t lbp_extract_u8(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
+                       const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
+                       int32_t cells_x, int32_t cells_y, int32_t bins, uint8_t* packed,
+                       int64_t pitch, int32_t* exc_n, uint32_t* exc, int32_t exc_cap,
+                       uint16_t* scratch, int32_t* roi_status, lbp_stream_t stream_) {
+    if (n_rois < 0) return LBP_E_ARG;
+    const int32_t dim = lbp_descriptor_dim(cells_x, cells_y, bins);
+    if (dim < 0) return dim;
+    if (dim > 65535 || pitch < dim || dmin > dmax) return LBP_E_ARG;
+    int32_t st = check_geometry(geom, true, depth != nullptr);
+    if (st != LBP_OK) return st;
+    if (exc_cap < lbp_u8_exc_cap_min(geom, dim)) return LBP_E_ARG;
+    if (n_rois == 0) return LBP_OK;
+    if (!grey || !rois || !packed || !exc_n || (exc_cap > 0 && !exc)) return LBP_E_ARG;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const DepthWindow win = make_window(dmin, dmax);
+    const bool frame = geom.width >= l59::Layout<true>::kGreyW;
+    if (n_rois >= num_sms() && bins == 59 && !frame && (pitch & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(packed) & 15) == 0 &&
+        fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, nullptr)) {
+        const U8Out uo{packed, exc_n, exc, exc_cap, pitch};
+        const cudaError_t e = launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win,
+                                                     nullptr, 0, roi_status, num_sms(), stream,
+                                                     false, false, nullptr, nullptr, &uo);
+        if (e != cudaErrorNotSupported) return launch_status(e);
+    }
+    if (!scratch) return LBP_E_ARG;
+    st = lbp_extract_source(grey, depth, geom, rois, n_rois, dmin, dmax, cells_x, cells_y, bins,
+                            LBP_SRC_GREY, scratch, roi_status, stream_);
+    if (st != LBP_OK) return st;
+    const int grid = (int)std::min<int64_t>(((int64_t)n_rois * 32 + 255) / 256,
+                                            (int64_t)num_sms() * 8);
+    desc_pack_rows_kernel<<<grid, 256, 0, stream>>>(scratch, n_rois, dim, packed, pitch, exc_n,
+                                                     exc, exc_cap);
+    return launch_status(cudaGetLastError());
+}
+
 int32_t lbp_fused_extract(const uint8_t* grey, const uint16_t* depth, lbp_images_t geom,
                           const lbp_roi_t* rois, int32_t n_rois, uint16_t dmin, uint16_t dmax,
                           int32_t cells_x, int32_t cells_y, int32_t bins, uint16_t* desc,
@@ -506,6 +550,60 @@ int32_t svm_prepare(const float* W, int32_t n_classes, int32_t dim, void* worksp
     else
         svm_prepare_kernel<<<h.total_rows, 256, 0, (cudaStream_t)stream>>>(W, h,
                                                                           (uint8_t*)workspace);
+    return launch_status(cudaGetLastError());
+}
+
+size_t svm_workspace_u8_bytes(int32_t n_classes, int32_t dim) {
+    SvmPrepHeader h;
+    if (!svm_layout_u8(n_classes, dim, &h)) return 0;
+    return svm_layout_u8_total(h);
+}
+
+int32_t svm_prepare_u8(const float* W, int32_t n_classes, int32_t dim, void* workspace,
+                       size_t workspace_bytes, lbp_stream_t stream) {
+    if (!W || !workspace || n_classes < 1 || dim < 1) return LBP_E_ARG;
+    SvmPrepHeader h;
+    if (!svm_layout_u8(n_classes, dim, &h)) return LBP_E_UNSUPPORTED;
+    if (workspace_bytes < svm_layout_u8_total(h)) return LBP_E_ARG;
+    svm_prepare_u8_kernel<kU8Digits><<<h.total_rows, 256, 0, (cudaStream_t)stream>>>(
+        W, h, (uint8_t*)workspace);
+    const U8Layout L4 = u8_layout(n_classes, 4);
+    svm_prepare_u8_kernel<4><<<L4.N * L4.n_pass, 256, 0, (cudaStream_t)stream>>>(
+        W, h, (uint8_t*)workspace);
+    return launch_status(cudaGetLastError());
+}
+
+int32_t svm_score_u8(const uint8_t* packed, int64_t pitch, const int32_t* exc_n,
+                     const uint32_t* exc, int32_t exc_cap, int32_t n, int32_t dim,
+                     const float* W, const float* bias, int32_t n_classes, const void* prepared,
+                     size_t prepared_bytes, float* scores, int32_t* labels, float* top_score,
+                     float reject_threshold, lbp_stream_t stream_) {
+    if (n < 0 || dim < 1 || dim > 65535 || n_classes < 1 || pitch < dim || exc_cap < 0)
+        return LBP_E_ARG;
+    if (prepared && prepared_bytes < svm_workspace_u8_bytes(n_classes, dim)) return LBP_E_ARG;
+    if (n == 0) return LBP_OK;
+    if (!packed || !exc_n || (exc_cap > 0 && !exc) || !W || !bias) return LBP_E_ARG;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    SvmPrepHeader h;
+    if (prepared && n >= kGemmM && svm_layout_u8(n_classes, dim, &h) && (pitch & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(packed) & 15) == 0) {
+        const cudaError_t e = launch_svm_gemm_u8(packed, pitch, exc_n, exc, exc_cap, n, dim, W,
+                                                 bias, h, (const uint8_t*)prepared, scores,
+                                                 labels, top_score, reject_threshold, num_sms(),
+                                                 stream);
+        if (e != cudaErrorNotSupported) return launch_status(e);
+    }
+    const size_t smem = (size_t)dim * sizeof(float);
+    if (smem > 200 * 1024) return LBP_E_UNSUPPORTED;
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(
+            svm_score_u8_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return launch_status(e);
+    }
+    const int grid = (int)std::min<int64_t>(n, (int64_t)num_sms() * 8);
+    svm_score_u8_fp64_kernel<<<grid, kU8F64Threads, smem, stream>>>(
+        packed, pitch, exc_n, exc, exc_cap, n, dim, W, bias, n_classes, scores, labels,
+        top_score, reject_threshold);
     return launch_status(cudaGetLastError());
 }
 

@@ -86,6 +86,17 @@ def lib():
         L.lbp_extract_gather.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, P,
                                          lbp_gather_dst_t, P, P, P]
         L.lbp_extract_gather.restype = i32
+        L.lbp_u8_exc_cap_min.argtypes = [lbp_images_t, i32]
+        L.lbp_u8_exc_cap_min.restype = i32
+        L.lbp_extract_u8.argtypes = [P, P, lbp_images_t, P, i32, u16, u16, i32, i32, i32, P, i64,
+                                     P, P, i32, P, P, P]
+        L.lbp_extract_u8.restype = i32
+        L.svm_workspace_u8_bytes.argtypes = [i32, i32]
+        L.svm_workspace_u8_bytes.restype = sz
+        L.svm_prepare_u8.argtypes = [P, i32, i32, P, sz, P]
+        L.svm_prepare_u8.restype = i32
+        L.svm_score_u8.argtypes = [P, i64, P, P, i32, i32, i32, P, P, i32, P, sz, P, P, P, f32, P]
+        L.svm_score_u8.restype = i32
         L.svm_workspace_bytes.argtypes = [i32, i32]
         L.svm_workspace_bytes.restype = sz
         L.svm_prepare.argtypes = [P, i32, i32, P, sz, P]
@@ -414,6 +425,145 @@ def svm_score(desc: torch.Tensor, W: torch.Tensor, bias: torch.Tensor, prepared=
                          reject_threshold, _stream(stream))
     if st != LBP_OK:
         raise LbpError(st, "svm_score")
+    return (scores if want_scores else None), labels, top_score
+
+
+# ---- compact descriptors (include/lbpfused.h lbp_extract_u8 / svm_score_u8)
+
+class CompactDesc:
+    """The compact descriptor of lbp_extract_u8: packed u8 [n][dim] = count & 255 (low byte),
+    exc_n int32 [n], exc int32 [n][cap] holding the uint32 records (d << 16) | count of the
+    entries above 255 (the first exc_n[i] of row i)."""
+
+    def __init__(self, packed: torch.Tensor, exc_n: torch.Tensor, exc: torch.Tensor):
+        self.packed, self.exc_n, self.exc = packed, exc_n, exc
+
+    @property
+    def n(self) -> int:
+        return self.packed.shape[0]
+
+    @property
+    def dim(self) -> int:
+        return self.packed.shape[1]
+
+    @property
+    def cap(self) -> int:
+        return self.exc.shape[1]
+
+    @staticmethod
+    def empty(n: int, dim: int, cap: int, device) -> "CompactDesc":
+        return CompactDesc(torch.empty((n, dim), dtype=torch.uint8, device=device),
+                           torch.empty(n, dtype=torch.int32, device=device),
+                           torch.empty((n, max(cap, 1)), dtype=torch.int32, device=device))
+
+    def _check(self, n: int, dim: int, device) -> None:
+        _out(self.packed, torch.uint8, n * dim, "packed", device)
+        _require(self.packed.dim() == 2 and self.packed.shape[1] == dim,
+                 f"packed is [n][{dim}]")
+        _out(self.exc_n, torch.int32, n, "exc_n", device)
+        _require(self.exc.dtype == torch.int32 and self.exc.is_contiguous() and
+                 self.exc.dim() == 2 and self.exc.shape[0] >= n, "exc int32 [n][cap]")
+        _require(self.exc.device == device, f"exc.device == {device}")
+
+
+def lbp_u8_exc_cap_min(geom: lbp_images_t, dim: int) -> int:
+    v = lib().lbp_u8_exc_cap_min(geom, dim)
+    if v < 0:
+        raise LbpError(v, "lbp_u8_exc_cap_min")
+    return v
+
+
+def lbp_extract_u8(grey: torch.Tensor, depth: torch.Tensor | None, rois: torch.Tensor,
+                   dmin: int, dmax: int, cells_x: int, cells_y: int, bins: int,
+                   out: CompactDesc | None = None, cap: int | None = None,
+                   scratch: torch.Tensor | None = None, roi_status: torch.Tensor | None = None,
+                   stream=None) -> CompactDesc:
+    """Compact descriptors (CompactDesc) of the ROIs: lbp_fused_extract's rows as u8 + records
+    of the entries above 255, written by the extraction kernel's epilogue."""
+    _check_cuda(grey, depth, rois, scratch, roi_status)
+    _require(grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16),
+             "grey.dtype == torch.uint8 and (depth is None or depth.dtype == torch.uint16)")
+    _require(rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5,
+             "rois.dtype == torch.int32 and rois.is_contiguous() and rois.shape[-1] == 5")
+    n = rois.shape[0]
+    dim = lbp_descriptor_dim(cells_x, cells_y, bins)
+    geom = images_geometry(grey, depth)
+    dev = grey.device
+    if out is None:
+        out = CompactDesc.empty(n, dim, cap if cap is not None else lbp_u8_exc_cap_min(geom, dim),
+                                dev)
+    out._check(n, dim, dev)
+    _out(scratch, torch.uint16, n * dim, "scratch", dev)
+    _out(roi_status, torch.int32, n, "roi_status", dev)
+    st = lib().lbp_extract_u8(_ptr(grey), _ptr(depth), geom, _ptr(rois), n, dmin, dmax,
+                              cells_x, cells_y, bins, _ptr(out.packed), dim, _ptr(out.exc_n),
+                              _ptr(out.exc), out.cap, _ptr(scratch), _ptr(roi_status),
+                              _stream(stream))
+    if st == LBP_E_ARG and scratch is None and n > 0:
+        # off the TMA kernel (small batch / other geometry): extract + pack via a u16 scratch
+        scratch = torch.empty((n, dim), dtype=torch.uint16, device=dev)
+        st = lib().lbp_extract_u8(_ptr(grey), _ptr(depth), geom, _ptr(rois), n, dmin, dmax,
+                                  cells_x, cells_y, bins, _ptr(out.packed), dim,
+                                  _ptr(out.exc_n), _ptr(out.exc), out.cap, _ptr(scratch),
+                                  _ptr(roi_status), _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "lbp_extract_u8")
+    return out
+
+
+def svm_workspace_u8_bytes(n_classes: int, dim: int) -> int:
+    return int(lib().svm_workspace_u8_bytes(n_classes, dim))
+
+
+def svm_prepare_u8(W: torch.Tensor, stream=None) -> torch.Tensor | None:
+    """Digit-plane workspace of svm_score_u8's tensor-core path (None if it does not apply)."""
+    _check_cuda(W)
+    _require(W.dtype == torch.float32 and W.is_contiguous() and W.dim() == 2,
+             "W fp32 contiguous [C][dim]")
+    C, dim = W.shape
+    nbytes = svm_workspace_u8_bytes(C, dim)
+    if nbytes == 0:
+        return None
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=W.device)
+    st = lib().svm_prepare_u8(_ptr(W), C, dim, _ptr(ws), nbytes, _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "svm_prepare_u8")
+    return ws
+
+
+def svm_score_u8(cd: CompactDesc, W: torch.Tensor, bias: torch.Tensor, prepared=None,
+                 reject_threshold: float = -math.inf, want_scores: bool = True,
+                 labels: torch.Tensor | None = None, top_score: torch.Tensor | None = None,
+                 scores: torch.Tensor | None = None, stream=None):
+    """svm_score on a CompactDesc: (scores or None, labels, top)."""
+    _check_cuda(W, bias, prepared)
+    n, dim = cd.n, cd.dim
+    dev = cd.packed.device
+    cd._check(n, dim, dev)
+    C = _model(W, bias, dim, dev, "svm_score_u8")
+    pbytes = 0
+    if prepared is not None:
+        _require(prepared.dtype == torch.uint8 and prepared.is_contiguous() and
+                 prepared.device == dev, "prepared uint8 contiguous on the descriptors' device")
+        _require(prepared.numel() >= svm_workspace_u8_bytes(C, dim),
+                 "prepared.numel() >= svm_workspace_u8_bytes(C, dim)")
+        pbytes = prepared.numel()
+    if want_scores and scores is None:
+        scores = torch.empty((n, C), dtype=torch.float32, device=dev)
+    if labels is None:
+        labels = torch.empty(n, dtype=torch.int32, device=dev)
+    if top_score is None:
+        top_score = torch.empty(n, dtype=torch.float32, device=dev)
+    _out(labels, torch.int32, n, "labels", dev)
+    _out(top_score, torch.float32, n, "top_score", dev)
+    if want_scores:
+        _out(scores, torch.float32, n * C, "scores", dev)
+    st = lib().svm_score_u8(_ptr(cd.packed), dim, _ptr(cd.exc_n), _ptr(cd.exc), cd.cap, n, dim,
+                            _ptr(W), _ptr(bias), C, _ptr(prepared), pbytes,
+                            _ptr(scores if want_scores else None), _ptr(labels),
+                            _ptr(top_score), reject_threshold, _stream(stream))
+    if st != LBP_OK:
+        raise LbpError(st, "svm_score_u8")
     return (scores if want_scores else None), labels, top_score
 
 

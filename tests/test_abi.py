@@ -218,3 +218,42 @@ def test_extract_gather_argument_errors(L):
     assert call(grey=None) == lb.LBP_E_ARG
     with pytest.raises(ValueError):
         lb.gather_dst(lb.LBP_GATHER_PEERS, [base] * 9, 0, 64, -1, 0)
+
+
+def test_compact_path_argument_errors(L):
+    """lbp_extract_u8 / svm_score_u8 / svm_prepare_u8 (the compact recognition path):
+    host-detectable errors return before any CUDA call; exc_cap must cover the bound."""
+    from paper_1504_01883_b200 import lbpfused as lb
+    P = ctypes.c_void_p
+    dummy = P(0x1000)
+    g = lb.lbp_images_t(1, 128, 128, 0, 128, 128, 128 * 128, 128 * 128)
+    assert lb.lbp_u8_exc_cap_min(g, 3776) == (126 * 126) // 256 == 62
+    assert lb.lbp_u8_exc_cap_min(lb.lbp_images_t(1, 2, 2, 0, 2, 2, 4, 4), 59) == 0
+    assert lb.lbp_u8_exc_cap_min(_geom(lb, H=400, W=400, pitch=400), 59) == 59  # capped at dim
+
+    def ext(n=1, cap=64, pitch=3776, bins=59, packed=dummy, exc_n=dummy, exc=dummy, grey=dummy):
+        return L.lbp_extract_u8(grey, None, g, dummy, n, 0, 10, 8, 8, bins, packed, pitch,
+                                exc_n, exc, cap, None, None, None)
+    assert ext(n=0) == lb.LBP_OK
+    assert ext(cap=61) == lb.LBP_E_ARG        # below the bound
+    assert ext(pitch=3775) == lb.LBP_E_ARG    # pitch < dim
+    assert ext(bins=60) == lb.LBP_E_ARG
+    assert ext(n=-1) == lb.LBP_E_ARG
+    assert ext(packed=None) == lb.LBP_E_ARG
+    assert ext(exc_n=None) == lb.LBP_E_ARG
+    assert ext(exc=None) == lb.LBP_E_ARG
+    assert ext(grey=None) == lb.LBP_E_ARG
+
+    def score(n=4, dim=3776, C=10, pitch=3776, cap=64, prep=None, pbytes=0):
+        return L.svm_score_u8(dummy, pitch, dummy, dummy, cap, n, dim, dummy, dummy, C, prep,
+                              pbytes, None, None, None, 0.0, None)
+    assert score(n=0) == lb.LBP_OK
+    assert score(n=-1) == lb.LBP_E_ARG
+    assert score(C=0) == lb.LBP_E_ARG
+    assert score(pitch=100) == lb.LBP_E_ARG
+    assert score(dim=70000, pitch=70000) == lb.LBP_E_ARG
+    assert score(prep=dummy, pbytes=16) == lb.LBP_E_ARG  # workspace too small
+    assert lb.svm_workspace_u8_bytes(100, 3776) > 0
+    assert lb.svm_workspace_u8_bytes(100, 40000) == 0    # dim > 32,768: no tensor-core layout
+    assert L.svm_prepare_u8(None, 10, 3776, dummy, 1 << 30, None) == lb.LBP_E_ARG
+    assert L.svm_prepare_u8(dummy, 10, 3776, dummy, 16, None) == lb.LBP_E_ARG
