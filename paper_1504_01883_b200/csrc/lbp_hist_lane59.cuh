@@ -48,7 +48,9 @@ static_assert(kStages == kGroups, "a group refills its own stage with its next c
 // epilogue output modes of the kernel (template parameter OUTM)
 constexpr int kOutU16 = 0;     // u16 row, one bulk store (lbp_fused_extract)
 constexpr int kOutGather = 1;  // u16 row stored into every destination (lbp_extract_gather)
-constexpr int kOutU8 = 2;      // compact row: u8 min(count, 255) + exceptions (lbp_extract_u8)
+constexpr int kOutU8 = 2;      // compact row: u8 low bytes + exceptions (lbp_extract_u8)
+constexpr int kOutFused = 3;   // u16 grey block then depth block from ONE staged tile
+                               // (lbp_extract_source LBP_SRC_FUSED)
 
 // Stage layout of the two variants.  FRAME (ROIs at any column of wider frames): the grey
 // box is 144 px wide at x & ~15 and the depth box 136 px at x & ~7 (TMA needs 16-B aligned
@@ -288,6 +290,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        const int32_t* __restrict__ glabels, const __grid_constant__ U8Out u8o) {
     constexpr bool GATHER = OUTM == l59::kOutGather;
     constexpr bool U8 = OUTM == l59::kOutU8;
+    constexpr bool FUSED = OUTM == l59::kOutFused;
+    static_assert(!FUSED || (HAS_DEPTH && !DEPTH_SRC && WINM != 0 && !FRAME),
+                  "fused grey||depth: depth plane staged, fp16 depth window, crop stacks");
     static_assert(OUTM == l59::kOutU16 || !FRAME, "the gather / u8 outputs use the crop-stack epilogue");
     using namespace l59;
     using L = Layout<FRAME>;
@@ -452,6 +457,12 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 HAS_DEPTH ? depth : nullptr, geom, roi, n, win, 8, 8, desc, desc_stride, roi_status,
                 reinterpret_cast<uint32_t*>(smem + (hist0 - stages0)), kHistBytes / 4,
                 smem + kPlainLutOff, 0, gtid, GroupSync{bar_id});
+            if constexpr (FUSED)  // the depth block of the row
+                extract_roi_generic<kBins, kGroupThreads>(
+                    CodePlane<uint16_t>{depth, geom.depth_pitch, geom.depth_img_stride}, depth, geom,
+                    roi, n, win, 8, 8, desc + 64 * kBins, desc_stride, nullptr,
+                    reinterpret_cast<uint32_t*>(smem + (hist0 - stages0)), kHistBytes / 4,
+                    smem + kPlainLutOff, 0, gtid, GroupSync{bar_id});
             named_barrier_sync(bar_id, kGroupThreads);
             if constexpr (GATHER) {  // forward the row written to the local scratch
                 gather_row_from_global<kGroupThreads>(gd, n, desc + (int64_t)n * desc_stride,
@@ -460,16 +471,20 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             }
             continue;
         }
+        // One code plane of the staged crop (FUSED: the grey plane, then the depth plane of the
+        // same staged tile -- depth read from HBM once); `last` releases the stage.
+        auto plane = [&](auto src_tag, uint16_t* out_row, bool last) {
+        constexpr bool DS = decltype(src_tag)::value;  // codes on the depth plane
         const uint32_t st = stages0 + s * kStageBytes;
-        // code plane rows: grey u8 (kGreyW B per row) or depth u16 (2 kDepthW B, DEPTH_SRC).
+        // code plane rows: grey u8 (kGreyW B per row) or depth u16 (2 kDepthW B, DS).
         // FRAME: the lane's bytes start og (grey) / 2 od (depth) bytes past its aligned words.
         constexpr uint32_t kDRow = 2 * L::kDepthW;
-        constexpr uint32_t kRowStep = DEPTH_SRC ? kDRow : L::kGreyW;
+        constexpr uint32_t kRowStep = DS ? kDRow : L::kGreyW;
         const uint32_t og = FRAME ? (uint32_t)roi.x & 15u : 0u;
         const uint32_t od2 = FRAME ? 2u * ((uint32_t)roi.x & 7u) : 0u;
         const uint32_t gsel = 0x3210u + (og & 3u) * 0x1111u;    // funnel by og & 3 bytes
         const uint32_t dsel = (od2 & 2u) ? 0x5432u : 0x3210u;  // funnel by 0 / 2 bytes
-        const uint32_t g0 = DEPTH_SRC ? opaque(st + kGreyBytes + i0 * kDRow + 8 * lane + (od2 & ~3u))
+        const uint32_t g0 = DS ? opaque(st + kGreyBytes + i0 * kDRow + 8 * lane + (od2 & ~3u))
                                       : opaque(st + i0 * L::kGreyW + 4 * lane + (og & ~3u));
         const uint32_t d0 = opaque(st + kGreyBytes + (i0 + 1) * kDRow + 8 * lane + (od2 & ~3u));
         // Raw shared-memory words of a row are loaded one row AHEAD of their use (the loop
@@ -491,13 +506,13 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             else return make_uint2(w.a, w.b);
         };
         auto raw_row = [&](uint32_t addr) {
-            if constexpr (DEPTH_SRC) return raw_depth(addr);
+            if constexpr (DS) return raw_depth(addr);
             Raw w{ld_shared_u32(addr), 0u, 0u};
             if constexpr (FRAME) w.b = ld_shared_u32(addr + 4);
             return w;
         };
         auto build_row = [&](const Raw& w) {
-            if constexpr (DEPTH_SRC) return depth_row_w(depth_words(w));
+            if constexpr (DS) return depth_row_w(depth_words(w));
             else if constexpr (FRAME) return lane_row_w(prmt(w.a, w.b, gsel));
             else return lane_row_w(w.a);
         };
@@ -508,7 +523,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         struct Pend { uint32_t bin[4], val[4]; };
         auto do_row = [&](const Row& top, const Row& mid, const Row& bot, const Raw& dc) {
             uint32_t t0, t1;
-            if constexpr (DEPTH_SRC) {
+            if constexpr (DS) {
                 t0 = lbp_offset2_cmp(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
                                      bot.lh0, mid.lh0, base2);
                 t1 = lbp_offset2_cmp(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
@@ -525,7 +540,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 // masked-out pixels are redirected to the dummy LUT row (-> dummy bin)
                 // instead of adding 0
                 uint32_t c0, c1;
-                if constexpr (DEPTH_SRC) {
+                if constexpr (DS) {
                     c0 = mid.raw0;
                     c1 = mid.raw1;
                 } else {
@@ -547,7 +562,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 for (int k = 0; k < 4; ++k) val[k] = mult[k];
             } else if (HAS_DEPTH) {
                 uint2 d;
-                if constexpr (DEPTH_SRC) d = make_uint2(mid.raw0, mid.raw1);  // centre row
+                if constexpr (DS) d = make_uint2(mid.raw0, mid.raw1);  // centre row
                 else d = depth_words(dc);
                 // depth window on a u16 in either half of a word
                 const uint32_t x[4] = {d.x * 0x10000u - lo16, d.x - lo16, d.y * 0x10000u - lo16,
@@ -573,7 +588,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             for (int k = 0; k < 4; ++k) red_shared_add(colb[k] + p.bin[k] * (32 * 4), p.val[k]);
         };
         // 16 rows, straight-line (the 15-row cell rows stop before the 16th).
-        constexpr bool kMaskRow = HAS_DEPTH && !DEPTH_SRC;  // a separate depth centre row
+        constexpr bool kMaskRow = HAS_DEPTH && !DS;  // a separate depth centre row
         Row r0 = build_row(raw_row(g0)), r1 = build_row(raw_row(g0 + kRowStep));
         Raw wn = raw_row(g0 + 2 * kRowStep), dn{0u, 0u, 0u};
         Pend pend;
@@ -600,7 +615,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
 
         if (gtid == 0) bulk_wait_read_all();        // previous descriptor left the staging
         named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
-        if (gtid == 0) {
+        if (gtid == 0 && last) {
             issue(i + kStages, roi_next);
             if (roi_status) roi_status[n] = LBP_OK;
         }
@@ -656,7 +671,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 if (q < kQ && (q >> 3) < kBins) put(1, q >> 3, q & 7, cnt[k]);
             }
             named_barrier_sync(bar_id, kGroupThreads);  // staging complete
-            uint16_t* out = desc + (int64_t)n * desc_stride;
+            uint16_t* out = out_row;
             for (int idx = gtid; idx < kQ; idx += kGroupThreads) {  // g = 0 region: 480 x 16 B
                 const uint32_t sa = hist0 + idx * 16;
                 if (idx < kDescBytes / 16) {
@@ -712,8 +727,15 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             } else {
                 fence_proxy_async_smem();                   // staging writes -> async proxy
                 named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-                if (gtid == 0) bulk_store_s2g(desc + (int64_t)n * desc_stride, staging, kDescBytes);
+                if (gtid == 0) bulk_store_s2g(out_row, staging, kDescBytes);
             }
+        }
+        };
+        if constexpr (FUSED) {
+            plane(std::false_type{}, desc + (int64_t)n * desc_stride, false);
+            plane(std::true_type{}, desc + (int64_t)n * desc_stride + 64 * kBins, true);
+        } else {
+            plane(std::integral_constant<bool, DEPTH_SRC>{}, desc + (int64_t)n * desc_stride, true);
         }
         pending = n;
     }
@@ -750,8 +772,8 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
                                           bool frame = false,
                                           const lbp_gather_dst_t* gather = nullptr,
                                           const int32_t* glabels = nullptr,
-                                          const U8Out* u8out = nullptr) {
-    if ((gather || u8out) && (frame || depth_source)) return cudaErrorNotSupported;
+                                          const U8Out* u8out = nullptr, bool fused = false) {
+    if ((gather || u8out || fused) && (frame || depth_source)) return cudaErrorNotSupported;
     CUtensorMap gm, dm;
     if (!depth_source &&
         !encode_stack_map(&gm, grey, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, geom, geom.grey_pitch,
@@ -789,7 +811,10 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
                              : lbp_hist_lane59_kernel<true, false, 0, false, O>;
         return lbp_hist_lane59_kernel<false, false, 0, false, O>;
     };
-    auto kern = gather  ? pick_out(std::integral_constant<int, l59::kOutGather>{})
+    if (fused && !fp16win) return cudaErrorNotSupported;  // (the depth plane's compares)
+    auto kern = fused   ? (centred ? lbp_hist_lane59_kernel<true, false, 2, false, l59::kOutFused>
+                                   : lbp_hist_lane59_kernel<true, false, 1, false, l59::kOutFused>)
+                : gather  ? pick_out(std::integral_constant<int, l59::kOutGather>{})
                 : u8out ? pick_out(std::integral_constant<int, l59::kOutU8>{})
                 : frame ? pick(std::true_type{})
                         : pick(std::false_type{});

@@ -174,6 +174,16 @@ int32_t lbp_extract_source(const uint8_t* grey, const uint16_t* depth, lbp_image
     cudaStream_t stream = (cudaStream_t)stream_;
     const DepthWindow win = make_window(dmin, dmax);
     const int64_t stride = source == LBP_SRC_FUSED ? 2 * (int64_t)dim : dim;
+    // grey || depth in ONE pass of the TMA kernel (both code planes of one staged tile, depth
+    // read from HBM once) for crop stacks of the headline geometry; else two blocks
+    if (source == LBP_SRC_FUSED && n_rois >= num_sms() && bins == 59 &&
+        geom.width < l59::Layout<true>::kGreyW &&
+        fast_path_applicable(geom, grey, depth, cells_x, cells_y, bins, desc)) {
+        const cudaError_t e = launch_lbp_hist_lane59(grey, depth, geom, rois, n_rois, win, desc,
+                                                     stride, roi_status, num_sms(), stream, false,
+                                                     false, nullptr, nullptr, nullptr, true);
+        if (e != cudaErrorNotSupported) return launch_status(e);
+    }
     if (need_grey) {
         st = extract_block(grey, depth, false, geom, rois, n_rois, win, cells_x, cells_y, bins,
                            desc, stride, roi_status, stream);

@@ -725,15 +725,17 @@ inline int u8_smem_bytes(int N) {
            kU8Distinct * 128 * 4 + kGemmM * 4 + (kU8EpiWays - 1) * kGemmM * (8 + 8 + 4);
 }
 
-// D = 5 when scores are requested (or labels are not: the recheck marker lives in them),
-// else the label-only D = 4 kernel followed by its fix-up.
+// D = 5 when scores are requested (or labels are not: the recheck marker lives in them) or
+// the model fits two D = 5 passes (C <= 102: one tile's two passes, where the fix-up launch
+// would cost more than the fifth of the MMAs it saves); else the label-only D = 4 kernel
+// followed by its fix-up.
 inline cudaError_t launch_svm_gemm_u8(const uint8_t* packed, int64_t pitch,
                                       const int32_t* exc_n, const uint32_t* exc, int32_t exc_cap,
                                       int32_t n, int32_t dim, const float* W, const float* bias,
                                       const SvmPrepHeader& h, const uint8_t* ws, float* scores,
                                       int32_t* labels, float* top, float reject, int sms,
                                       cudaStream_t stream) {
-    const bool lbl = scores == nullptr && labels != nullptr;
+    const bool lbl = scores == nullptr && labels != nullptr && u8_layout(h.n_classes).n_pass > 2;
     const int D = lbl ? 4 : kU8Digits;
     const U8Layout LY = u8_layout(h.n_classes, D);
     if (LY.P > 128) return cudaErrorNotSupported;  // (the epilogue tables hold 128 classes)

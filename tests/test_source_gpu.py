@@ -132,3 +132,23 @@ def test_depth_source_128_full_range(lb, dmax):
     rois = synthgen.full_rois(150, 128, 128)
     for source in (1, 2):
         _check(lb, grey, depth, rois, 1, dmax, 8, 8, 59, source)
+
+
+@pytest.mark.parametrize("dmin,dmax", [(600, 1400), (600, 1401), (1, 31742), (0, 0)])
+def test_fused_one_pass_mixed_rois(lb, dmin, dmax):
+    """LBP_SRC_FUSED in ONE pass of the TMA kernel (both code planes of one staged tile): the
+    centred (600..1400) and plain fp16 windows, an empty window, fast 128x128 crops mixed with
+    ROIs off the TMA path (the in-kernel generic path writes both blocks), >= 148 ROIs."""
+    n_img = 60
+    grey, depth = synthgen.face_crops(n_img, 128, 128, seed=33)
+    grey[5] = 99
+    depth[5] = 1000  # uniform crop: counts of 256 in both blocks
+    rois = np.concatenate([synthgen.full_rois(n_img, 128, 128),
+                           synthgen.random_rois(200, n_img, 128, 128, seed=7)]).astype(np.int32)
+    _check(lb, grey, depth, rois, dmin, dmax, 8, 8, 59, 2)
+
+
+def test_fused_one_pass_large_batch(lb):
+    n = 2000
+    grey, depth = synthgen.face_crops(n, 128, 128, seed=34)
+    _check(lb, grey, depth, synthgen.full_rois(n, 128, 128), 600, 1400, 8, 8, 59, 2)
