@@ -55,14 +55,16 @@ __device__ __forceinline__ int64_t gather_row_off(const lbp_gather_dst_t& g, int
     return g.desc_offset + (row + g.row_base) * g.desc_pitch * 2;
 }
 
-// Row of ROI n from a 16-B aligned shared-memory staging buffer of `chunks16` chunks (the
-// lane kernel's epilogue), by the t-th of NT threads; pad chunks up to desc_pitch are zero.
+// Chunks [c0, c1) (c1 < 0: to the end of the padded row) of the row of ROI n from a 16-B
+// aligned shared-memory staging buffer of `chunks16` chunks (the lane kernel's epilogue), by
+// the t-th of NT threads; pad chunks up to desc_pitch are zero.
 template <int NT>
 __device__ __forceinline__ void gather_row_from_smem(const lbp_gather_dst_t& g, int64_t n,
-                                                     uint32_t staging, int chunks16, int t) {
+                                                     uint32_t staging, int c0, int c1,
+                                                     int chunks16, int t) {
     const int64_t base = gather_row_off(g, n);
-    const int total = (int)(g.desc_pitch / 8);
-    for (int c = t; c < total; c += NT) {
+    const int total = c1 < 0 ? (int)(g.desc_pitch / 8) : c1;
+    for (int c = c0 + t; c < total; c += NT) {
         uint4 v = make_uint4(0, 0, 0, 0);
         if (c < chunks16)
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"

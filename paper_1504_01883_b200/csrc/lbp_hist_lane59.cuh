@@ -32,7 +32,10 @@
 namespace lbpf {
 
 namespace l59 {
-constexpr int kGroups = 3;
+#ifndef LBPF_L59_GROUPS
+#define LBPF_L59_GROUPS 3  // (2 groups with 113 registers: 10% slower -- fewer warps)
+#endif
+constexpr int kGroups = LBPF_L59_GROUPS;  // 8-warp groups per CTA, one crop each
 constexpr int kGroupThreads = 256;
 constexpr int kThreads = kGroups * kGroupThreads;
 constexpr int kTile = 128;
@@ -43,8 +46,9 @@ constexpr int kHistBytes = 2 * kBinsAlloc * 32 * 4;            // [g][bin][lane]
 constexpr int kDescBytes = 64 * kBins * 2;                     // 7,552
 constexpr int kGroupBytes = (kHistBytes + kDescBytes + 255) / 256 * 256;  // 23,040 (+ staging)
 constexpr int kLutBytes = 65 * 128;  // 64 lane-banked rows + the dummy row (bin 59 everywhere)
-constexpr uint32_t kDummyOff2 = 0x84008400u;  // LUT offset of the dummy row, both halves
-static_assert(kStages == kGroups, "a group refills its own stage with its next crop");
+constexpr uint32_t kLutMod = 0x6000u;       // the LUT's shared address mod 2^16 (lut_placement)
+constexpr uint32_t kDummyOff2 = 0x80008000u;  // LUT offset of the dummy row (64), both halves
+static_assert(kStages >= kGroups, "every group has a staged crop");
 // epilogue output modes of the kernel (template parameter OUTM)
 constexpr int kOutU16 = 0;     // u16 row, one bulk store (lbp_fused_extract)
 constexpr int kOutGather = 1;  // u16 row stored into every destination (lbp_extract_gather)
@@ -66,11 +70,12 @@ struct Layout {
     static constexpr int kGroupOff = kStages * kStageBytes;
     static constexpr int kGroupBytes = FRAME ? kHistBytes : l59::kGroupBytes;
     // the lane-banked LUT goes at the first offset >= kLutMin whose shared-window address is
-    // 0x6400 mod 2^16 (lut_placement): then the LUT address of a code offset t (a 16-bit half
-    // 0x6400 + ...) is (address - 0x6400) | t, one LOP3 / LEA.HI per half.  The plain LUT and
+    // 0x6000 mod 2^16 (lut_placement): then the LUT address of a code offset t (a 16-bit half
+    // 0x6000 + ...) is (address - 0x6000) | t, one LOP3 / IMAD.HI per half.  The plain LUT and
     // the stage barriers follow it.
     static constexpr int kLutMin = kGroupOff + kGroups * kGroupBytes;
-    static constexpr int kTailBytes = kLutBytes + 256 + kStages * 8 + 128;  // + align slack
+    // LUT, plain LUT, stage barriers, stage-release counters, align slack
+    static constexpr int kTailBytes = kLutBytes + 256 + kStages * 8 + kStages * 4 + 128;
     // headline: stages 3 x 49,152, groups 3 x 23,040 (counters + staging), LUT >= 216,576;
     // FRAME: stages 3 x 53,248, groups 3 x 15,360, LUT >= 205,824
     static_assert(kStageBytes % 128 == 0 && kGreyBytes % 128 == 0 && kLutMin % 256 == 0,
@@ -136,6 +141,16 @@ __device__ __forceinline__ uint32_t atom_shared_add(uint32_t addr, uint32_t v) {
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
     return old;
 }
+// The halves' hand-off counters (stage release, exception count) are relaxed shared-memory
+// atomics (acq_rel would add a MEMBAR after the bulk store): what they order is complete
+// before them -- the stage rows were consumed before the half's barrier A, and the half's
+// exception-count increments returned (their slots were used) before its barrier B -- and
+// the atomics of one thread reach the CTA's shared memory in program order.
+__device__ __forceinline__ uint32_t atom_shared_exch(uint32_t addr, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+    return old;
+}
 
 // entry d of row n holds count v: its low byte (staged; st.u8 keeps bits 0-7) ...
 __device__ __forceinline__ void put_u8(uint32_t staging, uint32_t d, uint32_t v) {
@@ -171,25 +186,27 @@ __device__ __forceinline__ LaneRow lane_row(uint32_t word_addr) {
 }
 
 // Eq. 2 for the centre pair c as the lane-banked LUT offset, per 16-bit half:
-// 0x6400 + 4 lane + (code & 3) + 128 * (code >> 2) with the Fig. 7 bits (TL 1, T 2, TR 4,
-// R 8, BR 16, B 32, BL 64, L 128).  TL, T, TR, R, BR: FMA pipe, sat(g_p - g_c + 1) in {0,1}
-// scaled by 1, 2, 128, 256, 512 onto base2 = 1024 + 4 lane (exact fp16 integers, sum <=
-// 1024 + 124 + 899 = 2047, so the bits are 0x6400 + the integer); B, BL, L: ALU pipe, HSET2
-// masks at offsets 1024..4096 (each half <= 0x6400 + 8191: no carry between halves).
+// 0x6000 + 4 lane + (code & 3) + 128 * (code >> 2) with the Fig. 7 bits (TL 1, T 2, TR 4,
+// R 8, BR 16, B 32, BL 64, L 128).  fp16 values in [512, 1024) have ulp 0.5 and bits
+// 0x6000 + m (value 512 + m/2, m < 1024), so bits 10-12 are zero there.  TL, T, TR, R, BR: FMA
+// pipe, sat(g_c - g_p) in {0,1} scaled by -0.5, -1, -64, -128, -256 (offsets 1, 2, 128, 256,
+// 512) onto top2 = base2 + 899/2 with base2 = 512 + 2 lane (exact: every value stays on the
+// 0.5 grid in [512, 1024)); B, BL, L: ALU pipe, HSET2 masks OR-ed into bits 10, 11, 12 (offsets
+// 1024, 2048, 4096) -- no carry, so no add: one LOP3 per bit.
 __device__ __forceinline__ uint32_t lbp_offset2(uint32_t c, uint32_t tl, uint32_t t, uint32_t tr,
                                                 uint32_t r, uint32_t br, uint32_t b, uint32_t bl,
                                                 uint32_t l, uint32_t top2) {
-    // [g_p >= g_c] = 1 - sat(g_c - g_p) (integers): start from top2 = base2 + 899 (all five
-    // bits set) and subtract w_p sat(g_c - g_p) -- one HADD2.SAT per bit, no 1 - g_c term
-    uint32_t f = f16_fma(hsub2_sat(c, tl), 0xBC00BC00u, top2);        // TL -1
-    f = f16_fma(hsub2_sat(c, t), 0xC000C000u, f);                      // T  -2
-    f = f16_fma(hsub2_sat(c, tr), 0xD800D800u, f);                     // TR -128
-    f = f16_fma(hsub2_sat(c, r), 0xDC00DC00u, f);                      // R  -256
-    f = f16_fma(hsub2_sat(c, br), 0xE000E000u, f);                     // BR -512 (>= base2)
-    uint32_t a = hge2_mask(b, c) & 0x04000400u;                        // B  +1024
-    a |= hge2_mask(bl, c) & 0x08000800u;                               // BL +2048
-    a |= hge2_mask(l, c) & 0x10001000u;                                // L  +4096
-    return f + a;
+    // [g_p >= g_c] = 1 - sat(g_c - g_p) (integers): start from top2 (all five bits set) and
+    // subtract w_p sat(g_c - g_p) -- one HADD2.SAT per bit, no 1 - g_c term
+    uint32_t f = f16_fma(hsub2_sat(c, tl), 0xB800B800u, top2);        // TL -0.5   (offset 1)
+    f = f16_fma(hsub2_sat(c, t), 0xBC00BC00u, f);                      // T  -1     (2)
+    f = f16_fma(hsub2_sat(c, tr), 0xD400D400u, f);                     // TR -64    (128)
+    f = f16_fma(hsub2_sat(c, r), 0xD800D800u, f);                      // R  -128   (256)
+    f = f16_fma(hsub2_sat(c, br), 0xDC00DC00u, f);                     // BR -256   (512)
+    f |= hge2_mask(b, c) & 0x04000400u;                                // B  bit 10 (1024)
+    f |= hge2_mask(bl, c) & 0x08000800u;                               // BL bit 11 (2048)
+    f |= hge2_mask(l, c) & 0x10001000u;                                // L  bit 12 (4096)
+    return f;
 }
 
 // ---- depth source: codes on the u16 depth plane.  A u16 d <= 0x7BFF read as
@@ -246,21 +263,22 @@ __device__ __forceinline__ uint32_t hge2_one(uint32_t a, uint32_t b) {
 }
 
 // Same LUT offset as lbp_offset2, every bit from an exact compare: TL, T, TR, R, BR as
-// 1.0/0.0 halves accumulated by HFMA2 onto 1024.0 (weights 1, 2, 128, 256, 512; exact
-// fp16 integers <= 1923), B, BL, L as HSET2 masks at 1024..4096.
+// 1.0/0.0 halves accumulated by HFMA2 onto base2 = 512 + 2 lane (weights 0.5, 1, 64, 128, 256:
+// offsets 1, 2, 128, 256, 512 on the 0.5 grid of [512, 1024)), B, BL, L as HSET2 masks OR-ed
+// into bits 10, 11, 12.
 __device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uint32_t t,
                                                     uint32_t tr, uint32_t r, uint32_t br,
                                                     uint32_t b, uint32_t bl, uint32_t l,
                                                     uint32_t base2) {
-    uint32_t f = f16_fma(hge2_one(tl, c), 0x3C003C00u, base2);        // TL +1
-    f = f16_fma(hge2_one(t, c), 0x40004000u, f);                       // T  +2
-    f = f16_fma(hge2_one(tr, c), 0x58005800u, f);                      // TR +128
-    f = f16_fma(hge2_one(r, c), 0x5C005C00u, f);                       // R  +256
-    f = f16_fma(hge2_one(br, c), 0x60006000u, f);                      // BR +512
-    uint32_t a = hge2_mask(b, c) & 0x04000400u;                        // B  +1024
-    a |= hge2_mask(bl, c) & 0x08000800u;                               // BL +2048
-    a |= hge2_mask(l, c) & 0x10001000u;                                // L  +4096
-    return f + a;
+    uint32_t f = f16_fma(hge2_one(tl, c), 0x38003800u, base2);        // TL +0.5 (offset 1)
+    f = f16_fma(hge2_one(t, c), 0x3C003C00u, f);                       // T  +1   (2)
+    f = f16_fma(hge2_one(tr, c), 0x54005400u, f);                      // TR +64  (128)
+    f = f16_fma(hge2_one(r, c), 0x58005800u, f);                       // R  +128 (256)
+    f = f16_fma(hge2_one(br, c), 0x5C005C00u, f);                      // BR +256 (512)
+    f |= hge2_mask(b, c) & 0x04000400u;                                // B  bit 10
+    f |= hge2_mask(bl, c) & 0x08000800u;                               // BL bit 11
+    f |= hge2_mask(l, c) & 0x10001000u;                                // L  bit 12
+    return f;
 }
 
 // WINM: how the depth window is tested.  0: integer compare per pixel; 1: both halves of a
@@ -317,9 +335,22 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t stages0 = smem_u32(smem);
     const uint32_t hist0 = stages0 + kGroupOff + group * kGroupBytes;
     const uint32_t staging = FRAME ? hist0 : hist0 + kHistBytes;
-    const uint32_t exc_cnt = staging + kDescBytes;  // U8: the crop's exception count (slack)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     const uint32_t bar_id = 1 + group;
+    // SUB (crop stacks): the two cell-row halves of a group -- warps 4 sub .. 4 sub + 3, one warp
+    // per SMSP, whose counters are the cell-row group g = sub -- run the rows, the epilogue and
+    // the store of their half of the descriptor row with 128-thread barriers of their own (the
+    // scheduler's warp priorities no longer stall a whole 8-warp group at every barrier); the
+    // stage is refilled by whichever half releases it second.  FRAME keeps 8-warp barriers.
+    constexpr bool SUB = !FRAME;
+    const int sub = warp >> 2, stid = gtid & 127;
+    const uint32_t sub_bar = 4 + 2 * group + sub;  // named barriers 4..9 (0: CTA, 1..3: groups)
+    const bool leader = SUB ? stid == 0 : gtid == 0;  // owns a bulk-store group
+    // group slack words after the staging (crop stacks): [0..1] exception counts and [2..3]
+    // halves-done counts by crop parity (U8)
+    const uint32_t slack = staging + kDescBytes;
+    // per-stage release counts (after the stage barriers): two halves release each position
+    const uint32_t rel0 = smem_u32(smem + kBarOff + kStages * 8);
 
     // crop positions of this CTA: position i -> crop blockIdx.x + i * gridDim.x
     const int n_pos = (n_rois > (int)blockIdx.x) ? (n_rois - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -345,6 +376,15 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             mbar_arrive(&bars[s]);
         }
     };
+    // L2 prefetch of position i's boxes (crop stacks): the stage ring holds one crop per group,
+    // so the load of position i + 3, issued when position i releases its stage, would wait for
+    // HBM while the group idles; prefetching position i + 6 at the same moment lets that load
+    // hit L2 (more bytes in flight per SM than the shared-memory ring can hold)
+    auto prefetch = [&](int i, int32_t x, int32_t y, int32_t img) {
+        if (FRAME || i >= n_pos) return;
+        if (HAS_DEPTH) tma_prefetch_l2_3d(&depth_map, x, y, img);
+        if (!DEPTH_SRC) tma_prefetch_l2_3d(&grey_map, x, y, img);
+    };
 
     // the dependent launch (the scorer) may be scheduled now: its CTAs take SMs as these
     // CTAs exit, run their prologue, and wait for this grid's completion
@@ -357,17 +397,23 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     if (tid < 256) smem[kPlainLutOff + tid] = kUniformLutDev.v[tid];
     for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
-    if (U8 && gtid == 0) st_shared_u32(exc_cnt, 0u);
+    if (SUB && gtid < 4) st_shared_u32(slack + 4 * gtid, 0u);
+    if (SUB && tid < kStages) st_shared_u32(rel0 + 4 * tid, 0u);
     if (tid == 0) {
         // the host placed the LUT from the device's reserved shared memory size; a mismatch
         // would misaddress every lookup, so it stops the kernel (LBP_E_CUDA) instead
-        if ((smem_u32(smem + kLutOff) & 0xFFFFu) != 0x6400u) __trap();
+        if ((smem_u32(smem + kLutOff) & 0xFFFFu) != kLutMod) __trap();
         for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
         prefetch_tensormap(&grey_map);
         if (HAS_DEPTH) prefetch_tensormap(&depth_map);
         for (int i = 0; i < kStages; ++i)
             if (i < n_pos) issue(i, rois[crop_of(i)]);
+        for (int i = kStages; i < 2 * kStages; ++i)
+            if (i < n_pos) {
+                const lbp_roi_t r = rois[crop_of(i)];
+                prefetch(i, r.x, r.y, r.img);
+            }
     }
     __syncthreads();
 
@@ -388,10 +434,10 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // WINM 1
     const uint32_t mid2 = ((2 * win.lo + win.span) / 2) * 0x10001u;                 // WINM 2
     const uint32_t half2 = (win.span / 2) * 0x10001u;
-    // LUT address of an offset half t: lutb | t (the LUT sits at 0x6400 mod 2^16)
-    const uint32_t lutb = opaque(smem_u32(smem + kLutOff) - 0x6400u);
-    const uint32_t base2 = opaque((0x6400u + 4u * lane) * 0x10001u);  // 1024.0 + 4 lane
-    const uint32_t top2 = opaque((0x6400u + 4u * lane + 899u) * 0x10001u);  // + TL..BR
+    // LUT address of an offset half t: lutb | t (the LUT sits at 0x6000 mod 2^16)
+    const uint32_t lutb = opaque(smem_u32(smem + kLutOff) - kLutMod);
+    const uint32_t base2 = opaque((kLutMod + 4u * lane) * 0x10001u);  // 512.0 + 2 lane
+    const uint32_t top2 = opaque((kLutMod + 4u * lane + 899u) * 0x10001u);  // + TL..BR
     const int i0 = (warp * (kTile - 2)) / 8;                   // first interior row of cell row
     const int nrows = ((warp + 1) * (kTile - 2)) / 8 - i0;     // 15 or 16
 
@@ -410,16 +456,30 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int32_t n = crop_of(i);
         const lbp_roi_t roi = roi_next;
         if (i + kGroups < n_pos) roi_next = rois[crop_of(i + kGroups)];
+        // position i + kStages: its TMA is issued when this crop releases stage s
+        lbp_roi_t roi_fill{};
+        if constexpr (kStages == kGroups) roi_fill = roi_next;
+        else if (i + kStages < n_pos) roi_fill = rois[crop_of(i + kStages)];
+        // the box of position i + 6, prefetched to L2 when this crop releases its stage (read
+        // now by the releasing threads, used after the rows)
+        int32_t pf_x = 0, pf_y = 0, pf_img = 0;
+        if (!FRAME && (SUB ? stid == 0 : gtid == 0) && i + 2 * kStages < n_pos) {
+            const lbp_roi_t& rp = rois[crop_of(i + 2 * kStages)];
+            pf_x = rp.x; pf_y = rp.y; pf_img = rp.img;
+        }
         const int s = i % kStages;
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
+        const uint32_t par = (uint32_t)(i / kGroups) & 1u;
+        const uint32_t exc_cnt = slack + 4 * par;  // U8: the crop's exception count
         if (!is_fast(roi)) {
             if (gtid == 0) {  // stage s was never filled: release it at once
-                issue(i + kStages, roi_next);  // (position i + 3 = this group's next)
+                issue(i + kStages, roi_fill);
+                prefetch(i + 2 * kStages, pf_x, pf_y, pf_img);
             }
             if constexpr (U8) {
                 // counts stay in the group's counters (KEEP; 64 cells x 59 bins fit one chunk),
                 // then the row is staged as u8 + exceptions like the fast path's
-                if (gtid == 0) bulk_wait_read_all();        // previous row left the staging
+                if (leader) bulk_wait_read_all();           // previous rows left the staging
                 named_barrier_sync(bar_id, kGroupThreads);
                 uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (hist0 - stages0));
                 uint16_t* zrow = reinterpret_cast<uint16_t*>(smem + (staging - stages0));
@@ -441,9 +501,15 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                     bulk_store_s2g(u8o.packed + (int64_t)n * u8o.pitch, staging, kDescBytes / 2);
                     u8o.exc_n[n] = (int32_t)ld_shared_u32(exc_cnt);
                     st_shared_u32(exc_cnt, 0u);
+                    // the other half's leader does not wait on this thread's bulk group
+                    bulk_wait_read_all();
                 }
                 pending = n;
                 continue;
+            }
+            if constexpr (SUB) {  // both halves past the previous crop (counters zero)
+                if (leader) bulk_wait_read_all();
+                named_barrier_sync(bar_id, kGroupThreads);
             }
             if (DEPTH_SRC)
                 extract_roi_generic<kBins, kGroupThreads>(
@@ -573,6 +639,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
 #pragma unroll
                 for (int k = 0; k < 4; ++k) val[k] = mult[k];
             }
+            // (an IMAD.HI form of the high halves, to move them to the FMA pipe, needs a register
+            // for 2^16 and costs more moves than it saves at 80 registers: LEA.HI stays)
             const uint32_t la[4] = {lutb | (t0 & 0xFFFFu), __umulhi(t0, 0x10000u) + lutb,
                                     lutb | (t1 & 0xFFFFu), __umulhi(t1, 0x10000u) + lutb};
             Pend p;
@@ -613,11 +681,21 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             if (j == 15) flush(pend);
         }
 
-        if (gtid == 0) bulk_wait_read_all();        // previous descriptor left the staging
-        named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
-        if (gtid == 0 && last) {
-            issue(i + kStages, roi_next);
-            if (roi_status) roi_status[n] = LBP_OK;
+        if (leader) bulk_wait_read_all();  // this thread's previous store left the staging
+        if constexpr (SUB) {
+            named_barrier_sync(sub_bar, 128);  // A: this half's counters complete, its rows read
+            // the second half to release stage s refills it with position i + 3
+            if (stid == 0 && last && (atom_shared_add(rel0 + 4 * s, 1u) & 1u)) {
+                issue(i + kStages, roi_fill);
+                prefetch(i + 2 * kStages, pf_x, pf_y, pf_img);
+                if (roi_status) roi_status[n] = LBP_OK;
+            }
+        } else {
+            named_barrier_sync(bar_id, kGroupThreads);  // A: stage read, counters complete
+            if (gtid == 0 && last) {
+                issue(i + kStages, roi_fill);
+                if (roi_status) roi_status[n] = LBP_OK;
+            }
         }
         // ---- epilogue: quad q = (g, bin, cx) holds the 4 lane columns of cells (4g + j, cx),
         // j = byte.  Byte-transpose the 4 words and sum each byte column with IDP4A.
@@ -682,52 +760,79 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             }
             named_barrier_sync(bar_id, kGroupThreads);  // counters zero for the next crop
         } else {
-            for (int q = gtid; q < 2 * kBinsAlloc * 8; q += kGroupThreads) {
-                const uint32_t qa = hist0 + q * 16;
-                const int g = q / (kBinsAlloc * 8), rem = q - g * (kBinsAlloc * 8);
-                const int bin = rem >> 3, cx = rem & 7;
-                if (bin == kBins) {  // dummy bin (masked-out pixels): only re-zeroed
+            // thread -> quads: cx = gtid & 7, bin = bp + 16 k (bp = (gtid >> 3) & 15, k = 0..3),
+            // g = gtid >> 7, so the counter quad and the staged entries are affine in k ([R +
+            // imm] addressing, no per-quad index math) and each quarter-warp reads 128
+            // contiguous bytes (8 cx of one bin).  Bins 60..63 do not exist (k = 3, bp >= 12);
+            // bin 59 is the dummy (masked-out pixels): only re-zeroed.
+            static_assert(kGroupThreads == 2 * 8 * 16 && kBins > 48 && kBins <= 60, "epilogue map");
+            const int ecx = gtid & 7, ebp = (gtid >> 3) & 15, eg = gtid >> 7;
+            const uint32_t qbase = hist0 + (uint32_t)(((eg * kBinsAlloc + ebp) * 8 + ecx) * 16);
+            const uint32_t dbase = (uint32_t)(((4 * eg) * 8 + ecx) * kBins + ebp);
+            uint4 cq[4];
+            uint32_t any = 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (k == 3 && ebp >= 12) break;
+                const uint32_t qa = qbase + k * (16 * 128);
+                if (k == 3 && ebp == kBins - 48) {
                     st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
-                    continue;
+                    break;
                 }
                 const uint4 c = counts(qa);
                 st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
                 if constexpr (U8) {
-                    const uint32_t d0 = (uint32_t)(((4 * g) * 8 + cx) * kBins + bin);
                     constexpr uint32_t kRowE = 8 * kBins;  // next cell row
+                    const uint32_t d0 = dbase + 16 * k;
                     put_u8(staging, d0, c.x);
                     put_u8(staging, d0 + kRowE, c.y);
                     put_u8(staging, d0 + 2 * kRowE, c.z);
                     put_u8(staging, d0 + 3 * kRowE, c.w);
-                    if ((c.x | c.y | c.z | c.w) > 255u) {  // one test per quad
-                        record_u8(u8o, n, exc_cnt, d0, c.x);
-                        record_u8(u8o, n, exc_cnt, d0 + kRowE, c.y);
-                        record_u8(u8o, n, exc_cnt, d0 + 2 * kRowE, c.z);
-                        record_u8(u8o, n, exc_cnt, d0 + 3 * kRowE, c.w);
-                    }
+                    cq[k] = c;
+                    any |= c.x | c.y | c.z | c.w;
                 } else {
-                    put(g, bin, cx, c);
+                    put(eg, ebp + 16 * k, ecx, c);
                 }
             }
             if constexpr (U8) {
-                fence_proxy_async_smem();                   // staging writes -> async proxy
-                named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-                if (gtid == 0) {
-                    bulk_store_s2g(u8o.packed + (int64_t)n * u8o.pitch, staging, kDescBytes / 2);
-                    u8o.exc_n[n] = (int32_t)ld_shared_u32(exc_cnt);
-                    st_shared_u32(exc_cnt, 0u);
+                if (any > 255u) {  // rare: a 16x16 cell whose 256 pixels share a bin
+                    constexpr uint32_t kRowE = 8 * kBins;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (k == 3 && ebp >= kBins - 48) break;
+                        const uint32_t d0 = dbase + 16 * k;
+                        record_u8(u8o, n, exc_cnt, d0, cq[k].x);
+                        record_u8(u8o, n, exc_cnt, d0 + kRowE, cq[k].y);
+                        record_u8(u8o, n, exc_cnt, d0 + 2 * kRowE, cq[k].z);
+                        record_u8(u8o, n, exc_cnt, d0 + 3 * kRowE, cq[k].w);
+                    }
+                }
+            }
+            // this half's part of the row: cell rows 4 sub .. 4 sub + 3 (contiguous)
+            constexpr uint32_t kHalfB = kDescBytes / 2;  // u16 bytes (the u8 half: kHalfB / 2)
+            if constexpr (U8) {
+                fence_proxy_async_smem();          // staging writes -> async proxy
+                named_barrier_sync(sub_bar, 128);  // B: this half's counters zero, staged
+                if (stid == 0) {
+                    bulk_store_s2g(u8o.packed + (int64_t)n * u8o.pitch + sub * (kHalfB / 2),
+                                   staging + sub * (kHalfB / 2), kHalfB / 2);
+                    // the second half done: the crop's exception count is final
+                    if (atom_shared_add(slack + 8 + 4 * par, 1u) & 1u)
+                        u8o.exc_n[n] = (int32_t)atom_shared_exch(exc_cnt, 0u);
                 }
             } else if constexpr (GATHER) {
-                // every thread forwards 16-B chunks of the staged row to every destination
-                // (the staging is rewritten only after the next crop's barrier A, which every
-                // thread reaches after its loads here)
-                named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-                gather_row_from_smem<kGroupThreads>(gd, n, staging, kDescBytes / 16, gtid);
+                // every thread of the half forwards 16-B chunks of its part of the staged row
+                // to every destination (rewritten only after this half's next barrier A, which
+                // its threads reach after their loads here); half 1 also writes the padding
+                named_barrier_sync(sub_bar, 128);  // B: this half's counters zero, staged
+                gather_row_from_smem<128>(gd, n, staging, sub * (kHalfB / 16),
+                                          sub ? -1 : (int)(kHalfB / 16), kDescBytes / 16, stid);
                 if (gtid == 0) gather_label(gd, n, glabels);
             } else {
-                fence_proxy_async_smem();                   // staging writes -> async proxy
-                named_barrier_sync(bar_id, kGroupThreads);  // B: counters zero, staging complete
-                if (gtid == 0) bulk_store_s2g(out_row, staging, kDescBytes);
+                fence_proxy_async_smem();          // staging writes -> async proxy
+                named_barrier_sync(sub_bar, 128);  // B: this half's counters zero, staged
+                if (stid == 0)
+                    bulk_store_s2g(out_row + sub * (kHalfB / 2), staging + sub * kHalfB, kHalfB);
             }
         }
         };
@@ -739,12 +844,12 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         pending = n;
     }
-    if (gtid == 0 && pending >= 0) bulk_wait_all();
+    if (leader && pending >= 0) bulk_wait_all();
     if constexpr (GATHER) __threadfence_system();  // before the caller's cross-rank barrier
 }
 
 // Offset of the lane-banked LUT in the dynamic shared memory: the first offset >= lut_min
-// whose shared-window address is 0x6400 mod 2^16.  Dynamic shared memory starts at the
+// whose shared-window address is l59::kLutMod (0x6000) mod 2^16.  Dynamic shared memory starts at the
 // device's reserved shared memory per block (these kernels have no static shared memory),
 // and the kernel rounds its base up to 128 B.  False if the layout does not fit.
 inline bool lut_placement(int lut_min, int tail_bytes, int* lut_off, int* smem_bytes) {
@@ -758,7 +863,7 @@ inline bool lut_placement(int lut_min, int tail_bytes, int* lut_off, int* smem_b
     }();
     if (reserved < 0) return false;
     const int base = (reserved + 127) & ~127;
-    const int off = lut_min + (((0x6400 - base - lut_min) % 65536) + 65536) % 65536;
+    const int off = lut_min + ((((int)l59::kLutMod - base - lut_min) % 65536) + 65536) % 65536;
     *lut_off = off;
     *smem_bytes = off + tail_bytes;
     return *smem_bytes <= 227 * 1024;
