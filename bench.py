@@ -107,10 +107,12 @@ def parse():
     p.add_argument("--compact", action="store_true",
                    help="config5: all-gather u8 descriptors + exception lists (serial; "
                         "lbp_desc_pack_u8 / lbp_desc_unpack_u8), and time pack/unpack")
-    p.add_argument("--format", default="u8", choices=["u8", "u16"],
+    p.add_argument("--format", default="auto", choices=["auto", "u8", "u16"],
                    help="descriptor between extraction and scoring (grey source): u8 = the "
                         "compact form (lbp_extract_u8 + svm_score_u8: u8 rows + records of the "
-                        "entries above 255), u16 = lbp_fused_extract + svm_score")
+                        "entries above 255), u16 = lbp_fused_extract + svm_score; auto = the "
+                        "faster step for the class count: u16 up to 124 classes (one TMEM "
+                        "pass of the fp16 scorer: config3), u8 above (config4)")
     p.add_argument("--fused", action="store_true",
                    help="config5: the fused database build (SURVEY §8e way 2): the extraction "
                         "epilogue stores every row into every rank's symmetric-memory copy "
@@ -374,6 +376,8 @@ def main():
     n, H, Wd, cx, cy, bins, C, desc_txt = WORKLOADS[args.workload]
     n = args.crops or n
     bins = args.bins or bins
+    if args.format == "auto":
+        args.format = "u16" if C <= 124 else "u8"
     source = SOURCES[args.source]
     if source != 0 and args.no_depth:
         raise SystemExit("--source depth/fused needs the depth plane")

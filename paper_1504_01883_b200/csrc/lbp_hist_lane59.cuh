@@ -472,7 +472,12 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const uint32_t par = (uint32_t)(i / kGroups) & 1u;
         const uint32_t exc_cnt = slack + 4 * par;  // U8: the crop's exception count
         if (!is_fast(roi)) {
-            if (gtid == 0) {  // stage s was never filled: release it at once
+            // stage s was never filled: release it at once -- but only once every thread of
+            // the group has passed its wait on this position's phase (a plain arrive for
+            // position i + 3 completes the NEXT phase at once, and a thread still polling the
+            // parity of this phase would then wait for the phase after that: deadlock)
+            named_barrier_sync(bar_id, kGroupThreads);
+            if (gtid == 0) {
                 issue(i + kStages, roi_fill);
                 prefetch(i + 2 * kStages, pf_x, pf_y, pf_img);
             }

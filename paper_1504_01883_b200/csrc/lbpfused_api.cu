@@ -11,6 +11,7 @@
 #include "tma_util.cuh"
 #include "lbp_hist_lane59.cuh"
 #include "lbp_hist_lane256.cuh"
+#include "lbp_hist_tile.cuh"
 #include "lbp_resize.cuh"
 #include "lbp_recognize.cuh"
 #include "svm_fp64.cuh"
@@ -100,6 +101,22 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
     // box so that 128x128 ROIs at any column take the TMA path (crop stacks keep the
     // 128-wide boxes).
     const bool frame = geom.width >= l59::Layout<true>::kGreyW;
+    // crop stacks of 64x64 or 200x200 images (8x8 cells, 59 bins, grey codes): the tile
+    // variant of the TMA kernel (two 64-px crops per warp row / four 200-px quadrant tiles)
+    if (!depth_source && !small_batch && bins == 59 && cells_x == 8 && cells_y == 8 &&
+        geom.width == geom.height && (geom.width == 64 || geom.width == 200) &&
+        tile_path_applicable(geom, grey, depth) &&
+        // whole rows leave the 64-px tiles by bulk copies (16 B), the 200-px quadrants' runs
+        // of 4 cells by 8-B stores
+        (reinterpret_cast<uintptr_t>(desc) & 15) == 0 && ((desc_stride * 2) & 15) == 0) {
+        const cudaError_t e =
+            geom.width == 64
+                ? launch_lbp_hist_tile<64>(grey, depth, geom, rois, n_rois, win, desc, desc_stride,
+                                           roi_status, num_sms(), stream)
+                : launch_lbp_hist_tile<200>(grey, depth, geom, rois, n_rois, win, desc,
+                                            desc_stride, roi_status, num_sms(), stream);
+        if (e != cudaErrorNotSupported) return launch_status(e);
+    }
     if (!depth_source && !small_batch) {
         // Fast path (8x8 cells, 16-B aligned rows): one TMA-staged persistent kernel; ROIs
         // that are not fully-inside 128x128 boxes take the generic code path inside it.

@@ -110,6 +110,10 @@ __device__ __forceinline__ uint2 ld_shared_u32x2(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ void st_shared_u32x2(uint32_t addr, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
+}
+
 __device__ __forceinline__ uint4 ld_shared_u32x4(uint32_t addr) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"

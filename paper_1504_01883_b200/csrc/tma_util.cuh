@@ -31,6 +31,18 @@ inline bool fast_path_applicable(const lbp_images_t& g, const uint8_t* grey, con
     return true;
 }
 
+// The tile kernels (lbp_hist_tile.cuh): TMA-legal image stacks of any size (16-B aligned
+// bases, pitches and image strides, strides < 2^40 bytes).
+inline bool tile_path_applicable(const lbp_images_t& g, const uint8_t* grey, const uint16_t* depth) {
+    if (!grey || (reinterpret_cast<uintptr_t>(grey) & 15) || (g.grey_pitch & 15) ||
+        (g.grey_img_stride & 15) || g.grey_img_stride >= (int64_t(1) << 39))
+        return false;
+    if (depth && ((reinterpret_cast<uintptr_t>(depth) & 15) || ((g.depth_pitch * 2) & 15) ||
+                  ((g.depth_img_stride * 2) & 15) || g.depth_img_stride >= (int64_t(1) << 38)))
+        return false;
+    return true;
+}
+
 inline PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     // resolved once (thread-safe static init); immutable afterwards
     static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() {

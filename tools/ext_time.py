@@ -3,7 +3,7 @@ around K back-to-back launches on one stream (no other kernels in between), inpu
 than L2.  Prints us per launch and the HBM fraction on the algorithmic bytes (grey + depth
 read + the descriptor written) against MEASURED_PEAKS.json.
 argv: [crops=16384] [K=50] [variants=u8,u16,fused,depth] [l2: ROIs cycle over 16 images, so
-the inputs are L2-resident -- the kernel's compute-only time]"""
+the inputs are L2-resident -- the kernel's compute-only time; hbm: not] [crop size=128]"""
 import json
 import os
 import sys
@@ -18,8 +18,13 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 variants = (sys.argv[3] if len(sys.argv) > 3 else "u8,u16,fused,depth").split(",")
 dev = torch.device('cuda', 0)
-H = 128
+H = int(sys.argv[5]) if len(sys.argv) > 5 else 128
 g, d = synthgen.gpu_face_crops(n, H, H, seed=1, device=dev)
+if H % 16:  # TMA needs 16-B multiple row pitches: pad the grey rows (200 -> 208 B)
+    P = (H + 15) // 16 * 16
+    gb = torch.zeros((n, H, P), dtype=torch.uint8, device=dev)
+    gb[:, :, :H] = g
+    g = gb[:, :, :H]
 r = torch.from_numpy(synthgen.full_rois(n, H, H)).to(dev)
 if len(sys.argv) > 4 and sys.argv[4] == "l2":
     r[:, 0] = torch.arange(n, device=dev, dtype=torch.int32) % 16
