@@ -73,7 +73,9 @@ struct Geo {
     static constexpr int kGroupBytes = kHistBytes + up(kStageOut, 128) + 128;
     static constexpr int kGroupOff = kStages * kStageBytes;
     static constexpr int kLutMin = up(kGroupOff + kGroupsT * kGroupBytes, 256);
-    static constexpr int kTailBytes = l59::kLutBytes + 256 + kStages * 8 + 128;
+    // LUT, plain LUT, stage barriers, the lane tables (TileTab, copied to shared memory: the
+    // lane-indexed reads of the kernel-parameter copy serialise in the constant cache), slack
+    static constexpr int kTailBytes = l59::kLutBytes + 256 + kStages * 8 + 512 + 128;
     // rows of one warp: a cell row (kQ = 1) or half of one (kQ = 2)
     static constexpr int kMaxCellRows = (kInt + 7) / 8;
     static constexpr int kMaxRows = (kMaxCellRows + kQ - 1) / kQ;
@@ -117,6 +119,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t roi_slot = staging + up(G::kStageOut, 128);
     const int kLutOff = lut_off, kPlainLutOff = lut_off + l59::kLutBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPlainLutOff + 256);
+    const uint32_t tab_s = smem_u32(smem + kPlainLutOff + 256 + kStages * 8);  // TileTab copy
     const uint32_t bar_id = 1 + group;
 
     // tiles: crop pairs (kP = 2: crops 2t, 2t+1) or quadrants (kQ = 2: crop t / 4, q = t % 4)
@@ -183,6 +186,9 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         smem[kLutOff + i] = code < 256 ? kUniformLutDev.v[code] : (uint8_t)kBins;
     }
     if (tid < 256) smem[kPlainLutOff + tid] = kUniformLutDev.v[tid];
+    static_assert(sizeof(TileTab) % 4 == 0 && sizeof(TileTab) <= 512, "table copy");
+    if (tid < (int)sizeof(TileTab) / 4)
+        st_shared_u32(tab_s + 4 * tid, reinterpret_cast<const uint32_t*>(&tab)[tid]);
     for (int i = gtid; i < G::kHistBytes / 16; i += kGT)
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
     if (tid == 0) {
@@ -284,11 +290,15 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         // ---- per-tile lane setup: counter slots of the lane's 4 pixels (quadrant column qx)
         uint32_t colb[4], mult[4];
+        // the lane's 4 slots (TileTab::slot[qx][lane][0..3]) in one conflict-free LDS
+        const uint32_t slots4 = ld_shared_u32(tab_s + (uint32_t)(qx * 128 + lane * 4));
         const bool crop_ok = p_lane == 0 ? tr.valid[0] : tr.valid[kP - 1];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t sl = tab.slot[qx][lane][k];
-            colb[k] = hist_g + (sl & 31u) * 4u;
+            const uint32_t sl = (slots4 >> (8 * k)) & 0xFFu;
+            // uncounted pixels add 0 to their own lane's word (a shared dummy word would make
+            // the idle lanes' atomics collide)
+            colb[k] = hist_g + (sl == 0xFFu ? (uint32_t)lane : sl) * 4u;
             mult[k] = (sl != 0xFFu && crop_ok && !none) ? byte_mult : 0u;
         }
         // rows: interior rows [a, b) of the cell row, this warp's half of them
@@ -423,7 +433,8 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                             st_shared_u32x4(row + l * 4, make_uint4(0, 0, 0, 0));
                     continue;
                 }
-                const int lo = tab.lo[qx][cc], nl = tab.hi[qx][cc] - lo;
+                const int lo = (int)ld_shared_u8(tab_s + offsetof(TileTab, lo) + qx * 8 + cc);
+                const int nl = (int)ld_shared_u8(tab_s + offsetof(TileTab, hi) + qx * 8 + cc) - lo;
                 int l = lo + bin % nl;
                 uint32_t a02 = 0, a13 = 0;
                 for (int j = 0; j < nl; ++j) {
@@ -476,8 +487,8 @@ namespace tile {
 // the lane tables of crop size T (TileTab): pixel (lane, k) of tile column qx is crop column
 // x = bx(qx) + 4 (lane % lanes_per_crop) + k; it is counted iff x is an interior column of the
 // tile (halo < x <= halo + span), into its own lane's word when its cell is the lane's home
-// cell (the cell of the lane's first counted pixel), else into the neighbour lane whose home
-// it is.  False when the cells are too narrow for that (never for the instantiated T).
+// cell (the cell of most of the lane's counted pixels), else into the neighbour lane whose
+// home it is.  False when the cells are too narrow for that (never for the instantiated T).
 template <int T>
 inline bool build_tab(TileTab* tab) {
     using G = Geo<T>;
@@ -488,10 +499,19 @@ inline bool build_tab(TileTab* tab) {
         auto cell = [&](int x) { return (((x - 1) + 1) * 8 - 1) / G::kInt - qx * G::kCT; };
         for (int l = 0; l < 32; ++l) {
             const int li = l % G::kLanesPerCrop;
+            // home = the cell holding most of the lane's counted pixels (ties: the lower):
+            // the fewest spill pixels, each of which costs a 2-way conflict in its atomic
             home[l] = -1;
-            for (int k = 0; k < 4 && home[l] < 0; ++k) {
+            int best = 0;
+            for (int k = 0; k < 4; ++k) {
                 const int x = G::bx(qx) + 4 * li + k;
-                if (x >= lo_x && x <= hi_x) home[l] = cell(x);
+                if (x < lo_x || x > hi_x) continue;
+                int cnt = 0;
+                for (int k2 = 0; k2 < 4; ++k2) {
+                    const int x2 = G::bx(qx) + 4 * li + k2;
+                    cnt += (x2 >= lo_x && x2 <= hi_x && cell(x2) == cell(x));
+                }
+                if (cnt > best) { best = cnt; home[l] = cell(x); }
             }
         }
         for (int c = 0; c < G::kCT; ++c) {
