@@ -47,6 +47,13 @@ WORKLOADS = {
     "config2": (4, 128, 128, 8, 8, 59, 10,
                 "BASELINE configs[1]: 640x480 Kinect-shaped grey+depth frame stream, 4 tracked "
                 "faces (128x128 ROIs moving <= 20 px/frame), 10 identities"),
+    # the tile variant of the TMA kernel (csrc/lbp_hist_tile.cuh): other crop sizes, batched
+    "tile64": (16384, 64, 64, 8, 8, 59, 100,
+               "16384 x 64x64 grey+depth crops (the crop size of BASELINE configs[0], batched), "
+               "8x8 cells x 59 uniform bins, 100-identity one-vs-all linear SVM"),
+    "tile200": (16384, 200, 200, 8, 8, 59, 100,
+                "16384 x 200x200 grey+depth crops (the paper's resized face, P:154; grey rows "
+                "padded to 208 B for TMA), 8x8 cells x 59 uniform bins, 100-identity SVM"),
     # crops = TOTAL database size (strong scaling: sharded over the ranks)
     "config5": (262144, 128, 128, 8, 8, 59, 0,
                 "BASELINE configs[4]: online database build, 256k 128x128 crops sharded over the "
@@ -302,6 +309,19 @@ def workload_config(args, n, H, W, cx, cy, bins, C, desc_txt):
                   "inputs L2-resident (latency config)"}
 
 
+def pad_rows(torch, t):
+    """A view of t ([n][H][W]) in a buffer whose rows are a multiple of 16 B (TMA strides):
+    200-px grey rows -> 208 B.  t itself when already aligned."""
+    row = t.shape[-1] * t.element_size()
+    if row % 16 == 0:
+        return t
+    P = (row + 15) // 16 * 16 // t.element_size()
+    buf = torch.zeros((*t.shape[:-1], P), dtype=t.dtype, device=t.device,
+                      pin_memory=(t.device.type == "cpu" and torch.cuda.is_available()))
+    buf[..., :t.shape[-1]] = t
+    return buf[..., :t.shape[-1]]
+
+
 def compact_format(args) -> bool:
     """The recognition step runs on the compact descriptor (grey source only)."""
     return getattr(args, "format", "u16") == "u8" and getattr(args, "source", "grey") == "grey"
@@ -386,6 +406,7 @@ def main():
 
     grey, depth = synthgen.gpu_face_crops(n, H, Wd, seed=args.seed, first_index=first,
                                           dist=args.dist, device=dev)
+    grey = pad_rows(torch, grey)
     if args.no_depth:
         depth = None
     rois = torch.from_numpy(synthgen.full_rois(n, H, Wd)).to(dev)
@@ -956,7 +977,9 @@ def run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins,
     extraction + SVM, D2H of labels and top scores, every step."""
     import synthgen
     steps = args.e2e_steps or min(args.steps, 10)
-    g_h = grey.cpu().pin_memory()
+    g_h = pad_rows(torch, grey.cpu()) if grey.stride(1) != grey.shape[2] else grey.cpu().pin_memory()
+    if not g_h.is_pinned():
+        g_h = g_h.pin_memory()
     d_h = depth.cpu().pin_memory() if depth is not None else None
     r_h = torch.from_numpy(synthgen.full_rois(n, H, Wd)).pin_memory()
     lab_h = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -985,7 +1008,9 @@ def run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins,
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
-    h2d = g_h.numel() + (d_h.numel() * 2 if d_h is not None else 0) + r_h.numel() * 4
+    # bytes the call copies: whole images including any row padding
+    h2d = (g_h.untyped_storage().nbytes() +
+           (d_h.untyped_storage().nbytes() if d_h is not None else 0) + r_h.numel() * 4)
     return {"value": n * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(n * 8),
             "api": "lbp_recognize_host (C ABI, pinned host buffers)"}
@@ -999,7 +1024,7 @@ def run_cpu_leg(args, torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy
     threads = len(os.sched_getaffinity(0))
     n = grey.shape[0]
     m = min(n, 4096)
-    g = grey[:m].cpu().numpy()
+    g = np.ascontiguousarray(grey[:m].cpu().numpy())
     d = depth[:m].cpu().view(torch.int16).numpy().view(np.uint16) if depth is not None else None
     r = rois[:m].cpu().numpy()
     rate, done, secs, passes, odesc, olab = oracle_rate(g, d, r, W_np, b_np, cx, cy, bins,
@@ -1090,7 +1115,7 @@ def rank_gate(torch, grey, depth, rois, desc, labels, W_np, b_np, cx, cy, bins, 
     rank's first m crops."""
     import oracle
     m = min(m, grey.shape[0])
-    g = grey[:m].cpu().numpy()
+    g = np.ascontiguousarray(grey[:m].cpu().numpy())
     d = depth[:m].cpu().view(torch.int16).numpy().view(np.uint16) if depth is not None else None
     r = rois[:m].cpu().numpy()
     odesc = oracle.lbp_extract(g, d, r, DMIN, DMAX, cx, cy, bins, source=source)
