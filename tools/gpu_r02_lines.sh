@@ -4,10 +4,12 @@
 #   /usr/local/graft/bin/gpurun --timeout 3000 -- bash tools/gpu_r02_lines.sh TAG
 cd "$GRAFT_REPO_ROOT" || exit 1
 T=${1:-r02_lines}
+PART=${2:-lines}   # lines | ncu1 | ncu2  (one gpurun call each: gpurun_out/ comes back <= 64 MiB)
 O=gpurun_out/$T
 mkdir -p $O/lines $O/ncu
 python __graft_entry__.py build > $O/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
+if [ "$PART" = lines ]; then
 run() {  # name, args...
   local name=$1; shift
   timeout 600 python bench.py "$@" > $O/lines/$name.json 2> $O/lines/$name.err
@@ -30,15 +32,19 @@ run reference --impl reference --steps 3 --warmup 1
 # launch list (cold, serialised) of the headline step
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ncu/launches_config3.csv \
   python bench.py --steps 3 --warmup 3 --skip-cpu --e2e-steps 1 > $O/ncu/launches_config3.log 2>&1; echo "launches rc=$?"
+fi
 full() {  # name, kernel regex, bench args...
   local name=$1 k=$2; shift 2
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o $O/ncu/$name \
     python bench.py --steps 3 --warmup 3 --skip-cpu --e2e-steps 1 "$@" > $O/ncu/$name.log 2>&1; echo "ncu $name rc=$?"
 }
+if [ "$PART" = ncu1 ]; then
 full lane59_config3 lbp_hist_lane59
 full svm_gemm_config3 svm_gemm_kernel
 full lane59_fused lbp_hist_lane59 --source fused
+fi
+if [ "$PART" = ncu2 ]; then
 full tile64 lbp_hist_tile --workload tile64
 full tile200 lbp_hist_tile --workload tile200
-full lane59_u8 lbp_hist_lane59 --format u8
 full svm_u8_config4 svm_gemm_u8 --workload config4 --crops 16384
+fi
