@@ -9,7 +9,7 @@
 //    crop B's; warp w = cell row w of both.  The shuffles across the 15|16 lane boundary only
 //    feed border pixels, which have no code.
 //  * T > 128 (kQ = 2): one QUADRANT of a crop (4x4 cells): the box of its interior plus the
-//    1-px halo (101 x 101 for T = 200), 2 warps per cell row (upper / lower rows).  A
+//    1-px halo (101 x 101 for T = 200), processed by a 4-warp group (warp = cell row).  A
 //    quadrant's cells are disjoint from the other quadrants', so its 16 cell histograms are
 //    final at the end of the tile: no cross-tile merge.
 // Boxes start 16-B aligned (TMA); a quadrant's box starts at its halo column rounded down to
@@ -25,9 +25,6 @@
 namespace lbpf {
 namespace tile {
 
-constexpr int kGroupsT = 3;
-constexpr int kGroupThreadsT = 256;
-constexpr int kThreadsT = kGroupsT * kGroupThreadsT;
 constexpr int kBins = 59;
 constexpr int kBinsAlloc = 60;  // + the dummy bin of masked-out pixels
 
@@ -43,6 +40,13 @@ struct Geo {
     static constexpr int kP = T <= 64 ? 2 : 1;         // crops side by side in a tile
     static constexpr int kCT = 8 / kQ;                 // cells per tile axis
     static constexpr int kInt = T - 2;                 // interior pixels per axis
+    // one warp per cell row of the tile: 8-warp groups x 3 (64 px), 4-warp groups x 5 (200 px:
+    // a quadrant's 4 cell rows of 24-25 rows each -- twice the rows per warp of two warps per
+    // cell row, half the per-tile head per crop, one warp per SMSP in each group barrier)
+    static constexpr int kWarps = kCT;
+    static constexpr int kGT = kWarps * 32;
+    static constexpr int kGroups = kQ == 2 ? 5 : 3;
+    static constexpr int kThreads = kGroups * kGT;
     static constexpr int kG = kCT / 4 > 0 ? kCT / 4 : 1;  // counter words per (bin, lane)
     // halo column (= crop column of the tile's first interior pixel - 1) and aligned box start
     static constexpr int halo(int q) { return cstart(q * kCT, kInt); }
@@ -61,7 +65,7 @@ struct Geo {
     // one stage per group: a group's positions i, i + 3, ... always reuse ITS stage, so the
     // stage barrier's phases are consumed in order (with more stages than groups a fast group
     // could wait on a phase two ahead, which mbarrier parity cannot tell from the last one)
-    static constexpr int kStages = kGroupsT;
+    static constexpr int kStages = kGroups;
     // staged row pitch (kQ = 1): 16 B more than the row, so the two rows' entries of one cell
     // land in different banks
     static constexpr int kRowPad = 64 * kBins + 8;
@@ -72,13 +76,13 @@ struct Geo {
     // + the ROIs of the tile this group's release will load next (kP x 20 B, cp.async)
     static constexpr int kGroupBytes = kHistBytes + up(kStageOut, 128) + 128;
     static constexpr int kGroupOff = kStages * kStageBytes;
-    static constexpr int kLutMin = up(kGroupOff + kGroupsT * kGroupBytes, 256);
+    static constexpr int kLutMin = up(kGroupOff + kGroups * kGroupBytes, 256);
     // LUT, plain LUT, stage barriers, the lane tables (TileTab, copied to shared memory: the
     // lane-indexed reads of the kernel-parameter copy serialise in the constant cache), slack
     static constexpr int kTailBytes = l59::kLutBytes + 256 + kStages * 8 + 512 + 128;
-    // rows of one warp: a cell row (kQ = 1) or half of one (kQ = 2)
-    static constexpr int kMaxCellRows = (kInt + 7) / 8;
-    static constexpr int kMaxRows = (kMaxCellRows + kQ - 1) / kQ;
+    // rows of one warp: a cell row
+    static constexpr int kMaxRows = (kInt + 7) / 8;
+    static constexpr int kMinRows = kInt / 8;  // every warp has at least these rows
     static constexpr int kLanesPerCrop = 32 / kP;
     static_assert(kNeed <= 4 * kLanesPerCrop, "a tile row fits the lanes");
     static_assert(kLutMin + kTailBytes <= 227 * 1024, "shared memory");
@@ -93,7 +97,7 @@ struct TileTab {
 }  // namespace tile
 
 template <int T, bool HAS_DEPTH, int WINM>
-__global__ void __launch_bounds__(tile::kThreadsT, 1)
+__global__ void __launch_bounds__(tile::Geo<T>::kThreads, 1)
 lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                      const __grid_constant__ CUtensorMap depth_map,
                      const uint8_t* __restrict__ grey, const uint16_t* __restrict__ depth,
@@ -104,7 +108,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     using namespace tile;
     using G = Geo<T>;
     constexpr int kQ = G::kQ, kP = G::kP, kCT = G::kCT, kInt = G::kInt;
-    constexpr int kStages = G::kStages, kGroups = kGroupsT, kGT = kGroupThreadsT;
+    constexpr int kStages = G::kStages, kGroups = G::kGroups, kGT = G::kGT;
     constexpr int kTilesPerCrop = kQ * kQ;
     constexpr int kDim = 64 * kBins;
     extern __shared__ uint8_t smem_raw[];
@@ -181,7 +185,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     };
 
     // ---- one-time setup: LUTs, zero counters, barriers, the first kStages positions
-    for (int i = tid; i < l59::kLutBytes; i += kThreadsT) {
+    for (int i = tid; i < l59::kLutBytes; i += G::kThreads) {
         const int code = (i >> 7) * 4 + (i & 3);
         smem[kLutOff + i] = code < 256 ? kUniformLutDev.v[code] : (uint8_t)kBins;
     }
@@ -210,7 +214,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t top2 = opaque((l59::kLutMod + 4u * lane + 899u) * 0x10001u);
     const int p_lane = lane / G::kLanesPerCrop, l_in = lane % G::kLanesPerCrop;
     // the warp's cell row in the tile and its share of that cell row's interior rows
-    const int cr = kQ == 2 ? warp >> 1 : warp, half = kQ == 2 ? (warp & 1) : 0;
+    const int cr = warp;  // the warp's cell row in the tile
     const uint32_t byte_mult = 1u << (8 * (cr & 3));
     const uint32_t hist_g = hist0 + (uint32_t)((cr >> 2) * kBinsAlloc * 128);
     const bool none = HAS_DEPTH && win.none_valid;
@@ -301,12 +305,10 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
             colb[k] = hist_g + (sl == 0xFFu ? (uint32_t)lane : sl) * 4u;
             mult[k] = (sl != 0xFFu && crop_ok && !none) ? byte_mult : 0u;
         }
-        // rows: interior rows [a, b) of the cell row, this warp's half of them
+        // rows: interior rows [a, b) of the cell row
         const int cy = qy * kCT + cr;
         const int ra = cstart(cy, kInt), rb = cstart(cy + 1, kInt);
-        const int first = kQ == 2 ? (rb - ra) / 2 : (rb - ra);
-        const int i0 = ra + (half ? first : 0);
-        const int nrows = half ? (rb - ra) - first : first;
+        const int i0 = ra, nrows = rb - ra;
         // box row of interior row i: i + 1 - halo(qy); the top neighbour of i0 is box row
         // i0 - halo(qy)
         const int br0 = i0 - G::halo(qy);
@@ -363,14 +365,17 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (HAS_DEPTH) dn = ld_shared_u32x2(d0);
         Pend pend;
 #pragma unroll
+        // straight-line rows; only the last (kMaxRows - kMinRows) test the warp's row count, and
+        // the look-ahead loads are unconditional (a row past the warp's band is read but not
+        // used: still inside the CTA's shared memory)
         for (int j = 0; j < G::kMaxRows; ++j) {
-            if (j == nrows) {  // warp-uniform
-                if (j > 0) flush(pend);
+            if (j >= G::kMinRows && j == nrows) {  // warp-uniform
+                flush(pend);
                 break;
             }
             const uint32_t wc = wn;
             const uint2 dc = dn;
-            if (j + 1 < G::kMaxRows && j + 1 < nrows) {
+            if (j + 1 < G::kMaxRows) {
                 wn = ld_shared_u32(g0 + (j + 3) * G::kGW);
                 if (HAS_DEPTH) dn = ld_shared_u32x2(d0 + (j + 1) * (2 * G::kDW));
             }
@@ -605,7 +610,7 @@ inline cudaError_t launch_lbp_hist_tile(const uint8_t* grey, const uint16_t* dep
     const int64_t n_tiles = G::kP == 2 ? ((int64_t)n_rois + 1) / 2
                                        : (int64_t)n_rois * G::kQ * G::kQ;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n_tiles));
-    kern<<<grid, tile::kThreadsT, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win,
+    kern<<<grid, G::kThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win,
                                                    desc, desc_stride, roi_status, lut_off, tab);
     return cudaGetLastError();
 }
