@@ -79,7 +79,7 @@ struct Geo {
     static constexpr int kLutMin = up(kGroupOff + kGroups * kGroupBytes, 256);
     // LUT, plain LUT, stage barriers, the lane tables (TileTab, copied to shared memory: the
     // lane-indexed reads of the kernel-parameter copy serialise in the constant cache), slack
-    static constexpr int kTailBytes = l59::kLutBytes + 256 + kStages * 8 + 512 + 128;
+    static constexpr int kTailBytes = l59::kLutBytes + 256 + kStages * 8 + 512 + kStages * 4 + 128;
     // rows of one warp: a cell row
     static constexpr int kMaxRows = (kInt + 7) / 8;
     static constexpr int kMinRows = kInt / 8;  // every warp has at least these rows
@@ -124,6 +124,14 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     const int kLutOff = lut_off, kPlainLutOff = lut_off + l59::kLutBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPlainLutOff + 256);
     const uint32_t tab_s = smem_u32(smem + kPlainLutOff + 256 + kStages * 8);  // TileTab copy
+    // 64 px (kQ = 1): the two 4-warp halves of a group (cell rows 0-3 / 4-7 = the counter
+    // words g = 0 / 1, one warp per SMSP) sync among themselves and store their half of both
+    // rows; the stage is refilled by the half that releases it second (per-stage counter)
+    constexpr bool SUB = kQ == 1;
+    const int sub = warp >> 2, stid = gtid & 127;
+    const uint32_t sub_bar = 1 + kGroups + 2 * group + sub;  // after the group barriers
+    const bool leader = SUB ? stid == 0 : gtid == 0;
+    const uint32_t rel0 = tab_s + 512;  // per-stage release counts
     const uint32_t bar_id = 1 + group;
 
     // tiles: crop pairs (kP = 2: crops 2t, 2t+1) or quadrants (kQ = 2: crop t / 4, q = t % 4)
@@ -193,6 +201,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     static_assert(sizeof(TileTab) % 4 == 0 && sizeof(TileTab) <= 512, "table copy");
     if (tid < (int)sizeof(TileTab) / 4)
         st_shared_u32(tab_s + 4 * tid, reinterpret_cast<const uint32_t*>(&tab)[tid]);
+    if (tid < kStages) st_shared_u32(tab_s + 512 + 4 * tid, 0u);
     for (int i = gtid; i < G::kHistBytes / 16; i += kGT)
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
     if (tid == 0) {
@@ -219,7 +228,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t hist_g = hist0 + (uint32_t)((cr >> 2) * kBinsAlloc * 128);
     const bool none = HAS_DEPTH && win.none_valid;
 
-    bool pending = false;  // thread 0: a bulk store of the staging is in flight
+    bool pending = false;  // leader: a bulk store of the staging is in flight
     TileRois tr_next = group < n_pos ? load_tile(group) : TileRois{};
     for (int i = group; i < n_pos; i += kGroups) {
         const int64_t t = tile_of(i);
@@ -227,7 +236,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (i + kGroups < n_pos) tr_next = load_tile(i + kGroups);
         // the ROIs of position i + kStages (loaded when this tile releases stage s): fetched
         // now by cp.async into the group's slot, so no registers hold them through the rows
-        if (gtid == 0 && i + kStages < n_pos) {
+        if (leader && i + kStages < n_pos) {  // each leader into its own slot
             const int64_t tf = tile_of(i + kStages);
 #pragma unroll
             for (int p = 0; p < kP; ++p) {
@@ -235,13 +244,13 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                 if (c < n_rois)
                     for (int w = 0; w < 5; ++w)
                         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                         roi_slot + (uint32_t)(p * 20 + 4 * w)),
+                                         roi_slot + (uint32_t)(sub * 64 + p * 20 + 4 * w)),
                                      "l"(reinterpret_cast<const int32_t*>(rois + c) + w)
                                      : "memory");
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        auto fill_rois = [&]() {  // (thread 0) the ROIs of position i + kStages
+        auto fill_rois = [&]() {  // (a leader) the ROIs of position i + kStages, its own slot
             TileRois f{};
             if (i + kStages >= n_pos) return f;
             asm volatile("cp.async.wait_all;" ::: "memory");
@@ -252,7 +261,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                 if (f.valid[p]) {
                     int32_t* d = reinterpret_cast<int32_t*>(&f.r[p]);
                     for (int w = 0; w < 5; ++w)
-                        d[w] = (int32_t)ld_shared_u32(roi_slot + (uint32_t)(p * 20 + 4 * w));
+                        d[w] = (int32_t)ld_shared_u32(roi_slot + (uint32_t)(sub * 64 + p * 20 + 4 * w));
                 }
             }
             return f;
@@ -266,6 +275,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
             // phase (see lbp_hist_lane59.cuh: an early plain arrive completes the next phase)
             named_barrier_sync(bar_id, kGT);
             if (gtid == 0) issue(i + kStages, fill_rois());
+            else if (leader) asm volatile("cp.async.wait_all;" ::: "memory");  // its own copies
             uint32_t* hist = reinterpret_cast<uint32_t*>(smem + (hist0 - stages0));
 #pragma unroll
             for (int p = 0; p < kP; ++p) {
@@ -388,9 +398,11 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
             if (j == G::kMaxRows - 1) flush(pend);
         }
 
-        if (kQ == 1 && gtid == 0 && pending) bulk_wait_read_all();  // staging free again
-        named_barrier_sync(bar_id, kGT);  // A: stage read, counters complete
-        if (gtid == 0) {
+        if (SUB && leader && pending) bulk_wait_read_all();  // staging half free again
+        // A: this half's (SUB) / the group's counters complete and its stage rows read; the
+        // second half to get here refills the stage
+        named_barrier_sync(SUB ? sub_bar : bar_id, SUB ? 128 : kGT);
+        if (leader && (!SUB || (atom_shared_add(rel0 + 4 * s, 1u) & 1u))) {
             issue(i + kStages, fill_rois());
             if (roi_status && q == 0) {
 #pragma unroll
@@ -402,9 +414,10 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         // as u16 ([row][cell][bin]), then copied out
         if constexpr (kQ == 1) {
             // two crops, 2 home lanes per cell (lo = 2 cc: build_tab checks): thread -> cell
-            // column cc = bits 0-2, crop p = bit 3, counter word g = bit 4, bins bp + 8 k
-            // (bp = bits 5-7) -- affine in k; a quarter-warp's LDS.64 reads 64 contiguous B
-            const int ecc = gtid & 7, ep = (gtid >> 3) & 1, eg = (gtid >> 4) & 1, ebp = gtid >> 5;
+            // column cc = bits 0-2, crop p = bit 3, bins bp + 8 k (bp = bits 4-6), counter
+            // word g = bit 7 = the half -- affine in k; a quarter-warp's LDS.64 reads 64
+            // contiguous B
+            const int ecc = gtid & 7, ep = (gtid >> 3) & 1, ebp = (gtid >> 4) & 7, eg = gtid >> 7;
             const uint32_t q0 =
                 hist0 + (uint32_t)((eg * kBinsAlloc + ebp) * 128 + (2 * ecc + 16 * ep) * 4);
             const uint32_t e0 = staging + 2u * (uint32_t)(ep * G::kRowPad +
@@ -461,13 +474,14 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         if constexpr (kQ == 1) {
             fence_proxy_async_smem();          // staged rows -> async proxy
-            named_barrier_sync(bar_id, kGT);   // B: counters zero, rows staged
-            if (gtid == 0) {
+            named_barrier_sync(sub_bar, 128);  // B: this half's counters zero, its half staged
+            if (stid == 0) {  // cell rows 4 sub .. 4 sub + 3 of both rows: contiguous halves
+                constexpr int kHalf = kDim / 2;
 #pragma unroll
                 for (int p = 0; p < kP; ++p)
                     if (p == 0 ? tr.valid[0] : tr.valid[kP - 1])
-                        bulk_store_s2g(desc + crop_of(t, p) * desc_stride,
-                                       staging + p * G::kRowPad * 2, kDim * 2);
+                        bulk_store_s2g(desc + crop_of(t, p) * desc_stride + sub * kHalf,
+                                       staging + (p * G::kRowPad + sub * kHalf) * 2, kHalf * 2);
                 pending = true;
             }
         } else {
@@ -483,7 +497,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
             }
         }
     }
-    if (kQ == 1 && gtid == 0 && pending) bulk_wait_all();
+    if (SUB && leader && pending) bulk_wait_all();
 }
 
 // ---- host side
