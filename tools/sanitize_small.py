@@ -25,6 +25,19 @@ lb.lbp_extract_resized(gf, dft, rf, 200, 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)
 gb, db, rb = synthgen.kinect_frames(40, seed=4)                           # FRAME variant (160 ROIs)
 gb, dbt = torch.from_numpy(gb).to(dev), torch.from_numpy(db.view(np.int16)).to(dev).view(torch.uint16)
 lb.lbp_extract_source(gb, dbt, torch.from_numpy(rb).to(dev), 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)
+for T in (64, 200):                                                       # tile kernels
+    gt, dt = synthgen.gpu_face_crops(151, T, T, seed=T, device=dev)
+    if T % 16:
+        gp = torch.zeros((151, T, 208), dtype=torch.uint8, device=dev)
+        gp[:, :, :T] = gt
+        gt = gp[:, :, :T]
+    rt = torch.from_numpy(synthgen.full_rois(151, T, T)).to(dev)
+    rt[::9, 1:] = torch.tensor([3, 2, T - 9, T - 5], dtype=torch.int32)    # generic positions
+    lb.lbp_fused_extract(gt, dt, rt, 600, 1400, 8, 8, 59)
+cu8 = lb.lbp_extract_u8(g, d, r, 600, 1400, 8, 8, 59)                    # compact path
+W8, b8 = synthgen.svm_weights(100, 3776, seed=8)
+W8t, b8t = torch.from_numpy(W8).to(dev), torch.from_numpy(b8).to(dev)
+lb.svm_score_u8(cu8, W8t, b8t, prepared=lb.svm_prepare_u8(W8t))
 pk, exc, cnt = lb.desc_pack_u8(desc, row_base=0, cap=64)                  # compaction
 lb.desc_unpack_u8(pk, exc, cnt, 64)
 for C in (10, 130):
