@@ -149,6 +149,10 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            # the first query of each kind takes ~20 ms (tools/nvml_probe.py), the next ~1 us:
+            # issue them here, outside the timed region
+            pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             self.ok = True
         except Exception as e:  # pragma: no cover - no NVML on this host
             self.err = str(e)
@@ -169,6 +173,11 @@ class ClockSampler:
 
     def __enter__(self):
         if self.ok:
+            # the launching thread holds the GIL between its (GIL-releasing) ctypes calls;
+            # with the default 5-ms switch interval the sampler would get a few samples per
+            # timed region at most
+            self._switch = sys.getswitchinterval()
+            sys.setswitchinterval(1e-4)
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
@@ -177,6 +186,7 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+            sys.setswitchinterval(self._switch)
 
     def summary(self):
         if not self.ok:

@@ -100,18 +100,21 @@ def test_tile_mixed_rois(lb, T):
     _check(lb, grey, depth, rois, pitch=208 if T == 200 else None)
 
 
-def test_tile_full_size_sample(lb):
-    """16,384 crops of 64x64 (the bench's tile workload): rows of a seeded sample of crops
-    against the oracle computed on those crops only."""
-    n, T = 16384, 64
+@pytest.mark.parametrize("T", [64, 200])
+def test_tile_full_size_sample(lb, T):
+    """16,384 crops of 64x64 / 200x200 (the bench's tile workloads, 200-px grey rows padded to
+    208 B as there): rows of a seeded sample of crops against the oracle computed on those
+    crops only."""
+    n = 16384
     dev = torch.device(DEV)
     g, d = synthgen.gpu_face_crops(n, T, T, seed=5, device=dev)
+    g = _padded(g, 208 if T == 200 else None)
     r = torch.from_numpy(synthgen.full_rois(n, T, T)).to(dev)
     out = lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 59)
     torch.cuda.synchronize()
     idx = np.sort(np.random.default_rng(1).choice(n, size=48, replace=False))
     ti = torch.as_tensor(idx, device=dev)
-    grey = g[ti].cpu().numpy()
+    grey = np.ascontiguousarray(g[ti].cpu().numpy())
     depth = d.view(torch.int16)[ti].cpu().numpy().view(np.uint16)
     ref = oracle.lbp_extract(grey, depth, synthgen.full_rois(idx.size, T, T), 600, 1400, 8, 8, 59)
     got = out.view(torch.int16)[ti].cpu().numpy().view(np.uint16)
