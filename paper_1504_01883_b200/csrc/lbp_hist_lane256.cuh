@@ -4,13 +4,13 @@
 //
 //  * counters: u32 words [cell-row group g][bin 0..255 + dummy][lane], 4 cell rows per word
 //    as bytes (as lane59), 2 x 257 x 128 B = 65,792 B per 8-warp group;
-//  * codes: per 16-bit half t = 0x6400 + 4 col + 128 code (col = the pixel's counter lane:
-//    its own lane, or the first lane of the neighbouring cell for a spill-over column), built
-//    as in lane59: TL, T, TR (weights 128, 256, 512) on the FMA pipe as 1 - sat(g_c - g_p)
-//    accumulated down from 1024 + 4 col + 896 (exact fp16 integers <= 2044), R, BR, B, BL, L
-//    (1024 .. 16384) as HSET2 masks on the bits; the counter address is group base - 0x6400
-//    + t, and a masked-out pixel gets t of a dummy bin 256 in its own lane, so the update
-//    needs no select;
+//  * codes: per 16-bit half t = 4 col + 128 code (col = the pixel's counter lane: its own
+//    lane, or the first lane of the neighbouring cell for a spill-over column): TL, T, TR
+//    (weights 128, 256, 512) on the FMA pipe as 1 - sat(g_c - g_p) accumulated down from
+//    4 col + 896 in the fp16 SUBNORMAL range (bits = the integer, value = bits * 2^-24: exact,
+//    < 1024 so bits 10-15 stay zero), R, BR, B, BL, L (1024 .. 16384) as HSET2 masks OR-ed
+//    into bits 10-14 (no add); the counter address is group base + t, and a masked-out pixel
+//    gets t of a dummy bin 256 in its own lane, so the update needs no select;
 //  * 2 groups x 8 warps, 2 TMA stages (stage == group: grey 16 KB + depth 32 KB), the next
 //    crop's boxes issued as soon as the rows are consumed; the 32-KB descriptor is staged
 //    over the consumed counters (no room elsewhere): the epilogue reads a cell-row group's
@@ -46,20 +46,21 @@ static_assert(kDescBytes <= kRows * 128, "staging fits over the first cell-row g
 static_assert(kStages == kGroups, "stage == group");
 }  // namespace l256
 
-// Eq. 2 as the counter-address half 0x6400 + 4 col + 128 code (see the header)
+// Eq. 2 as the counter-address half 4 col + 128 code (see the header)
 __device__ __forceinline__ uint32_t lbp_addr2_256(uint32_t c, uint32_t tl, uint32_t t,
                                                   uint32_t tr, uint32_t r, uint32_t br,
                                                   uint32_t b, uint32_t bl, uint32_t l,
                                                   uint32_t top2) {
-    uint32_t f = f16_fma(hsub2_sat(c, tl), 0xD800D800u, top2);  // TL -128
-    f = f16_fma(hsub2_sat(c, t), 0xDC00DC00u, f);                // T  -256
-    f = f16_fma(hsub2_sat(c, tr), 0xE000E000u, f);               // TR -512
-    uint32_t a = hge2_mask(r, c) & 0x04000400u;                  // R  +1024
-    a |= hge2_mask(br, c) & 0x08000800u;                         // BR +2048
-    a |= hge2_mask(b, c) & 0x10001000u;                          // B  +4096
-    a |= hge2_mask(bl, c) & 0x20002000u;                         // BL +8192
-    a |= hge2_mask(l, c) & 0x40004000u;                          // L  +16384
-    return f + a;  // each half <= 0x6400 + 124 + 32640: no carry between halves
+    // subnormal weights: -128, -256, -512 times 2^-24 (bits 0x8080, 0x8100, 0x8200)
+    uint32_t f = f16_fma(hsub2_sat(c, tl), 0x80808080u, top2);  // TL -128
+    f = f16_fma(hsub2_sat(c, t), 0x81008100u, f);                // T  -256
+    f = f16_fma(hsub2_sat(c, tr), 0x82008200u, f);               // TR -512
+    f |= hge2_mask(r, c) & 0x04000400u;                          // R  bit 10 (1024)
+    f |= hge2_mask(br, c) & 0x08000800u;                         // BR bit 11
+    f |= hge2_mask(b, c) & 0x10001000u;                          // B  bit 12
+    f |= hge2_mask(bl, c) & 0x20002000u;                         // BL bit 13
+    f |= hge2_mask(l, c) & 0x40004000u;                          // L  bit 14 (16384)
+    return f;  // each half <= 124 + 32640
 }
 
 template <bool HAS_DEPTH, int WINM>
@@ -128,15 +129,11 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
     }
     // start values (all of TL, T, TR set) and dummy-bin addresses per pixel pair
-    const uint32_t top_a = opaque(((0x6400u + 4u * colk[0] + 896u)) |
-                                  ((0x6400u + 4u * colk[1] + 896u) << 16));
-    const uint32_t top_b = opaque(((0x6400u + 4u * colk[2] + 896u)) |
-                                  ((0x6400u + 4u * colk[3] + 896u) << 16));
-    const uint32_t dum_a = (0x6400u + 128u * kBins + 4u * colk[0]) |
-                           ((0x6400u + 128u * kBins + 4u * colk[1]) << 16);
-    const uint32_t dum_b = (0x6400u + 128u * kBins + 4u * colk[2]) |
-                           ((0x6400u + 128u * kBins + 4u * colk[3]) << 16);
-    const uint32_t gbase = opaque(hist0 + (uint32_t)((warp >> 2) * kRows * 128) - 0x6400u);
+    const uint32_t top_a = opaque((4u * colk[0] + 896u) | ((4u * colk[1] + 896u) << 16));
+    const uint32_t top_b = opaque((4u * colk[2] + 896u) | ((4u * colk[3] + 896u) << 16));
+    const uint32_t dum_a = (128u * kBins + 4u * colk[0]) | ((128u * kBins + 4u * colk[1]) << 16);
+    const uint32_t dum_b = (128u * kBins + 4u * colk[2]) | ((128u * kBins + 4u * colk[3]) << 16);
+    const uint32_t gbase = opaque(hist0 + (uint32_t)((warp >> 2) * kRows * 128));
     const uint32_t lo16 = win.lo << 16;
     const uint32_t span16 = (win.span << 16) | 0xFFFFu;
     const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // WINM 1
@@ -161,7 +158,11 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int s = i % kStages;
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
         if (!roi_is_fast(roi, geom)) {
-            if (gtid == 0) issue(i + kStages, 3);  // stage s was never filled: release it
+            // stage s was never filled: release it, once every thread of the group has
+            // passed its wait on this phase (lbp_hist_lane59.cuh: an earlier plain arrive
+            // completes the next phase and a late thread waits on the one after it)
+            named_barrier_sync(bar_id, kGroupThreads);
+            if (gtid == 0) issue(i + kStages, 3);
             extract_roi_generic<kBins, kGroupThreads>(
                 CodePlane<uint8_t>{grey, geom.grey_pitch, geom.grey_img_stride},
                 HAS_DEPTH ? depth : nullptr, geom, roi, n, win, 8, 8, desc, desc_stride,

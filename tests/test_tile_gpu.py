@@ -122,7 +122,8 @@ def test_tile_full_size_sample(lb, T):
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("geom", ["frame256_roi100", "tile200_mixed", "tile64_mixed"])
+@pytest.mark.parametrize("geom", ["frame256_roi100", "tile200_mixed", "tile64_mixed",
+                                  "crops128_bins256_mixed"])
 def test_generic_positions_repeat_no_hang(lb, geom):
     """Large batches whose ROIs take the generic code path inside the persistent TMA kernels,
     launched repeatedly: a generic position releases its (unfilled) stage with a plain
@@ -135,8 +136,11 @@ def test_generic_positions_repeat_no_hang(lb, geom):
         n, T, S = 2048, 100, 256     # lane59 FRAME variant, every ROI generic
     elif geom == "tile200_mixed":
         n, T, S = 2048, 200, 200     # tile kernel, quadrants + generic crops
-    else:
+    elif geom == "tile64_mixed":
         n, T, S = 4096, 64, 64       # tile kernel, crop pairs + generic crops
+    else:
+        n, T, S = 2048, 128, 128     # lane256 kernel (256 bins) + generic crops
+    bins = 256 if geom == "crops128_bins256_mixed" else 59
     g, d = synthgen.gpu_face_crops(n, S, S, seed=3, device=dev)
     if S % 16:
         gb = torch.zeros((n, S, (S + 15) // 16 * 16), dtype=torch.uint8, device=dev)
@@ -152,9 +156,9 @@ def test_generic_positions_repeat_no_hang(lb, geom):
     ti = torch.as_tensor(idx, device=dev)
     ref = oracle.lbp_extract(g[ti].cpu().numpy(), d.view(torch.int16)[ti].cpu().numpy().view(np.uint16),
                              np.concatenate([np.arange(idx.size)[:, None], rois[idx, 1:]], 1).astype(np.int32),
-                             600, 1400, 8, 8, 59)
-    out = torch.empty((n, 3776), dtype=torch.uint16, device=dev)
+                             600, 1400, 8, 8, bins)
+    out = torch.empty((n, 64 * bins), dtype=torch.uint16, device=dev)
     for _ in range(40):
-        lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 59, out=out)
+        lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, bins, out=out)
         torch.cuda.synchronize()
         assert np.array_equal(out.view(torch.int16)[ti].cpu().numpy().view(np.uint16), ref)
