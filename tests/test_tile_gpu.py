@@ -162,3 +162,27 @@ def test_generic_positions_repeat_no_hang(lb, geom):
         lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, bins, out=out)
         torch.cuda.synchronize()
         assert np.array_equal(out.view(torch.int16)[ti].cpu().numpy().view(np.uint16), ref)
+
+
+@pytest.mark.parametrize("T", [64, 200])
+def test_tile_fused_source_and_compact(lb, T):
+    """The tile kernel inside the other entry points: the grey block of the fused grey||depth
+    descriptor (row stride 2 dim; the depth block takes the band kernel) and the compact u8
+    form (extraction into a scratch, then the row pack) -- both against the oracle."""
+    n = 160 if T == 200 else 301
+    grey, depth = synthgen.face_crops(n, T, T, seed=13 * T)
+    rois = synthgen.full_rois(n, T, T)
+    g = _padded(torch.from_numpy(grey).to(DEV), 208 if T == 200 else None)
+    d = torch.from_numpy(depth.view(np.int16)).to(DEV).view(torch.uint16)
+    r = torch.from_numpy(rois).to(DEV)
+    fused = lb.lbp_extract_source(g, d, r, 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)
+    cd = lb.lbp_extract_u8(g, d, r, 600, 1400, 8, 8, 59)
+    torch.cuda.synchronize()
+    ref_g = oracle.lbp_extract(grey, depth, rois, 600, 1400, 8, 8, 59)
+    ref_f = oracle.lbp_extract(grey, depth, rois, 600, 1400, 8, 8, 59, source=2)
+    got_f = fused.cpu().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got_f, ref_f)
+    assert np.array_equal(got_f[:, :ref_g.shape[1]], ref_g)
+    packed = cd.packed.cpu().numpy()
+    assert np.array_equal(packed[:, :ref_g.shape[1]], (ref_g & 255).astype(np.uint8))
+    assert np.array_equal(cd.exc_n.cpu().numpy(), (ref_g > 255).sum(1))
