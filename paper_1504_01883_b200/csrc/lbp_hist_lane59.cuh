@@ -242,6 +242,27 @@ __device__ __forceinline__ DepthRow depth_row(uint32_t addr) {
     return depth_row_w(ld_shared_u32x2(addr));
 }
 
+// DINT depth rows (window span <= 1022, lo <= 0x6400): every depth word clamped to
+// [lo - 1, lo + 1022] and offset to the fp16 bits of the INTEGER 1025 + (d' - lo) in
+// [1024, 2047] (one VIMNMX pair and one packed add per word: no carry between the halves).
+// The order is preserved for the codes that are counted: a counted centre c is in
+// [lo, lo + span], so d' >= c iff d >= c; and the values are exact fp16 integers, so the
+// codes use the grey plane's HADD2.SAT arithmetic (FMA pipe) instead of HSET2 compares.
+__device__ __forceinline__ DepthRow depth_row_int(uint2 w, uint32_t lo2m1, uint32_t hi2,
+                                                  uint32_t off2) {
+    DepthRow r;
+    r.raw0 = w.x;
+    r.raw1 = w.y;
+    r.h0 = vmin_u16x2(__vmaxu2(w.x, lo2m1), hi2) + off2;
+    r.h1 = vmin_u16x2(__vmaxu2(w.y, lo2m1), hi2) + off2;
+    const uint32_t left = __shfl_up_sync(0xFFFFFFFFu, r.h1, 1);
+    const uint32_t right = __shfl_down_sync(0xFFFFFFFFu, r.h0, 1);
+    r.lh0 = prmt(left, r.h0, 0x5432);
+    r.mh = prmt(r.h0, r.h1, 0x5432);
+    r.rh1 = prmt(r.h1, right, 0x5432);
+    return r;
+}
+
 __device__ __forceinline__ uint32_t hle2_mask(uint32_t a, uint32_t b) {
     uint32_t r;  // 0xFFFF / 0 per half
     asm("set.le.u32.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -296,6 +317,7 @@ __device__ __forceinline__ uint32_t lbp_offset2_cmp(uint32_t c, uint32_t tl, uin
 // whose rows are forwarded from there.  OUTM == kOutU8: the compact row (U8Out) is staged
 // and bulk-stored; `desc` is unused (the generic path counts into the group's counters and
 // stages its row the same way).
+// WINM bit 2 (DINT, with WINM 1 or 2): depth-plane codes in the integer domain (depth_row_int).
 template <bool HAS_DEPTH, bool DEPTH_SRC, int WINM, bool FRAME, int OUTM = l59::kOutU16>
 __global__ void __launch_bounds__(l59::kThreads, 1)
 lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
@@ -309,12 +331,14 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     constexpr bool GATHER = OUTM == l59::kOutGather;
     constexpr bool U8 = OUTM == l59::kOutU8;
     constexpr bool FUSED = OUTM == l59::kOutFused;
-    static_assert(!FUSED || (HAS_DEPTH && !DEPTH_SRC && WINM != 0 && !FRAME),
+    static_assert(!FUSED || (HAS_DEPTH && !DEPTH_SRC && (WINM & 3) != 0 && !FRAME),
                   "fused grey||depth: depth plane staged, fp16 depth window, crop stacks");
     static_assert(OUTM == l59::kOutU16 || !FRAME, "the gather / u8 outputs use the crop-stack epilogue");
     using namespace l59;
     using L = Layout<FRAME>;
-    constexpr bool FP16WIN = WINM != 0;
+    constexpr int WIN = WINM & 3;          // the window test
+    constexpr bool DINT = (WINM & 4) != 0;  // depth codes in the integer domain
+    constexpr bool FP16WIN = WIN != 0;
     constexpr int kGreyBytes = L::kGreyBytes, kStageBytes = L::kStageBytes;
     constexpr int kGroupOff = L::kGroupOff, kGroupBytes = L::kGroupBytes;
     const int kLutOff = lut_off, kPlainLutOff = lut_off + kLutBytes;  // (lut_placement)
@@ -434,6 +458,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // WINM 1
     const uint32_t mid2 = ((2 * win.lo + win.span) / 2) * 0x10001u;                 // WINM 2
     const uint32_t half2 = (win.span / 2) * 0x10001u;
+    // DINT: clamp bounds and the offset to the fp16 integers 1025 + (d' - lo)
+    const uint32_t dlo2m1 = (win.lo - 1u) * 0x10001u, dhi2 = (win.lo + 1022u) * 0x10001u;
+    const uint32_t doff2 = ((0x6401u - win.lo) & 0xFFFFu) * 0x10001u;
     // LUT address of an offset half t: lutb | t (the LUT sits at 0x6000 mod 2^16)
     const uint32_t lutb = opaque(smem_u32(smem + kLutOff) - kLutMod);
     const uint32_t base2 = opaque((kLutMod + 4u * lane) * 0x10001u);  // 512.0 + 2 lane
@@ -583,7 +610,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
             return w;
         };
         auto build_row = [&](const Raw& w) {
-            if constexpr (DS) return depth_row_w(depth_words(w));
+            if constexpr (DS && DINT) return depth_row_int(depth_words(w), dlo2m1, dhi2, doff2);
+            else if constexpr (DS) return depth_row_w(depth_words(w));
             else if constexpr (FRAME) return lane_row_w(prmt(w.a, w.b, gsel));
             else return lane_row_w(w.a);
         };
@@ -594,7 +622,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         struct Pend { uint32_t bin[4], val[4]; };
         auto do_row = [&](const Row& top, const Row& mid, const Row& bot, const Raw& dc) {
             uint32_t t0, t1;
-            if constexpr (DS) {
+            if constexpr (DS && !DINT) {
                 t0 = lbp_offset2_cmp(mid.h0, top.lh0, top.h0, top.mh, mid.mh, bot.mh, bot.h0,
                                      bot.lh0, mid.lh0, base2);
                 t1 = lbp_offset2_cmp(mid.h1, top.mh, top.h1, top.rh1, mid.rh1, bot.rh1, bot.h1,
@@ -620,7 +648,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                     c1 = d.y;
                 }
                 uint32_t m0, m1;
-                if constexpr (WINM == 2) {
+                if constexpr (WIN == 2) {
                     m0 = hle2_mask(habsdiff2(c0, mid2), half2);
                     m1 = hle2_mask(habsdiff2(c1, mid2), half2);
                 } else {
@@ -902,11 +930,15 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     const bool fp16win = depth && !win.none_valid && win.lo + win.span <= 0x7BFEu;
     const uint32_t whi = win.lo + win.span;
     const bool centred = fp16win && whi < 2048u && ((win.lo + whi) & 1u) == 0;  // WINM 2
+    // depth-plane codes in the integer domain (WINM | 4): window span <= 1022, lo <= 0x6400
+    const bool dint = fp16win && win.span <= 1022u && win.lo <= 0x6400u;
     auto pick = [&](auto frame_tag) {
         constexpr bool F = decltype(frame_tag)::value;
         if (depth_source)
-            return centred ? lbp_hist_lane59_kernel<true, true, 2, F>
-                           : lbp_hist_lane59_kernel<true, true, 1, F>;
+            return dint ? (centred ? lbp_hist_lane59_kernel<true, true, 6, F>
+                                   : lbp_hist_lane59_kernel<true, true, 5, F>)
+                        : (centred ? lbp_hist_lane59_kernel<true, true, 2, F>
+                                   : lbp_hist_lane59_kernel<true, true, 1, F>);
         if (depth)
             return centred   ? lbp_hist_lane59_kernel<true, false, 2, F>
                    : fp16win ? lbp_hist_lane59_kernel<true, false, 1, F>
@@ -922,8 +954,10 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
         return lbp_hist_lane59_kernel<false, false, 0, false, O>;
     };
     if (fused && !fp16win) return cudaErrorNotSupported;  // (the depth plane's compares)
-    auto kern = fused   ? (centred ? lbp_hist_lane59_kernel<true, false, 2, false, l59::kOutFused>
-                                   : lbp_hist_lane59_kernel<true, false, 1, false, l59::kOutFused>)
+    auto kern = fused   ? (dint ? (centred ? lbp_hist_lane59_kernel<true, false, 6, false, l59::kOutFused>
+                                           : lbp_hist_lane59_kernel<true, false, 5, false, l59::kOutFused>)
+                                : (centred ? lbp_hist_lane59_kernel<true, false, 2, false, l59::kOutFused>
+                                           : lbp_hist_lane59_kernel<true, false, 1, false, l59::kOutFused>))
                 : gather  ? pick_out(std::integral_constant<int, l59::kOutGather>{})
                 : u8out ? pick_out(std::integral_constant<int, l59::kOutU8>{})
                 : frame ? pick(std::true_type{})
