@@ -51,6 +51,9 @@ WORKLOADS = {
     "tile64": (16384, 64, 64, 8, 8, 59, 100,
                "16384 x 64x64 grey+depth crops (the crop size of BASELINE configs[0], batched), "
                "8x8 cells x 59 uniform bins, 100-identity one-vs-all linear SVM"),
+    "tile100": (16384, 100, 100, 8, 8, 59, 100,
+                "16384 x 100x100 grey+depth crops (SPEC's 100x100 ROI size; rows padded to 112 / "
+                "208 B for TMA), 8x8 cells x 59 uniform bins, 100-identity SVM"),
     "tile200": (16384, 200, 200, 8, 8, 59, 100,
                 "16384 x 200x200 grey+depth crops (the paper's resized face, P:154; grey rows "
                 "padded to 208 B for TMA), 8x8 cells x 59 uniform bins, 100-identity SVM"),
@@ -417,6 +420,7 @@ def main():
     grey, depth = synthgen.gpu_face_crops(n, H, Wd, seed=args.seed, first_index=first,
                                           dist=args.dist, device=dev)
     grey = pad_rows(torch, grey)
+    depth = pad_rows(torch, depth)
     if args.no_depth:
         depth = None
     rois = torch.from_numpy(synthgen.full_rois(n, H, Wd)).to(dev)
@@ -992,7 +996,11 @@ def run_e2e(args, lb, torch, dist, world, dev, grey, depth, H, Wd, cx, cy, bins,
     g_h = pad_rows(torch, grey.cpu()) if grey.stride(1) != grey.shape[2] else grey.cpu().pin_memory()
     if not g_h.is_pinned():
         g_h = g_h.pin_memory()
-    d_h = depth.cpu().pin_memory() if depth is not None else None
+    d_h = None
+    if depth is not None:
+        d_h = pad_rows(torch, depth.cpu()) if depth.stride(1) != depth.shape[2] else depth.cpu()
+        if not d_h.is_pinned():
+            d_h = d_h.pin_memory()
     r_h = torch.from_numpy(synthgen.full_rois(n, H, Wd)).pin_memory()
     lab_h = torch.empty(n, dtype=torch.int32).pin_memory()
     top_h = torch.empty(n, dtype=torch.float32).pin_memory()

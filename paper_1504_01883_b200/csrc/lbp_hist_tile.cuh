@@ -34,8 +34,8 @@ __host__ __device__ constexpr int up(int v, int m) { return (v + m - 1) / m * m;
 
 template <int T>
 struct Geo {
-    static_assert(T % 4 == 0 && T >= 32 && T <= 252 && (T <= 64 || T > 128),
-                  "tile kernel: T <= 64 (two crops per tile) or 128 < T <= 252 (quadrants)");
+    static_assert(T % 4 == 0 && T >= 32 && T <= 252,
+                  "tile kernel: T <= 64 (two crops per tile), <= 128 (one), <= 252 (quadrants)");
     static constexpr int kQ = T > 128 ? 2 : 1;        // tiles per axis of a crop
     static constexpr int kP = T <= 64 ? 2 : 1;         // crops side by side in a tile
     static constexpr int kCT = 8 / kQ;                 // cells per tile axis
@@ -412,7 +412,39 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
         // ---- epilogue: the home lanes of each cell summed, counters re-zeroed, counts staged
         // as u16 ([row][cell][bin]), then copied out
-        if constexpr (kQ == 1) {
+        if constexpr (kQ == 1 && kP == 1) {
+            // one crop (64 < T <= 128): this half's items (bin, cc) of its counter word
+            // g = sub, cc fastest; each sums its cell's ~3 home lanes as 16-bit pairs
+            constexpr int kItems = kBinsAlloc * 8;
+            const uint32_t ghist = hist0 + (uint32_t)(sub * kBinsAlloc * 128);
+            for (int it = stid; it < kItems; it += 128) {
+                const int cc = it & 7, bin = it >> 3;
+                const uint32_t row = ghist + (uint32_t)(bin * 128);
+                if (bin == kBins) {  // dummy bin: re-zero the whole row once
+                    if (cc == 0)
+                        for (int l = 0; l < 32; l += 4)
+                            st_shared_u32x4(row + l * 4, make_uint4(0, 0, 0, 0));
+                    continue;
+                }
+                const int lo = (int)ld_shared_u8(tab_s + offsetof(TileTab, lo) + cc);
+                const int hi = (int)ld_shared_u8(tab_s + offsetof(TileTab, hi) + cc);
+                uint32_t a02 = 0, a13 = 0;
+                for (int l = lo; l < hi; ++l) {
+                    const uint32_t w = ld_shared_u32(row + l * 4);
+                    st_shared_u32(row + l * 4, 0u);
+                    a02 += w & 0x00FF00FFu;
+                    a13 += (w >> 8) & 0x00FF00FFu;
+                }
+                const uint32_t c[4] = {a02 & 0xFFFFu, a13 & 0xFFFFu, a02 >> 16, a13 >> 16};
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int e = ((4 * sub + b) * 8 + cc) * kBins + bin;
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(staging + 2 * e),
+                                 "h"((uint16_t)c[b])
+                                 : "memory");
+                }
+            }
+        } else if constexpr (kQ == 1) {
             // two crops, 2 home lanes per cell (lo = 2 cc: build_tab checks): thread -> cell
             // column cc = bits 0-2, crop p = bit 3, bins bp + 8 k (bp = bits 4-6), counter
             // word g = bit 7 = the half -- affine in k; a quarter-warp's LDS.64 reads 64

@@ -101,10 +101,12 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
     // box so that 128x128 ROIs at any column take the TMA path (crop stacks keep the
     // 128-wide boxes).
     const bool frame = geom.width >= l59::Layout<true>::kGreyW;
-    // crop stacks of 64x64 or 200x200 images (8x8 cells, 59 bins, grey codes): the tile
-    // variant of the TMA kernel (two 64-px crops per warp row / four 200-px quadrant tiles)
+    // crop stacks of 64x64, 100x100 or 200x200 images (8x8 cells, 59 bins, grey codes): the
+    // tile variant of the TMA kernel (two 64-px crops per warp row / one 100-px crop / four
+    // 200-px quadrant tiles)
     if (!depth_source && !small_batch && bins == 59 && cells_x == 8 && cells_y == 8 &&
-        geom.width == geom.height && (geom.width == 64 || geom.width == 200) &&
+        geom.width == geom.height &&
+        (geom.width == 64 || geom.width == 100 || geom.width == 200) &&
         tile_path_applicable(geom, grey, depth) &&
         // whole rows leave the 64-px tiles by bulk copies (16 B), the 200-px quadrants' runs
         // of 4 cells by 8-B stores
@@ -113,6 +115,9 @@ int32_t extract_block(const uint8_t* grey, const uint16_t* depth, bool depth_sou
             geom.width == 64
                 ? launch_lbp_hist_tile<64>(grey, depth, geom, rois, n_rois, win, desc, desc_stride,
                                            roi_status, num_sms(), stream)
+            : geom.width == 100
+                ? launch_lbp_hist_tile<100>(grey, depth, geom, rois, n_rois, win, desc,
+                                            desc_stride, roi_status, num_sms(), stream)
                 : launch_lbp_hist_tile<200>(grey, depth, geom, rois, n_rois, win, desc,
                                             desc_stride, roi_status, num_sms(), stream);
         if (e != cudaErrorNotSupported) return launch_status(e);

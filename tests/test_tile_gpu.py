@@ -57,18 +57,19 @@ def _check(lb, grey, depth, rois, dmin=600, dmax=1400, pitch=None):
 # 200-px rows need a 16-B multiple pitch for TMA (208 B grey; depth rows are 400 B): the tight
 # pitch takes the band kernel, also checked here
 @pytest.mark.parametrize("T,n,pitch", [(64, 301, None), (64, 300, None), (200, 160, 208),
-                                       (200, 161, 224), (200, 160, None)])
+                                       (200, 161, 224), (200, 160, None), (100, 150, 112),
+                                       (100, 151, None)])
 @pytest.mark.parametrize("dist", ["face", "noise", "constant"])
 def test_tile_crops_bitexact(lb, T, n, pitch, dist):
     grey, depth = synthgen.face_crops(n, T, T, seed=T + n, dist=dist)
     _check(lb, grey, depth, synthgen.full_rois(n, T, T), pitch=pitch)
 
 
-@pytest.mark.parametrize("T", [64, 200])
+@pytest.mark.parametrize("T", [64, 100, 200])
 @pytest.mark.parametrize("window", [(600, 1400), (500, 3000), (0, 40000), (0, 0), None])
 def test_tile_window_modes(lb, T, window):
-    n = 160 if T == 200 else 297
-    pitch = 208 if T == 200 else None
+    n = 160 if T >= 100 else 297
+    pitch = {64: None, 100: 112, 200: 208}[T]
     grey, depth = synthgen.face_crops(n, T, T, seed=7 * T, dist="face")
     if window is None:
         _check(lb, grey, None, synthgen.full_rois(n, T, T), pitch=pitch)
@@ -76,12 +77,12 @@ def test_tile_window_modes(lb, T, window):
         _check(lb, grey, depth, synthgen.full_rois(n, T, T), *window, pitch=pitch)
 
 
-@pytest.mark.parametrize("T", [64, 200])
+@pytest.mark.parametrize("T", [64, 100, 200])
 def test_tile_mixed_rois(lb, T):
     """Full crops mixed with ROIs the tile path does not take (smaller, offset, clamped,
     out-of-range image, too small for the grid): those go through the generic code path
     inside the same kernel; statuses and rows must still match the oracle."""
-    n = 170 if T == 200 else 311
+    n = 170 if T >= 100 else 311
     grey, depth = synthgen.face_crops(n, T, T, seed=99 + T)
     rois = synthgen.full_rois(n, T, T)
     rng = np.random.default_rng(T)
@@ -97,10 +98,10 @@ def test_tile_mixed_rois(lb, T):
             rois[i, 1:] = (0, 0, 6, 6)                  # fewer interior pixels than cells
         else:
             rois[i, 1:] = (16, 0, T - 16, T)            # aligned x, narrower
-    _check(lb, grey, depth, rois, pitch=208 if T == 200 else None)
+    _check(lb, grey, depth, rois, pitch={64: None, 100: 112, 200: 208}[T])
 
 
-@pytest.mark.parametrize("T", [64, 200])
+@pytest.mark.parametrize("T", [64, 100, 200])
 def test_tile_full_size_sample(lb, T):
     """16,384 crops of 64x64 / 200x200 (the bench's tile workloads, 200-px grey rows padded to
     208 B as there): rows of a seeded sample of crops against the oracle computed on those
@@ -108,7 +109,8 @@ def test_tile_full_size_sample(lb, T):
     n = 16384
     dev = torch.device(DEV)
     g, d = synthgen.gpu_face_crops(n, T, T, seed=5, device=dev)
-    g = _padded(g, 208 if T == 200 else None)
+    g = _padded(g, {64: None, 100: 112, 200: 208}[T])
+    d = _padded(d.view(torch.int16), 112 if T == 100 else None).view(torch.uint16)
     r = torch.from_numpy(synthgen.full_rois(n, T, T)).to(dev)
     out = lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 59)
     torch.cuda.synchronize()
@@ -164,16 +166,18 @@ def test_generic_positions_repeat_no_hang(lb, geom):
         assert np.array_equal(out.view(torch.int16)[ti].cpu().numpy().view(np.uint16), ref)
 
 
-@pytest.mark.parametrize("T", [64, 200])
+@pytest.mark.parametrize("T", [64, 100, 200])
 def test_tile_fused_source_and_compact(lb, T):
     """The tile kernel inside the other entry points: the grey block of the fused grey||depth
     descriptor (row stride 2 dim; the depth block takes the band kernel) and the compact u8
     form (extraction into a scratch, then the row pack) -- both against the oracle."""
-    n = 160 if T == 200 else 301
+    n = 160 if T >= 100 else 301
     grey, depth = synthgen.face_crops(n, T, T, seed=13 * T)
     rois = synthgen.full_rois(n, T, T)
-    g = _padded(torch.from_numpy(grey).to(DEV), 208 if T == 200 else None)
-    d = torch.from_numpy(depth.view(np.int16)).to(DEV).view(torch.uint16)
+    pitch = {64: None, 100: 112, 200: 208}[T]
+    g = _padded(torch.from_numpy(grey).to(DEV), pitch)
+    d = _padded(torch.from_numpy(depth.view(np.int16)).to(DEV),
+                112 if T == 100 else None).view(torch.uint16)
     r = torch.from_numpy(rois).to(DEV)
     fused = lb.lbp_extract_source(g, d, r, 600, 1400, 8, 8, 59, lb.LBP_SRC_FUSED)
     cd = lb.lbp_extract_u8(g, d, r, 600, 1400, 8, 8, 59)
