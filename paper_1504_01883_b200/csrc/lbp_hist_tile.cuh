@@ -427,13 +427,16 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                     continue;
                 }
                 const int lo = (int)ld_shared_u8(tab_s + offsetof(TileTab, lo) + cc);
-                const int hi = (int)ld_shared_u8(tab_s + offsetof(TileTab, hi) + cc);
+                const int nl = (int)ld_shared_u8(tab_s + offsetof(TileTab, hi) + cc) - lo;
+                // (the 4 bins of a warp start at different home lanes: fewer bank conflicts)
+                int l = lo + (bin & 3) % nl;
                 uint32_t a02 = 0, a13 = 0;
-                for (int l = lo; l < hi; ++l) {
+                for (int j = 0; j < nl; ++j) {
                     const uint32_t w = ld_shared_u32(row + l * 4);
                     st_shared_u32(row + l * 4, 0u);
                     a02 += w & 0x00FF00FFu;
                     a13 += (w >> 8) & 0x00FF00FFu;
+                    if (++l == lo + nl) l = lo;
                 }
                 const uint32_t c[4] = {a02 & 0xFFFFu, a13 & 0xFFFFu, a02 >> 16, a13 >> 16};
 #pragma unroll

@@ -25,6 +25,11 @@ if H % 16:  # TMA needs 16-B multiple row pitches: pad the grey rows (200 -> 208
     gb = torch.zeros((n, H, P), dtype=torch.uint8, device=dev)
     gb[:, :, :H] = g
     g = gb[:, :, :H]
+if H % 8:  # ... and the depth rows (100 px = 200 B -> 208 B)
+    P = (H + 7) // 8 * 8
+    db = torch.zeros((n, H, P), dtype=torch.uint16, device=dev)
+    db[:, :, :H] = d
+    d = db[:, :, :H]
 r = torch.from_numpy(synthgen.full_rois(n, H, H)).to(dev)
 if len(sys.argv) > 4 and sys.argv[4] == "l2":
     r[:, 0] = torch.arange(n, device=dev, dtype=torch.int32) % 16
