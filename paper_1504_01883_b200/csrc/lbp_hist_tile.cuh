@@ -413,35 +413,29 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         // ---- epilogue: the home lanes of each cell summed, counters re-zeroed, counts staged
         // as u16 ([row][cell][bin]), then copied out
         if constexpr (kQ == 1 && kP == 1) {
-            // one crop (64 < T <= 128): this half's items (bin, cc) of its counter word
-            // g = sub, cc fastest; each sums its cell's ~3 home lanes as 16-bit pairs
-            constexpr int kItems = kBinsAlloc * 8;
-            const uint32_t ghist = hist0 + (uint32_t)(sub * kBinsAlloc * 128);
-            for (int it = stid; it < kItems; it += 128) {
-                const int cc = it & 7, bin = it >> 3;
-                const uint32_t row = ghist + (uint32_t)(bin * 128);
-                if (bin == kBins) {  // dummy bin: re-zero the whole row once
-                    if (cc == 0)
-                        for (int l = 0; l < 32; l += 4)
-                            st_shared_u32x4(row + l * 4, make_uint4(0, 0, 0, 0));
-                    continue;
-                }
-                const int lo = (int)ld_shared_u8(tab_s + offsetof(TileTab, lo) + cc);
-                const int nl = (int)ld_shared_u8(tab_s + offsetof(TileTab, hi) + cc) - lo;
-                // (the 4 bins of a warp start at different home lanes: fewer bank conflicts)
-                int l = lo + (bin & 3) % nl;
-                uint32_t a02 = 0, a13 = 0;
-                for (int j = 0; j < nl; ++j) {
-                    const uint32_t w = ld_shared_u32(row + l * 4);
-                    st_shared_u32(row + l * 4, 0u);
-                    a02 += w & 0x00FF00FFu;
-                    a13 += (w >> 8) & 0x00FF00FFu;
-                    if (++l == lo + nl) l = lo;
-                }
-                const uint32_t c[4] = {a02 & 0xFFFFu, a13 & 0xFFFFu, a02 >> 16, a13 >> 16};
+            // one crop (64 < T <= 128), quad slots (build_tab): this half's quads (bin, cell
+            // x) of its counter word g = sub, as the 128-px kernel's epilogue -- thread ->
+            // cx = stid & 7, bins bp + 16 k (bp = stid >> 3); one 16-B load, a byte transpose
+            // and IDP4A give the cell's 4 cell rows
+            const int ecx = stid & 7, ebp = stid >> 3;
+            const uint32_t qbase = hist0 + (uint32_t)(((sub * kBinsAlloc + ebp) * 8 + ecx) * 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int bin = ebp + 16 * k;
+                if (bin > kBins) break;
+                const uint32_t qa = qbase + k * (16 * 128);
+                const uint4 w = ld_shared_u32x4(qa);
+                st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+                if (bin == kBins) break;  // dummy bin: only re-zeroed
+                const uint32_t lo01 = prmt(w.x, w.y, 0x5140), hi01 = prmt(w.x, w.y, 0x7362);
+                const uint32_t lo23 = prmt(w.z, w.w, 0x5140), hi23 = prmt(w.z, w.w, 0x7362);
+                const uint32_t c[4] = {__dp4a(prmt(lo01, lo23, 0x5410), 0x01010101u, 0u),
+                                       __dp4a(prmt(lo01, lo23, 0x7632), 0x01010101u, 0u),
+                                       __dp4a(prmt(hi01, hi23, 0x5410), 0x01010101u, 0u),
+                                       __dp4a(prmt(hi01, hi23, 0x7632), 0x01010101u, 0u)};
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    const int e = ((4 * sub + b) * 8 + cc) * kBins + bin;
+                    const int e = ((4 * sub + b) * 8 + ecx) * kBins + bin;
                     asm volatile("st.shared.u16 [%0], %1;" ::"r"(staging + 2 * e),
                                  "h"((uint16_t)c[b])
                                  : "memory");
@@ -473,37 +467,41 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                                  : "memory");
             }
         } else {
-            // quadrant: items (bin, cc), cc fastest; each sums its cell's ~6 home lanes as
-            // 16-bit pairs, starting at a bin-dependent lane so that the 8 bins of a warp read
-            // different banks at each step
-            constexpr int kItems = kBinsAlloc * kCT;
-            for (int it = gtid; it < kItems; it += kGT) {
-                const int cc = it % kCT, bin = it / kCT;
-                const uint32_t row = hist0 + (uint32_t)(bin * 128);
-                if (bin == kBins) {  // dummy bin: re-zero the whole row once
-                    if (cc == 0)
-                        for (int l = 0; l < 32; l += 4)
-                            st_shared_u32x4(row + l * 4, make_uint4(0, 0, 0, 0));
-                    continue;
-                }
-                const int lo = (int)ld_shared_u8(tab_s + offsetof(TileTab, lo) + qx * 8 + cc);
-                const int nl = (int)ld_shared_u8(tab_s + offsetof(TileTab, hi) + qx * 8 + cc) - lo;
-                int l = lo + bin % nl;
-                uint32_t a02 = 0, a13 = 0;
-                for (int j = 0; j < nl; ++j) {
-                    const uint32_t w = ld_shared_u32(row + l * 4);
-                    st_shared_u32(row + l * 4, 0u);
-                    a02 += w & 0x00FF00FFu;
-                    a13 += (w >> 8) & 0x00FF00FFu;
-                    if (++l == lo + nl) l = lo;
-                }
-                const uint32_t c[4] = {a02 & 0xFFFFu, a13 & 0xFFFFu, a02 >> 16, a13 >> 16};
+            // quadrant, octet slots (build_tab): thread -> quad lq = gtid & 7 (slots 4 lq ..
+            // 4 lq + 3: half of cell lq >> 1), bins bp + 16 k (bp = gtid >> 3); a quarter-warp
+            // reads one bin's 128 contiguous bytes; the two quads of a cell (adjacent lanes)
+            // are combined by one shuffle of the packed 16-bit partial counts.  The loop runs
+            // uniformly (the shuffles need the whole warp); bins past the dummy are predicated.
+            static_assert(kGT == 128 && kCT == 4, "quadrant epilogue map");
+            const int lq = gtid & 7, ebp = gtid >> 3;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int e = (b * kCT + cc) * kBins + bin;
-                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(staging + 2 * e),
-                                 "h"((uint16_t)c[b])
-                                 : "memory");
+            for (int k = 0; k < 4; ++k) {
+                const int bin = ebp + 16 * k;
+                const uint32_t qa = hist0 + (uint32_t)(bin * 128 + lq * 16);
+                uint4 w = make_uint4(0, 0, 0, 0);
+                if (bin <= kBins) {
+                    w = ld_shared_u32x4(qa);
+                    st_shared_u32x4(qa, make_uint4(0, 0, 0, 0));
+                }
+                const uint32_t lo01 = prmt(w.x, w.y, 0x5140), hi01 = prmt(w.x, w.y, 0x7362);
+                const uint32_t lo23 = prmt(w.z, w.w, 0x5140), hi23 = prmt(w.z, w.w, 0x7362);
+                const uint32_t p01 = __dp4a(prmt(lo01, lo23, 0x5410), 0x01010101u, 0u) |
+                                     (__dp4a(prmt(lo01, lo23, 0x7632), 0x01010101u, 0u) << 16);
+                const uint32_t p23 = __dp4a(prmt(hi01, hi23, 0x5410), 0x01010101u, 0u) |
+                                     (__dp4a(prmt(hi01, hi23, 0x7632), 0x01010101u, 0u) << 16);
+                // each partial <= 4 x 255: the 16-bit halves do not carry
+                const uint32_t s01 = p01 + __shfl_xor_sync(0xFFFFFFFFu, p01, 1);
+                const uint32_t s23 = p23 + __shfl_xor_sync(0xFFFFFFFFu, p23, 1);
+                if (bin < kBins && (lq & 1) == 0) {
+                    const int cc = lq >> 1;
+                    const uint32_t c[4] = {s01 & 0xFFFFu, s01 >> 16, s23 & 0xFFFFu, s23 >> 16};
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int e = (b * kCT + cc) * kBins + bin;
+                        asm volatile("st.shared.u16 [%0], %1;" ::"r"(staging + 2 * e),
+                                     "h"((uint16_t)c[b])
+                                     : "memory");
+                    }
                 }
             }
         }
@@ -551,6 +549,57 @@ inline bool build_tab(TileTab* tab) {
         const int h = G::halo(qx), lo_x = h + 1, hi_x = h + G::span(qx);  // counted columns
         int home[32];
         auto cell = [&](int x) { return (((x - 1) + 1) * 8 - 1) / G::kInt - qx * G::kCT; };
+        if (G::kQ == 2) {
+            // quadrant (4 cells of ~25 px, <= 8 lanes each): OCTET slots -- pixel (l, k) of
+            // tile cell c counts into slot 8 c + (l & 7): conflict-free atomics (a cell's
+            // lanes are <= 8 consecutive lanes), each cell's slots two 16-B quads
+            int first[4], last[4];
+            for (int c = 0; c < 4; ++c) { first[c] = 99; last[c] = -1; }
+            for (int l = 0; l < 32; ++l)
+                for (int k = 0; k < 4; ++k) {
+                    const int x = G::bx(qx) + 4 * l + k;
+                    uint8_t sl = 0xFF;
+                    if (x >= lo_x && x <= hi_x) {
+                        const int c = cell(x);
+                        sl = (uint8_t)(8 * c + (l & 7));
+                        first[c] = first[c] < l ? first[c] : l;
+                        last[c] = last[c] > l ? last[c] : l;
+                    }
+                    tab->slot[qx][l][k] = sl;
+                }
+            for (int c = 0; c < 4; ++c) {
+                if (last[c] < 0 || last[c] - first[c] > 7) return false;
+                tab->lo[qx][c] = (uint8_t)(8 * c);
+                tab->hi[qx][c] = (uint8_t)(8 * c + 8);
+            }
+            continue;
+        }
+        if (G::kP == 1 && G::kQ == 1) {
+            // one crop, cells <= 13 px (<= 4 lanes): QUAD slots -- pixel (l, k) of cell c counts
+            // into slot 4 c + (l & 3); the lanes of one cell are <= 4 consecutive lanes, so their
+            // (l & 3) differ and the atomics stay conflict-free with no spill case, and each
+            // cell's 4 slots are one 16-B quad for the epilogue (as the 128-px kernel)
+            int first[8], last[8];
+            for (int c = 0; c < 8; ++c) { first[c] = 99; last[c] = -1; }
+            for (int l = 0; l < 32; ++l)
+                for (int k = 0; k < 4; ++k) {
+                    const int x = G::bx(qx) + 4 * l + k;
+                    uint8_t sl = 0xFF;
+                    if (x >= lo_x && x <= hi_x) {
+                        const int c = cell(x);
+                        sl = (uint8_t)(4 * c + (l & 3));
+                        first[c] = first[c] < l ? first[c] : l;
+                        last[c] = last[c] > l ? last[c] : l;
+                    }
+                    tab->slot[qx][l][k] = sl;
+                }
+            for (int c = 0; c < 8; ++c) {
+                if (last[c] < 0 || last[c] - first[c] > 3) return false;
+                tab->lo[qx][c] = (uint8_t)(4 * c);
+                tab->hi[qx][c] = (uint8_t)(4 * c + 4);
+            }
+            continue;
+        }
         for (int l = 0; l < 32; ++l) {
             const int li = l % G::kLanesPerCrop;
             // home = the cell holding most of the lane's counted pixels (ties: the lower):
