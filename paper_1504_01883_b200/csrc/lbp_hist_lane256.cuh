@@ -125,7 +125,7 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int x = 4 * lane + k;
         const bool inner = (x != 0) && (x != kTile - 1);  // the 1-px ROI border has no code
         const int cx = inner ? (8 * x - 1) / (kTile - 2) : (lane >> 2);
-        colk[k] = (cx == (lane >> 2)) ? lane : 4 * cx;  // spill-over -> next cell's lane
+        colk[k] = 4 * cx + (lane & 3);  // the cell's quad, position lane & 3 (lbp_hist_lane59.cuh)
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
     }
     // start values (all of TL, T, TR set) and dummy-bin addresses per pixel pair

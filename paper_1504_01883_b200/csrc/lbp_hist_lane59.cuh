@@ -449,7 +449,10 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int x = 4 * lane + k;
         const bool inner = (x != 0) && (x != kTile - 1);  // the 1-px ROI border has no code
         const int cx = inner ? (8 * x - 1) / (kTile - 2) : (lane >> 2);
-        const int col = (cx == (lane >> 2)) ? lane : 4 * cx;  // spill-over -> next cell's lane
+        // the cell's quad of slots 4 cx .. 4 cx + 3, position lane & 3: for one pixel index k
+        // a cell (<= 16 px) spans <= 4 consecutive lanes, so a spill-over pixel never shares a
+        // slot -- a bank -- with another lane's pixel of the same atomic
+        const int col = 4 * cx + (lane & 3);
         colb[k] = opaque(hist0 + (uint32_t)(((warp >> 2) * kBinsAlloc * 32 + col) * 4));
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
     }
