@@ -14,11 +14,10 @@
 //    final at the end of the tile: no cross-tile merge.
 // Boxes start 16-B aligned (TMA); a quadrant's box starts at its halo column rounded down to
 // 16 px, so its counted pixels begin o = 0..15 columns in.  Which counter lane ("slot") each
-// (lane, pixel) adds to, and which lanes hold each cell, is a host-built table (TileTab):
-// pixels count into their own lane's word unless they lie in the cell of a neighbour lane
-// (cells are >= 7 px wide, so a lane's 4 pixels span at most 2 cells), keeping the shared
-// atomics conflict-free except for those spill pixels.  The epilogue sums the home lanes of
-// each cell (bytes = 4 cell rows, summed as 16-bit pairs) and stores the u16 counts.
+// (lane, pixel) adds to is a host-built table (TileTab, build_tab): the cell's slot group at
+// position lane & (m - 1) -- conflict-free shared atomics -- and the epilogue reads each cell's
+// 2 / 4 / 8 slots as one 8-B pair / one or two 16-B quads (bytes = 4 cell rows) and stages u16
+// counts.
 #pragma once
 #include "lbp_hist_lane59.cuh"
 
@@ -91,7 +90,6 @@ struct Geo {
 // host-built lane tables of one tile column position qx (see the header)
 struct TileTab {
     uint8_t slot[2][32][4];  // [qx][lane][pixel k]: counter lane, 0xFF = not counted
-    uint8_t lo[2][8], hi[2][8];  // [qx][tile cell column]: home lanes [lo, hi) (crop A)
 };
 
 }  // namespace tile
@@ -410,7 +408,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                     if (tr.valid[p]) roi_status[crop_of(t, p)] = LBP_OK;
             }
         }
-        // ---- epilogue: the home lanes of each cell summed, counters re-zeroed, counts staged
+        // ---- epilogue: the slots of each cell summed, counters re-zeroed, counts staged
         // as u16 ([row][cell][bin]), then copied out
         if constexpr (kQ == 1 && kP == 1) {
             // one crop (64 < T <= 128), quad slots (build_tab): this half's quads (bin, cell
@@ -442,7 +440,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                 }
             }
         } else if constexpr (kQ == 1) {
-            // two crops, 2 home lanes per cell (lo = 2 cc: build_tab checks): thread -> cell
+            // two crops, pair slots (build_tab: cell c of crop p = slots 16 p + 2 c, + 1): thread -> cell
             // column cc = bits 0-2, crop p = bit 3, bins bp + 8 k (bp = bits 4-6), counter
             // word g = bit 7 = the half -- affine in k; a quarter-warp's LDS.64 reads 64
             // contiguous B
@@ -538,17 +536,36 @@ namespace tile {
 
 // the lane tables of crop size T (TileTab): pixel (lane, k) of tile column qx is crop column
 // x = bx(qx) + 4 (lane % lanes_per_crop) + k; it is counted iff x is an interior column of the
-// tile (halo < x <= halo + span), into its own lane's word when its cell is the lane's home
-// cell (the cell of most of the lane's counted pixels), else into the neighbour lane whose
-// home it is.  False when the cells are too narrow for that (never for the instantiated T).
+// tile (halo < x <= halo + span), into a SLOT (counter lane) of its cell: for one pixel index k
+// a cell of <= 4 m px spans <= m consecutive lanes, so slot m c + (lane & (m - 1)) never puts
+// two lanes of one atomic on the same bank, and a cell's m slots are contiguous words for the
+// epilogue -- m = 2 (two 64-px crops: 16 slots each), 4 (one crop of <= 128 px), 8 (200-px
+// quadrants: 4 cells).  False when the cells are too wide for that (never for the
+// instantiated T).
 template <int T>
 inline bool build_tab(TileTab* tab) {
     using G = Geo<T>;
     *tab = TileTab{};
     for (int qx = 0; qx < G::kQ; ++qx) {
         const int h = G::halo(qx), lo_x = h + 1, hi_x = h + G::span(qx);  // counted columns
-        int home[32];
         auto cell = [&](int x) { return (((x - 1) + 1) * 8 - 1) / G::kInt - qx * G::kCT; };
+        if (G::kP == 2) {
+            // two crops (cells <= 8 px): PAIR slots -- pixel (l, k) of cell c of crop p counts
+            // into slot 16 p + 2 c + (l & 1): for one pixel index k a cell spans <= 2
+            // consecutive lanes, so the atomics are conflict-free, and each cell's two slots
+            // are the 8-B pair the epilogue reads
+            for (int l = 0; l < 32; ++l) {
+                const int li = l % G::kLanesPerCrop, base = l - li;
+                for (int k = 0; k < 4; ++k) {
+                    const int x = G::bx(qx) + 4 * li + k;
+                    uint8_t sl = 0xFF;
+                    if (x >= lo_x && x <= hi_x) sl = (uint8_t)(base + 2 * cell(x) + (l & 1));
+                    tab->slot[qx][l][k] = sl;
+                }
+            }
+            if (G::kInt / 8 + 1 > 8) return false;  // pair slots need cells of <= 8 px
+            continue;
+        }
         if (G::kQ == 2) {
             // quadrant (4 cells of ~25 px, <= 8 lanes each): OCTET slots -- pixel (l, k) of
             // tile cell c counts into slot 8 c + (l & 7): conflict-free atomics (a cell's
@@ -569,8 +586,6 @@ inline bool build_tab(TileTab* tab) {
                 }
             for (int c = 0; c < 4; ++c) {
                 if (last[c] < 0 || last[c] - first[c] > 7) return false;
-                tab->lo[qx][c] = (uint8_t)(8 * c);
-                tab->hi[qx][c] = (uint8_t)(8 * c + 8);
             }
             continue;
         }
@@ -595,61 +610,10 @@ inline bool build_tab(TileTab* tab) {
                 }
             for (int c = 0; c < 8; ++c) {
                 if (last[c] < 0 || last[c] - first[c] > 3) return false;
-                tab->lo[qx][c] = (uint8_t)(4 * c);
-                tab->hi[qx][c] = (uint8_t)(4 * c + 4);
             }
             continue;
         }
-        for (int l = 0; l < 32; ++l) {
-            const int li = l % G::kLanesPerCrop;
-            // home = the cell holding most of the lane's counted pixels (ties: the lower):
-            // the fewest spill pixels, each of which costs a 2-way conflict in its atomic
-            home[l] = -1;
-            int best = 0;
-            for (int k = 0; k < 4; ++k) {
-                const int x = G::bx(qx) + 4 * li + k;
-                if (x < lo_x || x > hi_x) continue;
-                int cnt = 0;
-                for (int k2 = 0; k2 < 4; ++k2) {
-                    const int x2 = G::bx(qx) + 4 * li + k2;
-                    cnt += (x2 >= lo_x && x2 <= hi_x && cell(x2) == cell(x));
-                }
-                if (cnt > best) { best = cnt; home[l] = cell(x); }
-            }
-        }
-        for (int c = 0; c < G::kCT; ++c) {
-            tab->lo[qx][c] = 0xFF;
-            tab->hi[qx][c] = 0;
-        }
-        for (int l = 0; l < G::kLanesPerCrop; ++l) {
-            if (home[l] < 0) continue;
-            const int c = home[l];
-            if (tab->lo[qx][c] == 0xFF) tab->lo[qx][c] = (uint8_t)l;
-            if (tab->hi[qx][c] != 0 && tab->hi[qx][c] != l) return false;  // not contiguous
-            tab->hi[qx][c] = (uint8_t)(l + 1);
-        }
-        for (int c = 0; c < G::kCT; ++c) {
-            if (tab->lo[qx][c] == 0xFF) return false;
-            // the two-crop epilogue reads the home lanes of cell c as one 8-B pair at 2 c
-            if (G::kP == 2 && (tab->lo[qx][c] != 2 * c || tab->hi[qx][c] != 2 * c + 2))
-                return false;
-        }
-        for (int l = 0; l < 32; ++l) {
-            const int li = l % G::kLanesPerCrop, base = l - li;
-            for (int k = 0; k < 4; ++k) {
-                const int x = G::bx(qx) + 4 * li + k;
-                uint8_t sl = 0xFF;
-                if (x >= lo_x && x <= hi_x) {
-                    const int c = cell(x);
-                    if (c == home[l]) sl = (uint8_t)l;
-                    else if (li > 0 && home[l - 1] == c) sl = (uint8_t)(l - 1);
-                    else if (li + 1 < G::kLanesPerCrop && home[l + 1] == c) sl = (uint8_t)(l + 1);
-                    else return false;
-                    (void)base;
-                }
-                tab->slot[qx][l][k] = sl;
-            }
-        }
+        return false;  // (no slot scheme for this geometry)
     }
     return true;
 }
