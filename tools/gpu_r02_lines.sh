@@ -22,6 +22,7 @@ run config3_depth --source depth --skip-cpu --e2e-steps 1
 run config3_bins256 --bins 256 --skip-cpu --e2e-steps 1
 run config4 --workload config4 --steps 10 --warmup 3 --skip-cpu --e2e-steps 1
 run tile64 --workload tile64 --steps 20 --warmup 5
+run tile100 --workload tile100 --steps 20 --warmup 5
 run tile200 --workload tile200 --steps 10 --warmup 3
 run config1 --workload config1
 run config2 --workload config2
