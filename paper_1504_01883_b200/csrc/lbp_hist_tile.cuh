@@ -407,6 +407,10 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                 for (int p = 0; p < kP; ++p)
                     if (tr.valid[p]) roi_status[crop_of(t, p)] = LBP_OK;
             }
+        } else if (leader) {
+            // the half that released first: retire its own ROI copies too, so that they can
+            // never land after the next tile's copies into the same slot
+            asm volatile("cp.async.wait_all;" ::: "memory");
         }
         // ---- epilogue: the slots of each cell summed, counters re-zeroed, counts staged
         // as u16 ([row][cell][bin]), then copied out
