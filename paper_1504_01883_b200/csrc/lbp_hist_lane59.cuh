@@ -413,16 +413,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     // the dependent launch (the scorer) may be scheduled now: its CTAs take SMs as these
     // CTAs exit, run their prologue, and wait for this grid's completion
     launch_dependents();
-    // ---- one-time setup: LUTs, zero counters, barriers, first three positions
-    for (int i = tid; i < kLutBytes; i += kThreads) {
-        const int code = (i >> 7) * 4 + (i & 3);
-        smem[kLutOff + i] = code < 256 ? kUniformLutDev.v[code] : (uint8_t)kBins;  // row 64: dummy
-    }
-    if (tid < 256) smem[kPlainLutOff + tid] = kUniformLutDev.v[tid];
-    for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
-        st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
-    if (SUB && gtid < 4) st_shared_u32(slack + 4 * gtid, 0u);
-    if (SUB && tid < kStages) st_shared_u32(rel0 + 4 * tid, 0u);
+    // ---- one-time setup: barriers and the first positions' loads first (their latency
+    // overlaps the table fills), then LUTs and zeroed counters
     if (tid == 0) {
         // the host placed the LUT from the device's reserved shared memory size; a mismatch
         // would misaddress every lookup, so it stops the kernel (LBP_E_CUDA) instead
@@ -439,6 +431,15 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                 prefetch(i, r.x, r.y, r.img);
             }
     }
+    for (int i = tid; i < kLutBytes; i += kThreads) {
+        const int code = (i >> 7) * 4 + (i & 3);
+        smem[kLutOff + i] = code < 256 ? kUniformLutDev.v[code] : (uint8_t)kBins;  // row 64: dummy
+    }
+    if (tid < 256) smem[kPlainLutOff + tid] = kUniformLutDev.v[tid];
+    for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
+        st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
+    if (SUB && gtid < 4) st_shared_u32(slack + 4 * gtid, 0u);
+    if (SUB && tid < kStages) st_shared_u32(rel0 + 4 * tid, 0u);
     __syncthreads();
 
     // ---- per-lane / per-warp constants

@@ -190,7 +190,16 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
     };
 
-    // ---- one-time setup: LUTs, zero counters, barriers, the first kStages positions
+    // ---- one-time setup: barriers and the first kStages positions' loads first (their
+    // latency overlaps the table fills), then LUTs, lane table, zeroed counters
+    if (tid == 0) {
+        if ((smem_u32(smem + kLutOff) & 0xFFFFu) != l59::kLutMod) __trap();
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        prefetch_tensormap(&grey_map);
+        if (HAS_DEPTH) prefetch_tensormap(&depth_map);
+        for (int i = 0; i < kStages; ++i) issue(i, load_tile(i));
+    }
     for (int i = tid; i < l59::kLutBytes; i += G::kThreads) {
         const int code = (i >> 7) * 4 + (i & 3);
         smem[kLutOff + i] = code < 256 ? kUniformLutDev.v[code] : (uint8_t)kBins;
@@ -202,14 +211,6 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     if (tid < kStages) st_shared_u32(tab_s + 512 + 4 * tid, 0u);
     for (int i = gtid; i < G::kHistBytes / 16; i += kGT)
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
-    if (tid == 0) {
-        if ((smem_u32(smem + kLutOff) & 0xFFFFu) != l59::kLutMod) __trap();
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-        prefetch_tensormap(&grey_map);
-        if (HAS_DEPTH) prefetch_tensormap(&depth_map);
-        for (int i = 0; i < kStages; ++i) issue(i, load_tile(i));
-    }
     __syncthreads();
 
     // ---- per-thread constants
