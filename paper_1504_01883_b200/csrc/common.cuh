@@ -44,6 +44,26 @@ static_assert(kUniformLut.v[0] == 0 && kUniformLut.v[255] == 57 && kUniformLut.v
 // device copy (constant bank); kernels stage it into shared memory
 static __constant__ BinLut kUniformLutDev = make_uniform_lut();
 
+// Launch with programmatic stream serialization: the kernel's CTAs may be scheduled before
+// the previous kernel on the stream completes (once that kernel has run launch_dependents),
+// so the kernel must call grid_dependency_wait() before it touches memory the previous kernel
+// writes or reads.  Without a triggering predecessor this is an ordinary launch.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, int smem,
+                              cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(block, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+
 // Depth-window predicate parameters: valid(d) <=> d != 0 && dmin <= d <= dmax
 //   <=> (uint32)(d - lo) <= span with lo = max(dmin, 1), span = dmax - lo,
 // and nothing is valid when dmax < lo (i.e. dmax == 0): `none_valid`.

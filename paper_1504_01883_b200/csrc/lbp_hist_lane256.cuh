@@ -104,6 +104,8 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
     };
 
+    // the dependent launch (the scorer) may be scheduled now (see lbp_hist_lane59.cuh)
+    launch_dependents();
     // ---- one-time setup: identity LUT (generic path), zero counters, barriers, first stages
     if (tid < 256) smem[kLutOff + tid] = (uint8_t)tid;
     for (int i = gtid; i < kHistBytes / 16; i += kGroupThreads)
@@ -113,8 +115,12 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         fence_mbar_init();
         prefetch_tensormap(&grey_map);
         if (HAS_DEPTH) prefetch_tensormap(&depth_map);
+        grid_dependency_wait();
         for (int i = 0; i < kStages; ++i) issue(i, 3);
     }
+    // programmatic dependent launch: the setup above may overlap the tail of the previous
+    // kernel on the stream; inputs and outputs are touched only after it has completed
+    grid_dependency_wait();
     __syncthreads();
 
     // ---- per-lane / per-warp constants
@@ -334,10 +340,8 @@ inline cudaError_t launch_lbp_hist_lane256(const uint8_t* grey, const uint16_t* 
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, l256::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int grid = std::max(1, std::min(sms, n_rois));
-    kern<<<grid, l256::kThreads, l256::kSmemBytes, stream>>>(gm, dm, grey, depth, geom, rois,
-                                                            n_rois, win, desc, desc_stride,
-                                                            roi_status);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, l256::kThreads, l256::kSmemBytes, stream, gm, dm, grey, depth,
+                      geom, rois, n_rois, win, desc, desc_stride, roi_status);
 }
 
 }  // namespace lbpf

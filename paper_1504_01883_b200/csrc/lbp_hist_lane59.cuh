@@ -423,6 +423,7 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         fence_mbar_init();
         prefetch_tensormap(&grey_map);
         if (HAS_DEPTH) prefetch_tensormap(&depth_map);
+        grid_dependency_wait();  // (see below)
         for (int i = 0; i < kStages; ++i)
             if (i < n_pos) issue(i, rois[crop_of(i)]);
         for (int i = kStages; i < 2 * kStages; ++i)
@@ -440,6 +441,10 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
     if (SUB && gtid < 4) st_shared_u32(slack + 4 * gtid, 0u);
     if (SUB && tid < kStages) st_shared_u32(rel0 + 4 * tid, 0u);
+    // programmatic dependent launch: everything above may overlap the tail of the previous
+    // kernel on the stream (e.g. the scorer of the previous batch); its inputs and the outputs
+    // it reads (the descriptor rows) are touched only after it has completed
+    grid_dependency_wait();
     __syncthreads();
 
     // ---- per-lane / per-warp constants
@@ -977,10 +982,8 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     if (gather) gd = *gather;
     U8Out uo{};
     if (u8out) uo = *u8out;
-    kern<<<grid, l59::kThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win,
-                                                 desc, desc_stride, roi_status, lut_off, gd,
-                                                 glabels, uo);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, l59::kThreads, smem, stream, gm, dm, grey, depth, geom, rois,
+                      n_rois, win, desc, desc_stride, roi_status, lut_off, gd, glabels, uo);
 }
 
 }  // namespace lbpf

@@ -190,6 +190,8 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
     };
 
+    // the dependent launch (the scorer) may be scheduled now (see lbp_hist_lane59.cuh)
+    launch_dependents();
     // ---- one-time setup: barriers and the first kStages positions' loads first (their
     // latency overlaps the table fills), then LUTs, lane table, zeroed counters
     if (tid == 0) {
@@ -198,6 +200,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         fence_mbar_init();
         prefetch_tensormap(&grey_map);
         if (HAS_DEPTH) prefetch_tensormap(&depth_map);
+        grid_dependency_wait();  // (see below)
         for (int i = 0; i < kStages; ++i) issue(i, load_tile(i));
     }
     for (int i = tid; i < l59::kLutBytes; i += G::kThreads) {
@@ -211,6 +214,9 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     if (tid < kStages) st_shared_u32(tab_s + 512 + 4 * tid, 0u);
     for (int i = gtid; i < G::kHistBytes / 16; i += kGT)
         st_shared_u32x4(hist0 + i * 16, make_uint4(0, 0, 0, 0));
+    // programmatic dependent launch: the setup above may overlap the tail of the previous
+    // kernel on the stream; inputs and outputs are touched only after it has completed
+    grid_dependency_wait();
     __syncthreads();
 
     // ---- per-thread constants
@@ -677,9 +683,8 @@ inline cudaError_t launch_lbp_hist_tile(const uint8_t* grey, const uint16_t* dep
     const int64_t n_tiles = G::kP == 2 ? ((int64_t)n_rois + 1) / 2
                                        : (int64_t)n_rois * G::kQ * G::kQ;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n_tiles));
-    kern<<<grid, G::kThreads, smem, stream>>>(gm, dm, grey, depth, geom, rois, n_rois, win,
-                                                   desc, desc_stride, roi_status, lut_off, tab);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, G::kThreads, smem, stream, gm, dm, grey, depth, geom, rois,
+                      n_rois, win, desc, desc_stride, roi_status, lut_off, tab);
 }
 
 }  // namespace lbpf

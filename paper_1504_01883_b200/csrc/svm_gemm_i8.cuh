@@ -287,7 +287,10 @@ svm_gemm_i8_kernel(const __grid_constant__ CUtensorMap a_map,
     const bool bad_model = tmem_slot[1] != 0u;
     const int n_tiles = bad_model ? 0 : (n + 2 * kGemmM - 1) / (2 * kGemmM);
     // programmatic dependent launch: the prologue above may overlap the tail of the kernel
-    // that wrote the descriptors; everything below reads them (no-op without PDL)
+    // that wrote the descriptors; everything below reads them (no-op without PDL).  The next
+    // kernel on the stream (the next batch's extraction) may be scheduled from now on: it waits
+    // for this grid's completion before it touches the descriptors.
+    launch_dependents();
     grid_dependency_wait();
 
     if (warp == 0) {

@@ -703,6 +703,8 @@ svm_u8_fixup_kernel(const uint8_t* __restrict__ packed, int64_t pitch,
     __shared__ int wc[kU8F64Threads / 32];
     __shared__ int list[kU8F64Threads];
     __shared__ int count;
+    // (no launch_dependents here: scheduling the next batch's extraction this early measured
+    // ~1 % slower per config4 step, tools/gpu_ab_bench.sh; it launches when this grid ends)
     grid_dependency_wait();  // the labels come from the tensor-core kernel
     for (int64_t base = (int64_t)blockIdx.x * kU8F64Threads; base < n;
          base += (int64_t)gridDim.x * kU8F64Threads) {
