@@ -12,6 +12,10 @@
  *    The caller owns every buffer; the library never allocates, frees or
  *    synchronises.  All work is enqueued on `stream` (a cudaStream_t passed as
  *    void*; NULL = the legacy default stream) and returns immediately.
+ *    Stream order is kept: kernels launched as programmatic dependents (the
+ *    TMA extraction kernels, the tensor-core scorers) may start their setup
+ *    while the previous kernel on the stream runs, but touch no buffer before
+ *    it has completed ("Kernel boundaries of a step").
  *  - Calls are reentrant and thread-safe; the library keeps no mutable global
  *    state (its lookup tables are compile-time constants).
  *  - Host-detectable argument errors return a negative status and enqueue

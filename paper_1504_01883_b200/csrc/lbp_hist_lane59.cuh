@@ -74,8 +74,8 @@ struct Layout {
     // 0x6000 + ...) is (address - 0x6000) | t, one LOP3 / IMAD.HI per half.  The plain LUT and
     // the stage barriers follow it.
     static constexpr int kLutMin = kGroupOff + kGroups * kGroupBytes;
-    // LUT, plain LUT, stage barriers, stage-release counters, align slack
-    static constexpr int kTailBytes = kLutBytes + 256 + kStages * 8 + kStages * 4 + 128;
+    // LUT, plain LUT, stage barriers, stage-release counters, stage fast flags, align slack
+    static constexpr int kTailBytes = kLutBytes + 256 + kStages * 8 + 2 * kStages * 4 + 128;
     // headline: stages 3 x 49,152, groups 3 x 23,040 (counters + staging), LUT >= 216,576;
     // FRAME: stages 3 x 53,248, groups 3 x 15,360, LUT >= 205,824
     static_assert(kStageBytes % 128 == 0 && kGreyBytes % 128 == 0 && kLutMin % 256 == 0,
@@ -375,6 +375,11 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t slack = staging + kDescBytes;
     // per-stage release counts (after the stage barriers): two halves release each position
     const uint32_t rel0 = smem_u32(smem + kBarOff + kStages * 8);
+    // per-stage flag: the position staged there takes the fast path (written by the thread that
+    // issues the stage's loads, before its mbarrier arrive; read after the wait), so only the
+    // threads that issue loads (and, FRAME, every thread: the box offset) read the ROIs
+    const uint32_t fastf = rel0 + kStages * 4;
+    const bool loads_roi = FRAME || leader;
 
     // crop positions of this CTA: position i -> crop blockIdx.x + i * gridDim.x
     const int n_pos = (n_rois > (int)blockIdx.x) ? (n_rois - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -389,7 +394,9 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     auto issue = [&](int i, const lbp_roi_t& r) {
         if (i >= n_pos) return;
         const int s = i % kStages;
-        if (is_fast(r)) {
+        const bool fast = is_fast(r);
+        st_shared_u32(fastf + 4 * s, fast ? 1u : 0u);
+        if (fast) {
             uint8_t* st = smem + s * kStageBytes;
             const int gx = FRAME ? (r.x & ~15) : r.x, dx = FRAME ? (r.x & ~7) : r.x;
             mbar_arrive_expect_tx(&bars[s], DEPTH_SRC ? kStageBytes - kGreyBytes
@@ -487,15 +494,15 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
     int32_t pending = -1;  // last crop whose descriptor was bulk-stored
     // the group's next ROI is loaded one crop ahead (its latency hidden by the current crop);
     // with kStages == kGroups it is also the position whose TMA this group issues next
-    lbp_roi_t roi_next = group < n_pos ? rois[crop_of(group)] : lbp_roi_t{};
+    lbp_roi_t roi_next = loads_roi && group < n_pos ? rois[crop_of(group)] : lbp_roi_t{};
     for (int i = group; i < n_pos; i += kGroups) {
         const int32_t n = crop_of(i);
-        const lbp_roi_t roi = roi_next;
-        if (i + kGroups < n_pos) roi_next = rois[crop_of(i + kGroups)];
+        lbp_roi_t roi = roi_next;
+        if (loads_roi && i + kGroups < n_pos) roi_next = rois[crop_of(i + kGroups)];
         // position i + kStages: its TMA is issued when this crop releases stage s
         lbp_roi_t roi_fill{};
         if constexpr (kStages == kGroups) roi_fill = roi_next;
-        else if (i + kStages < n_pos) roi_fill = rois[crop_of(i + kStages)];
+        else if (loads_roi && i + kStages < n_pos) roi_fill = rois[crop_of(i + kStages)];
         // the box of position i + 6, prefetched to L2 when this crop releases its stage (read
         // now by the releasing threads, used after the rows)
         int32_t pf_x = 0, pf_y = 0, pf_img = 0;
@@ -507,7 +514,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
         const uint32_t par = (uint32_t)(i / kGroups) & 1u;
         const uint32_t exc_cnt = slack + 4 * par;  // U8: the crop's exception count
-        if (!is_fast(roi)) {
+        if (ld_shared_u32(fastf + 4 * s) == 0u) {
+            if (!loads_roi) roi = rois[n];
             // stage s was never filled: release it at once -- but only once every thread of
             // the group has passed its wait on this position's phase (a plain arrive for
             // position i + 3 completes the NEXT phase at once, and a thread still polling the
