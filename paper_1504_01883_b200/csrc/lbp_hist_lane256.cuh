@@ -40,7 +40,7 @@ constexpr int kDescBytes = 64 * kBins * 2;                   // 32,768 (staged o
 constexpr int kGroupOff = kStages * kStageBytes;             // 98,304
 constexpr int kLutOff = kGroupOff + kGroups * kHistBytes;    // 229,888: identity LUT (generic)
 constexpr int kBarOff = kLutOff + 256;
-constexpr int kSmemBytes = kBarOff + kStages * 8 + 128;      // + 128-B alignment slack
+constexpr int kSmemBytes = kBarOff + kStages * 12 + 128;     // barriers, fast flags, 128-B slack
 static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 static_assert(kDescBytes <= kRows * 128, "staging fits over the first cell-row group");
 static_assert(kStages == kGroups, "stage == group");
@@ -83,6 +83,9 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t hist0 = stages0 + kGroupOff + group * kHistBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
     const uint32_t bar_id = 1 + group;
+    // per-stage flag: the position staged there takes the fast path (written by the issuing
+    // thread before its mbarrier arrive, read after the wait: lbp_hist_lane59.cuh)
+    const uint32_t fastf = smem_u32(smem + kBarOff + kStages * 8);
 
     const int n_pos = (n_rois > (int)blockIdx.x) ? (n_rois - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     auto crop_of = [&](int i) -> int32_t { return (int32_t)blockIdx.x + i * (int32_t)gridDim.x; };
@@ -91,7 +94,9 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         if (i >= n_pos) return;
         const int s = i % kStages;
         const lbp_roi_t r = rois[crop_of(i)];
-        if (roi_is_fast(r, geom)) {
+        const bool fast = roi_is_fast(r, geom);
+        if (part & 1) st_shared_u32(fastf + 4 * s, fast ? 1u : 0u);
+        if (fast) {
             uint8_t* st = smem + s * kStageBytes;
             if (part & 1) {
                 mbar_arrive_expect_tx(&bars[s], HAS_DEPTH ? kStageBytes : kGreyBytes);
@@ -155,15 +160,12 @@ lbp_hist_lane256_kernel(const __grid_constant__ CUtensorMap grey_map,
         }
     };
 
-    // the group's next ROI is loaded one crop ahead (its latency hidden by the current crop)
-    lbp_roi_t roi_next = group < n_pos ? rois[crop_of(group)] : lbp_roi_t{};
     for (int i = group; i < n_pos; i += kGroups) {
         const int32_t n = crop_of(i);
-        const lbp_roi_t roi = roi_next;
-        if (i + kGroups < n_pos) roi_next = rois[crop_of(i + kGroups)];
         const int s = i % kStages;
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
-        if (!roi_is_fast(roi, geom)) {
+        if (ld_shared_u32(fastf + 4 * s) == 0u) {
+            const lbp_roi_t roi = rois[n];
             // stage s was never filled: release it, once every thread of the group has
             // passed its wait on this phase (lbp_hist_lane59.cuh: an earlier plain arrive
             // completes the next phase and a late thread waits on the one after it)
