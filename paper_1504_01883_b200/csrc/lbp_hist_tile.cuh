@@ -78,7 +78,7 @@ struct Geo {
     static constexpr int kLutMin = up(kGroupOff + kGroups * kGroupBytes, 256);
     // LUT, plain LUT, stage barriers, the lane tables (TileTab, copied to shared memory: the
     // lane-indexed reads of the kernel-parameter copy serialise in the constant cache), slack
-    static constexpr int kTailBytes = l59::kLutBytes + 256 + kStages * 8 + 512 + kStages * 4 + 128;
+    static constexpr int kTailBytes = l59::kLutBytes + 256 + kStages * 8 + 512 + kStages * 8 + 128;
     // rows of one warp: a cell row
     static constexpr int kMaxRows = (kInt + 7) / 8;
     static constexpr int kMinRows = kInt / 8;  // every warp has at least these rows
@@ -130,6 +130,10 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     const uint32_t sub_bar = 1 + kGroups + 2 * group + sub;  // after the group barriers
     const bool leader = SUB ? stid == 0 : gtid == 0;
     const uint32_t rel0 = tab_s + 512;  // per-stage release counts
+    // per-stage flag: the tile staged there takes the fast path (written by the issuing thread
+    // before its mbarrier arrive, read after the wait: lbp_hist_lane59.cuh), so the ROIs are
+    // read only by the issuing leaders and on the generic path
+    const uint32_t fastf = rel0 + kStages * 4;
     const uint32_t bar_id = 1 + group;
 
     // tiles: crop pairs (kP = 2: crops 2t, 2t+1) or quadrants (kQ = 2: crop t / 4, q = t % 4)
@@ -167,7 +171,9 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     auto issue = [&](int i, const TileRois& tr) {
         if (i >= n_pos) return;
         const int s = i % kStages;
-        if (!tile_fast(tr)) {
+        const bool fast = tile_fast(tr);
+        st_shared_u32(fastf + 4 * s, fast ? 1u : 0u);
+        if (!fast) {
             mbar_arrive(&bars[s]);
             return;
         }
@@ -234,11 +240,11 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
     const bool none = HAS_DEPTH && win.none_valid;
 
     bool pending = false;  // leader: a bulk store of the staging is in flight
-    TileRois tr_next = group < n_pos ? load_tile(group) : TileRois{};
     for (int i = group; i < n_pos; i += kGroups) {
         const int64_t t = tile_of(i);
-        const TileRois tr = tr_next;
-        if (i + kGroups < n_pos) tr_next = load_tile(i + kGroups);
+        bool valid[kP];
+#pragma unroll
+        for (int p = 0; p < kP; ++p) valid[p] = crop_of(t, p) < n_rois;
         // the ROIs of position i + kStages (loaded when this tile releases stage s): fetched
         // now by cp.async into the group's slot, so no registers hold them through the rows
         if (leader && i + kStages < n_pos) {  // each leader into its own slot
@@ -275,7 +281,8 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         const int q = kQ == 2 ? (int)(t % kTilesPerCrop) : 0;
         const int qx = q & 1, qy = q >> 1;
         mbar_wait(&bars[s], (uint32_t)(i / kStages) & 1u);
-        if (!tile_fast(tr)) {
+        if (ld_shared_u32(fastf + 4 * s) == 0u) {
+            const TileRois tr = load_tile(i);
             // release the unfilled stage only after every thread passed its wait on this
             // phase (see lbp_hist_lane59.cuh: an early plain arrive completes the next phase)
             named_barrier_sync(bar_id, kGT);
@@ -311,7 +318,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
         uint32_t colb[4], mult[4];
         // the lane's 4 slots (TileTab::slot[qx][lane][0..3]) in one conflict-free LDS
         const uint32_t slots4 = ld_shared_u32(tab_s + (uint32_t)(qx * 128 + lane * 4));
-        const bool crop_ok = p_lane == 0 ? tr.valid[0] : tr.valid[kP - 1];
+        const bool crop_ok = p_lane == 0 ? valid[0] : valid[kP - 1];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const uint32_t sl = (slots4 >> (8 * k)) & 0xFFu;
@@ -412,7 +419,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
             if (roi_status && q == 0) {
 #pragma unroll
                 for (int p = 0; p < kP; ++p)
-                    if (tr.valid[p]) roi_status[crop_of(t, p)] = LBP_OK;
+                    if (valid[p]) roi_status[crop_of(t, p)] = LBP_OK;
             }
         } else if (leader) {
             // the half that released first: retire its own ROI copies too, so that they can
@@ -521,7 +528,7 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                 constexpr int kHalf = kDim / 2;
 #pragma unroll
                 for (int p = 0; p < kP; ++p)
-                    if (p == 0 ? tr.valid[0] : tr.valid[kP - 1])
+                    if (p == 0 ? valid[0] : valid[kP - 1])
                         bulk_store_s2g(desc + crop_of(t, p) * desc_stride + sub * kHalf,
                                        staging + (p * G::kRowPad + sub * kHalf) * 2, kHalf * 2);
                 pending = true;
