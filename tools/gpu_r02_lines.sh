@@ -4,7 +4,7 @@
 #   /usr/local/graft/bin/gpurun --timeout 3000 -- bash tools/gpu_r02_lines.sh TAG
 cd "$GRAFT_REPO_ROOT" || exit 1
 T=${1:-r02_lines}
-PART=${2:-lines}   # lines | ncu1 | ncu2  (one gpurun call each: gpurun_out/ comes back <= 64 MiB)
+PART=${2:-lines}   # lines | ncu1 | ncu2 | ncu3  (one gpurun call each: gpurun_out/ comes back <= 64 MiB)
 O=gpurun_out/$T
 mkdir -p $O/lines $O/ncu
 python __graft_entry__.py build > $O/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
@@ -48,4 +48,8 @@ if [ "$PART" = ncu2 ]; then
 full tile64 lbp_hist_tile --workload tile64
 full tile200 lbp_hist_tile --workload tile200
 full svm_u8_config4 svm_gemm_u8 --workload config4 --crops 16384
+fi
+if [ "$PART" = ncu3 ]; then
+full tile100 lbp_hist_tile --workload tile100
+full lane59_config3_u8 lbp_hist_lane59 --format u8
 fi
