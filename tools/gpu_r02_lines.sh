@@ -4,7 +4,7 @@
 #   /usr/local/graft/bin/gpurun --timeout 3000 -- bash tools/gpu_r02_lines.sh TAG
 cd "$GRAFT_REPO_ROOT" || exit 1
 T=${1:-r02_lines}
-PART=${2:-lines}   # lines | ncu1 | ncu2 | ncu3  (one gpurun call each: gpurun_out/ comes back <= 64 MiB)
+PART=${2:-lines}   # lines | ncu:NAME (see the case list below)  (one gpurun call each: gpurun_out/ comes back <= 64 MiB)
 O=gpurun_out/$T
 mkdir -p $O/lines $O/ncu
 python __graft_entry__.py build > $O/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
@@ -39,17 +39,14 @@ full() {  # name, kernel regex, bench args...
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o $O/ncu/$name \
     python bench.py --steps 3 --warmup 3 --skip-cpu --e2e-steps 1 "$@" > $O/ncu/$name.log 2>&1; echo "ncu $name rc=$?"
 }
-if [ "$PART" = ncu1 ]; then
-full lane59_config3 lbp_hist_lane59
-full svm_gemm_config3 svm_gemm_kernel
-full lane59_fused lbp_hist_lane59 --source fused
-fi
-if [ "$PART" = ncu2 ]; then
-full tile64 lbp_hist_tile --workload tile64
-full tile200 lbp_hist_tile --workload tile200
-full svm_u8_config4 svm_gemm_u8 --workload config4 --crops 16384
-fi
-if [ "$PART" = ncu3 ]; then
-full tile100 lbp_hist_tile --workload tile100
-full lane59_config3_u8 lbp_hist_lane59 --format u8
-fi
+# one capture per call keeps gpurun_out/ under gpurun's 64 MiB copy-back limit: PART=ncu:NAME
+case "$PART" in
+  ncu:lane59_config3) full lane59_config3 lbp_hist_lane59 ;;
+  ncu:svm_gemm_config3) full svm_gemm_config3 svm_gemm_kernel ;;
+  ncu:lane59_fused) full lane59_fused lbp_hist_lane59 --source fused ;;
+  ncu:tile64) full tile64 lbp_hist_tile --workload tile64 ;;
+  ncu:tile100) full tile100 lbp_hist_tile --workload tile100 ;;
+  ncu:tile200) full tile200 lbp_hist_tile --workload tile200 ;;
+  ncu:svm_u8_config4) full svm_u8_config4 svm_gemm_u8 --workload config4 --crops 16384 ;;
+  ncu:lane59_config3_u8) full lane59_config3_u8 lbp_hist_lane59 --format u8 ;;
+esac
