@@ -39,12 +39,17 @@ struct Geo {
     static constexpr int kP = T <= 64 ? 2 : 1;         // crops side by side in a tile
     static constexpr int kCT = 8 / kQ;                 // cells per tile axis
     static constexpr int kInt = T - 2;                 // interior pixels per axis
-    // one warp per cell row of the tile: 8-warp groups x 3 (64 px), 4-warp groups x 5 (200 px:
-    // a quadrant's 4 cell rows of 24-25 rows each -- twice the rows per warp of two warps per
-    // cell row, half the per-tile head per crop, one warp per SMSP in each group barrier)
+    // one warp per cell row of the tile: 8-warp groups x 3 with one stage each (64 px), x 2
+    // with two stages each (65-128 px), 4-warp groups x 5 with one stage each (200 px: a
+    // quadrant's 4 cell rows of 24-25 rows each -- twice the rows per warp of two warps per
+    // cell row, half the per-tile head per crop, one warp per SMSP in each group barrier).
+    // A second stage per group hides the refill (the group's next tile is loaded while it
+    // works on the current one): 100 px 0.2055 -> 0.2030 ms per step; at 64 px three
+    // single-stage groups measured faster than two double-buffered ones (0.1174 vs 0.1235 ms);
+    // at 200 px two stages per group do not fit (3 groups x 2: 233,568 B)
     static constexpr int kWarps = kCT;
     static constexpr int kGT = kWarps * 32;
-    static constexpr int kGroups = kQ == 2 ? 5 : 3;
+    static constexpr int kGroups = kQ == 2 ? 5 : kP == 2 ? 3 : 2;
     static constexpr int kThreads = kGroups * kGT;
     static constexpr int kG = kCT / 4 > 0 ? kCT / 4 : 1;  // counter words per (bin, lane)
     // halo column (= crop column of the tile's first interior pixel - 1) and aligned box start
@@ -61,10 +66,12 @@ struct Geo {
     static constexpr int kCropBytes = up(kGreyRegion + kBH * 2 * kDW, 128);
     static constexpr int kBoxBytesGrey = kBH * kGW, kBoxBytesDepth = kBH * 2 * kDW;
     static constexpr int kStageBytes = kP * kCropBytes;
-    // one stage per group: a group's positions i, i + 3, ... always reuse ITS stage, so the
-    // stage barrier's phases are consumed in order (with more stages than groups a fast group
-    // could wait on a phase two ahead, which mbarrier parity cannot tell from the last one)
-    static constexpr int kStages = kGroups;
+    // kSPG stages per group: position i takes stage i % kStages and group i % kGroups, so a
+    // group's positions always reuse ITS stages in turn and each stage barrier's phases are
+    // consumed in order (stages shared between groups would let a fast group wait on a phase
+    // two ahead, which mbarrier parity cannot tell from the last one)
+    static constexpr int kSPG = kQ == 1 && kP == 1 ? 2 : 1;
+    static constexpr int kStages = kGroups * kSPG;
     // staged row pitch (kQ = 1): 16 B more than the row, so the two rows' entries of one cell
     // land in different banks
     static constexpr int kRowPad = 64 * kBins + 8;
