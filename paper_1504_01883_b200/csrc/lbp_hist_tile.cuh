@@ -145,9 +145,18 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
 
     // tiles: crop pairs (kP = 2: crops 2t, 2t+1) or quadrants (kQ = 2: crop t / 4, q = t % 4)
     const int64_t n_tiles = kP == 2 ? ((int64_t)n_rois + 1) / 2 : (int64_t)n_rois * kTilesPerCrop;
-    const int n_pos = (n_tiles > (int64_t)blockIdx.x)
-                          ? (int)((n_tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-    auto tile_of = [&](int i) -> int64_t { return (int64_t)blockIdx.x + (int64_t)i * gridDim.x; };
+    // quadrant tiles (kQ = 2): a CTA takes all four quadrants of its crops at consecutive
+    // positions (four groups at once), so the rows and columns the quadrant boxes share, and
+    // the DRAM sectors their edges share, are read while still in L2 (the four quadrants of a
+    // crop in four CTAs read 1.35x the crop's bytes from DRAM)
+    const int n_pos = kQ == 2
+        ? (n_rois > (int)blockIdx.x ? ((n_rois - 1 - (int)blockIdx.x) / (int)gridDim.x + 1) * 4 : 0)
+        : (n_tiles > (int64_t)blockIdx.x) ? (int)((n_tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    auto tile_of = [&](int i) -> int64_t {
+        if constexpr (kQ == 2)
+            return ((int64_t)blockIdx.x + (int64_t)(i >> 2) * gridDim.x) * 4 + (i & 3);
+        return (int64_t)blockIdx.x + (int64_t)i * gridDim.x;
+    };
     auto crop_of = [&](int64_t t, int p) -> int64_t {
         return kP == 2 ? 2 * t + p : t / kTilesPerCrop;
     };
@@ -694,9 +703,9 @@ inline cudaError_t launch_lbp_hist_tile(const uint8_t* grey, const uint16_t* dep
     if (!lut_placement(G::kLutMin, G::kTailBytes, &lut_off, &smem)) return cudaErrorNotSupported;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    const int64_t n_tiles = G::kP == 2 ? ((int64_t)n_rois + 1) / 2
-                                       : (int64_t)n_rois * G::kQ * G::kQ;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n_tiles));
+    // CTAs: crop pairs (kP = 2), crops (one tile, or all four quadrants of a crop in one CTA)
+    const int64_t n_units = G::kP == 2 ? ((int64_t)n_rois + 1) / 2 : (int64_t)n_rois;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, n_units));
     return launch_pdl(kern, grid, G::kThreads, smem, stream, gm, dm, grey, depth, geom, rois,
                       n_rois, win, desc, desc_stride, roi_status, lut_off, tab);
 }
