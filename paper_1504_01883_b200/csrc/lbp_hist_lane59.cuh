@@ -83,6 +83,25 @@ struct Layout {
     static_assert(kLutMin + kTailBytes <= 227 * 1024, "shared memory");
     static_assert(kDescBytes <= kBinsAlloc * 32 * 4, "FRAME staging fits over one cell-row group");
 };
+// the depth window as the packed words the row loop compares with (both fp16x2 halves, or
+// the high u16 of a word): lo16 / span16 (WINM 0), lo2 / hi2 (WINM 1), mid2 / half2 (WINM 2:
+// |d - mid| <= half), and DINT's clamp bounds lo - 1, lo + 1022 and offset 0x6401 - lo
+struct WinWords {
+    uint32_t lo16, span16, lo2, hi2, mid2, half2, dlo2m1, dhi2, doff2;
+};
+inline WinWords win_words(const DepthWindow& w) {
+    WinWords r;
+    r.lo16 = w.lo << 16;
+    r.span16 = (w.span << 16) | 0xFFFFu;
+    r.lo2 = w.lo * 0x10001u;
+    r.hi2 = (w.lo + w.span) * 0x10001u;
+    r.mid2 = ((2 * w.lo + w.span) / 2) * 0x10001u;
+    r.half2 = (w.span / 2) * 0x10001u;
+    r.dlo2m1 = (w.lo - 1u) * 0x10001u;
+    r.dhi2 = (w.lo + 1022u) * 0x10001u;
+    r.doff2 = ((0x6401u - w.lo) & 0xFFFFu) * 0x10001u;
+    return r;
+}
 }  // namespace l59
 
 // 4 bytes starting s = sel-encoded bytes into the word pair at addr (funnel shift by PRMT)
@@ -327,7 +346,8 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
                        DepthWindow win, uint16_t* __restrict__ desc, int64_t desc_stride,
                        int32_t* __restrict__ roi_status, int32_t lut_off,
                        const __grid_constant__ lbp_gather_dst_t gd,
-                       const int32_t* __restrict__ glabels, const __grid_constant__ U8Out u8o) {
+                       const int32_t* __restrict__ glabels, const __grid_constant__ U8Out u8o,
+                       const __grid_constant__ l59::WinWords ww) {
     constexpr bool GATHER = OUTM == l59::kOutGather;
     constexpr bool U8 = OUTM == l59::kOutU8;
     constexpr bool FUSED = OUTM == l59::kOutFused;
@@ -469,14 +489,12 @@ lbp_hist_lane59_kernel(const __grid_constant__ CUtensorMap grey_map,
         colb[k] = opaque(hist0 + (uint32_t)(((warp >> 2) * kBinsAlloc * 32 + col) * 4));
         mult[k] = opaque((inner && !(HAS_DEPTH && win.none_valid)) ? byte_mult : 0u);
     }
-    const uint32_t lo16 = win.lo << 16;
-    const uint32_t span16 = (win.span << 16) | 0xFFFFu;
-    const uint32_t lo2 = win.lo * 0x10001u, hi2 = (win.lo + win.span) * 0x10001u;  // WINM 1
-    const uint32_t mid2 = ((2 * win.lo + win.span) / 2) * 0x10001u;                 // WINM 2
-    const uint32_t half2 = (win.span / 2) * 0x10001u;
-    // DINT: clamp bounds and the offset to the fp16 integers 1025 + (d' - lo)
-    const uint32_t dlo2m1 = (win.lo - 1u) * 0x10001u, dhi2 = (win.lo + 1022u) * 0x10001u;
-    const uint32_t doff2 = ((0x6401u - win.lo) & 0xFFFFu) * 0x10001u;
+    // depth-window words, computed on the host (WinWords): kernel parameters the row loop
+    // reads as constant-bank operands instead of holding (or recomputing) them in registers
+    const uint32_t lo16 = ww.lo16, span16 = ww.span16;        // WINM 0
+    const uint32_t lo2 = ww.lo2, hi2 = ww.hi2;                // WINM 1
+    const uint32_t mid2 = ww.mid2, half2 = ww.half2;          // WINM 2
+    const uint32_t dlo2m1 = ww.dlo2m1, dhi2 = ww.dhi2, doff2 = ww.doff2;  // DINT
     // LUT address of an offset half t: lutb | t (the LUT sits at 0x6000 mod 2^16)
     const uint32_t lutb = opaque(smem_u32(smem + kLutOff) - kLutMod);
     const uint32_t base2 = opaque((kLutMod + 4u * lane) * 0x10001u);  // 512.0 + 2 lane
@@ -991,7 +1009,8 @@ inline cudaError_t launch_lbp_hist_lane59(const uint8_t* grey, const uint16_t* d
     U8Out uo{};
     if (u8out) uo = *u8out;
     return launch_pdl(kern, grid, l59::kThreads, smem, stream, gm, dm, grey, depth, geom, rois,
-                      n_rois, win, desc, desc_stride, roi_status, lut_off, gd, glabels, uo);
+                      n_rois, win, desc, desc_stride, roi_status, lut_off, gd, glabels, uo,
+                      l59::win_words(win));
 }
 
 }  // namespace lbpf
