@@ -1,6 +1,7 @@
 """Developer tool: phase timestamps of the fp16 SVM kernel (build with
 LBP_NVCC_EXTRA=-DLBP_SVM_TRACE; prints entry / prologue / MMA / epilogue / exit times in us
-of the first and the last cluster of the last of 3 launches at config3 size)."""
+of the first and the last cluster of the last of 3 launches at config3 size).  argv: [step=0:
+1 = each launch follows an extraction of the batch on the stream, as in bench.py's step]."""
 import sys, torch, numpy as np
 sys.path.insert(0, '.')
 import paper_1504_01883_b200 as lb, synthgen
@@ -11,7 +12,10 @@ desc = lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 59)
 W, b = synthgen.svm_weights(100, 3776, seed=1)
 W, b = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
 ws = lb.svm_prepare(W)
+step = len(sys.argv) > 1 and sys.argv[1] == "1"
 for i in range(3):
+    if step:
+        lb.lbp_fused_extract(g, d, r, 600, 1400, 8, 8, 59, out=desc)
     lb.svm_score(desc, W, b, prepared=ws, want_scores=False)
 torch.cuda.synchronize()
 import ctypes
