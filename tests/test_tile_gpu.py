@@ -125,7 +125,7 @@ def test_tile_full_size_sample(lb, T):
 
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("geom", ["frame256_roi100", "tile200_mixed", "tile64_mixed",
-                                  "crops128_bins256_mixed"])
+                                  "tile100_mixed", "crops128_bins256_mixed"])
 def test_generic_positions_repeat_no_hang(lb, geom):
     """Large batches whose ROIs take the generic code path inside the persistent TMA kernels,
     launched repeatedly: a generic position releases its (unfilled) stage with a plain
@@ -140,6 +140,8 @@ def test_generic_positions_repeat_no_hang(lb, geom):
         n, T, S = 2048, 200, 200     # tile kernel, quadrants + generic crops
     elif geom == "tile64_mixed":
         n, T, S = 4096, 64, 64       # tile kernel, crop pairs + generic crops
+    elif geom == "tile100_mixed":
+        n, T, S = 2048, 100, 100     # tile kernel, two stages per group + generic crops
     else:
         n, T, S = 2048, 128, 128     # lane256 kernel (256 bins) + generic crops
     bins = 256 if geom == "crops128_bins256_mixed" else 59
@@ -148,6 +150,10 @@ def test_generic_positions_repeat_no_hang(lb, geom):
         gb = torch.zeros((n, S, (S + 15) // 16 * 16), dtype=torch.uint8, device=dev)
         gb[:, :, :S] = g
         g = gb[:, :, :S]
+    if (2 * S) % 16:  # depth rows to a 16-B multiple too (100 px: 200 -> 208 B)
+        db = torch.zeros((n, S, (S + 7) // 8 * 8), dtype=torch.int16, device=dev)
+        db[:, :, :S] = d.view(torch.int16)
+        d = db[:, :, :S].view(torch.uint16)
     rois = synthgen.full_rois(n, S, S)
     if geom == "frame256_roi100":
         rois[:, 1:] = (37, 45, T, T)
