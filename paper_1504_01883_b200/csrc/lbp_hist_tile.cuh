@@ -493,9 +493,9 @@ lbp_hist_tile_kernel(const __grid_constant__ CUtensorMap grey_map,
                 if (bin == kBins) break;  // dummy bin (masked-out pixels): only re-zeroed
                 const uint32_t sum = w.x + w.y;  // bytewise: each byte <= 2 x 48
 #pragma unroll
-                for (int b = 0; b < 4; ++b)
+                for (int b = 0; b < 4; ++b)  // byte b zero-extended: one PRMT with a zero word
                     asm volatile("st.shared.u16 [%0], %1;" ::"r"(e0 + 2u * (8 * k + b * 8 * kBins)),
-                                 "h"((uint16_t)((sum >> (8 * b)) & 0xFFu))
+                                 "r"(prmt(sum, 0u, 0x4440u | (uint32_t)b))
                                  : "memory");
             }
         } else {
